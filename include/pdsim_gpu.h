@@ -1,0 +1,356 @@
+/* pdsim_gpu.h — C-ABI of the B200 plan-search replay engine.
+ *
+ * This is the drop-in boundary for the reference simulator's hot path:
+ *   SimResult pdsim::run(const Trace&, const DeploymentPlan&,
+ *                        const PerfProfile&, const SchedulerParams&, uint64_t)
+ *     (reference: proj/include/pdsim/sim_engine.hpp:125-127,
+ *                 proj/src/sim_engine.cpp:676-681)
+ * plus the batched candidate x trace-replica search that composes it with the
+ * reference candidate enumerator (proj/src/planner.cpp:582-657) and SLO scoring
+ * (proj/src/sim_engine.cpp:591-607, proj/src/metrics.cpp:171-186).
+ *
+ * Conventions
+ *  - Plain C types only. No allocation crosses the ABI: every output buffer is
+ *    caller-allocated. Device memory is owned by the context.
+ *  - Every entry point returns a status code (PDSIM_OK or PDSIM_ERR_*). The
+ *    error classes mirror the reference exception taxonomy
+ *    (proj/include/pdsim/errors.hpp:25-46): ConfigError -> PDSIM_ERR_CONFIG,
+ *    DomainError -> PDSIM_ERR_DOMAIN. No C++ exception crosses the ABI; the
+ *    message is available from pdsim_gpu_last_error() (per context) or
+ *    pdsim_last_error() (thread-local, for context-free calls).
+ *  - A context is bound to one CUDA device. Calls on distinct contexts may run
+ *    concurrently; calls on one context must be serialized by the caller.
+ */
+#ifndef PDSIM_GPU_H_
+#define PDSIM_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDSIM_ABI_VERSION 1
+
+#define PDSIM_MAX_DEGREES 8     /* profile degree set size */
+#define PDSIM_MAX_BREAKPOINTS 7 /* per piecewise curve; segments = bps + 1 */
+#define PDSIM_MAX_SEGMENTS (PDSIM_MAX_BREAKPOINTS + 1)
+#define PDSIM_MAX_GROUPS 8      /* distinct degrees per phase in a plan */
+#define PDSIM_MAX_WORKERS 64    /* prefill + decode replicas in one plan */
+
+/* Status codes (errors.hpp:25-46 mapping). */
+enum {
+  PDSIM_OK = 0,
+  PDSIM_ERR_CONFIG = 1,   /* pdsim::ConfigError */
+  PDSIM_ERR_DOMAIN = 2,   /* pdsim::DomainError */
+  PDSIM_ERR_CUDA = 3,     /* device / driver failure, or no usable device */
+  PDSIM_ERR_INTERNAL = 4, /* engine invariant or capacity violated */
+  PDSIM_ERR_PARSE = 5     /* pdsim::ParseError (document I/O helpers) */
+};
+
+/* RoutingMode (sim_engine.hpp:37-41). */
+enum {
+  PDSIM_ROUTING_ADAPTIVE = 0,
+  PDSIM_ROUTING_ALWAYS_REMOTE = 1,
+  PDSIM_ROUTING_ALWAYS_LOCAL = 2
+};
+
+/* RouteRationale (coordinator.hpp:27-33). */
+enum {
+  PDSIM_RATIONALE_SLACK_REMOTE = 0,
+  PDSIM_RATIONALE_SLACK_LOCAL = 1,
+  PDSIM_RATIONALE_ARGMIN = 2,
+  PDSIM_RATIONALE_FORCED_REMOTE = 3,
+  PDSIM_RATIONALE_FORCED_LOCAL = 4
+};
+
+/* Per-pair status in a search. */
+enum {
+  PDSIM_PAIR_OK = 0,
+  PDSIM_PAIR_INVALID = 1, /* run() would throw ConfigError (e.g. KV precheck,
+                             sim_engine.cpp:217-231); the candidate is invalid */
+  PDSIM_PAIR_ERROR = 2    /* engine capacity/invariant failure (never expected) */
+};
+
+/* ---- inputs --------------------------------------------------------------- */
+
+/* PiecewiseAlphaBeta (perf_model.hpp:48-74): segment i covers
+ * [bp[i-1], bp[i]); a load exactly on a breakpoint belongs to the right
+ * segment. eval(load) = alpha[i] + beta[i] * load, separately rounded. */
+typedef struct pdsim_curve {
+  int32_t n_breakpoints; /* 0..PDSIM_MAX_BREAKPOINTS */
+  int32_t reserved;
+  double breakpoints[PDSIM_MAX_BREAKPOINTS];
+  double alpha[PDSIM_MAX_SEGMENTS];
+  double beta[PDSIM_MAX_SEGMENTS];
+} pdsim_curve;
+
+/* PerfProfile (perf_model.hpp:76-91). Tables are indexed by the position of a
+ * degree in `degrees` (ascending); kv[src][dst]. */
+typedef struct pdsim_profile {
+  int32_t n_degrees;
+  int32_t degrees[PDSIM_MAX_DEGREES];
+  int32_t reserved;
+  pdsim_curve prefill[PDSIM_MAX_DEGREES];
+  pdsim_curve decode[PDSIM_MAX_DEGREES];
+  pdsim_curve kv[PDSIM_MAX_DEGREES][PDSIM_MAX_DEGREES];
+  int64_t kv_bytes_per_token;
+  int64_t gpu_memory_capacity;
+  double history_weight;
+} pdsim_profile;
+
+/* Trace (workload.hpp:28-62) as a structure of arrays. Round r of session i
+ * is element round_offset[i] + r. Caller-owned, read-only for the call. */
+typedef struct pdsim_trace {
+  int64_t n_sessions;
+  int64_t n_rounds;                 /* == round_offset[n_sessions] */
+  const int64_t* session_id;        /* [n_sessions] */
+  const double* arrival_time;       /* [n_sessions], non-decreasing */
+  const int64_t* round_offset;      /* [n_sessions + 1], round_offset[0] == 0 */
+  const int64_t* incr_input_len;    /* [n_rounds] */
+  const int64_t* decode_len;        /* [n_rounds] */
+  const double* interaction_delay;  /* [n_rounds] */
+  double ttft_thres;                /* SloSpec (workload.hpp:46-50) */
+  double itl_thres;
+} pdsim_trace;
+
+/* DeploymentPlan (planner.hpp:36-53): replica groups in ascending degree
+ * order (std::map iteration order). Worker ids: prefill replicas 0..P-1 in
+ * group order, decode replicas P..P+D-1 (sim_engine.cpp:175-203). */
+typedef struct pdsim_plan {
+  int32_t n_prefill_groups;
+  int32_t n_decode_groups;
+  int32_t prefill_degree[PDSIM_MAX_GROUPS];
+  int32_t prefill_count[PDSIM_MAX_GROUPS];
+  int32_t decode_degree[PDSIM_MAX_GROUPS];
+  int32_t decode_count[PDSIM_MAX_GROUPS];
+} pdsim_plan;
+
+/* SchedulerParams (sim_engine.hpp:46-54). */
+typedef struct pdsim_sched_params {
+  int32_t routing;  /* PDSIM_ROUTING_* */
+  int32_t reorder;  /* bool */
+  double alpha;
+  double beta;
+  int32_t window;
+  int32_t reserved;
+  double stat_window;
+} pdsim_sched_params;
+
+/* ---- outputs -------------------------------------------------------------- */
+
+/* DecisionRecord (sim_engine.hpp:86-94). */
+typedef struct pdsim_decision {
+  double time;
+  int64_t session_id;
+  int32_t round;
+  int32_t worker;
+  int8_t local;
+  int8_t rationale;
+  int8_t has_estimate;
+  int8_t reserved[5];
+  double estimated_cost;
+} pdsim_decision;
+
+/* TtftSample (sim_engine.hpp:56-64). kind: 0 initial, 1 incremental. */
+typedef struct pdsim_ttft_sample {
+  int64_t session_id;
+  int32_t round;
+  int8_t kind;
+  int8_t local;
+  int8_t reserved[2];
+  double created_time;
+  double completion_time;
+  double value;
+} pdsim_ttft_sample;
+
+/* SessionOutcome (sim_engine.hpp:74-84). */
+typedef struct pdsim_session_outcome {
+  int64_t session_id;
+  double arrival_time;
+  double completion_time;
+  double admission_wait;
+  double mean_itl;
+  int32_t rounds;
+  int8_t ttft_ok;
+  int8_t itl_ok;
+  int8_t slo_ok;
+  int8_t reserved;
+} pdsim_session_outcome;
+
+/* SimCounters (sim_engine.hpp:96-103). */
+typedef struct pdsim_counters {
+  int64_t tasks_created;
+  int64_t tasks_completed;
+  int64_t tokens_decoded;
+  int64_t kv_bytes_residual;
+  int32_t max_postpone_observed;
+  int32_t events_in_order;
+} pdsim_counters;
+
+/* Attainment numerators and denominator (metrics.cpp:171-186). */
+typedef struct pdsim_attainment {
+  int64_t sessions_total;
+  int64_t sessions_completed;
+  int64_t slo_ok;
+  int64_t ttft_ok;
+  int64_t itl_ok;
+} pdsim_attainment;
+
+/* Output of one replay (the SimResult of run()). Record arrays are optional
+ * (NULL to skip); when given they must hold n_rounds decisions / TTFT samples
+ * and n_sessions outcomes. Decisions and TTFT samples come in the reference
+ * push order; sessions are sorted by session id (sim_engine.cpp:165-168). */
+typedef struct pdsim_run_output {
+  pdsim_decision* decisions;
+  pdsim_ttft_sample* ttft_samples;
+  pdsim_session_outcome* sessions;
+  int64_t n_decisions;   /* out */
+  int64_t n_ttft;        /* out */
+  int64_t n_sessions;    /* out: completed sessions */
+  pdsim_counters counters;     /* out */
+  pdsim_attainment attainment; /* out */
+} pdsim_run_output;
+
+/* Batched search: pairs are (candidate c, trace replica r), pair index
+ * p = c * n_traces + r. Only pairs in [pair_begin, pair_end) are replayed
+ * (the shard of this device); pair_end < 0 means all pairs. */
+typedef struct pdsim_search_input {
+  int32_t n_traces;
+  int32_t n_candidates;
+  const pdsim_trace* traces;     /* [n_traces] */
+  const pdsim_plan* candidates;  /* [n_candidates] */
+  int64_t pair_begin;
+  int64_t pair_end;
+} pdsim_search_input;
+
+/* Search results. Arrays are caller-allocated; any may be NULL.
+ *  pair_attainment / pair_counters / pair_status: [pair_end - pair_begin].
+ *  candidate_slo_ok: [n_candidates], sum of slo_ok over this call's pairs;
+ *    -1 for a candidate with any invalid pair in this call.
+ * best_candidate = argmax candidate_slo_ok, ties -> smallest index (-1 when no
+ * candidate is valid). Timings are device (CUDA event) milliseconds. */
+typedef struct pdsim_search_output {
+  pdsim_attainment* pair_attainment;
+  pdsim_counters* pair_counters;
+  int8_t* pair_status;
+  int64_t* candidate_slo_ok;
+  int32_t best_candidate;
+  int32_t reserved;
+  int64_t best_slo_ok;
+  double kernel_ms;     /* replay kernel(s) only */
+  double device_ms;     /* whole device-side search incl. reductions */
+  int64_t kernel_launches;
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} pdsim_search_output;
+
+/* ---- context -------------------------------------------------------------- */
+
+typedef struct pdsim_gpu_ctx pdsim_gpu_ctx;
+
+int pdsim_abi_version(void);
+const char* pdsim_last_error(void); /* thread-local message of the last failure */
+
+/* Creates a context on CUDA device `device`. Fails with PDSIM_ERR_CUDA when no
+ * sm_100 device is present: there is no CPU fallback. */
+int pdsim_gpu_create(int device, pdsim_gpu_ctx** out);
+void pdsim_gpu_destroy(pdsim_gpu_ctx* ctx);
+const char* pdsim_gpu_last_error(const pdsim_gpu_ctx* ctx);
+/* Launch subsequent work on this cudaStream_t (NULL = the context's own). */
+int pdsim_gpu_set_stream(pdsim_gpu_ctx* ctx, void* cuda_stream);
+
+/* Drop-in for pdsim::run (sim_engine.hpp:125-127): one replay, full records. */
+int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace,
+                  const pdsim_plan* plan, const pdsim_profile* profile,
+                  const pdsim_sched_params* params, uint64_t seed,
+                  pdsim_run_output* out);
+
+/* Batched replay search: host inputs, host outputs (H2D + kernels + D2H). */
+int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in,
+                          const pdsim_profile* profile,
+                          const pdsim_sched_params* params, uint64_t seed,
+                          pdsim_search_output* out);
+
+/* Resident variant: pdsim_gpu_stage() copies traces + candidates into HBM
+ * once; pdsim_gpu_search_staged() replays them with inputs already resident
+ * (outputs still land in caller host buffers). */
+int pdsim_gpu_stage(pdsim_gpu_ctx* ctx, const pdsim_search_input* in,
+                    const pdsim_profile* profile,
+                    const pdsim_sched_params* params);
+int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
+                            int64_t pair_end, uint64_t seed,
+                            pdsim_search_output* out);
+
+/* ---- host-side helpers (reference generators; host C++, libm) ------------ */
+
+/* SynthProfileSpec (perf_model.hpp:110-139). */
+typedef struct pdsim_synth_spec {
+  int32_t n_degrees;
+  int32_t degrees[PDSIM_MAX_DEGREES];
+  int32_t n_prefill_breakpoints;
+  int32_t n_decode_breakpoints;
+  double prefill_alpha_min, prefill_alpha_max;
+  double prefill_beta_min, prefill_beta_max;
+  double prefill_breakpoints[PDSIM_MAX_BREAKPOINTS];
+  double decode_alpha_min, decode_alpha_max;
+  double decode_beta_min, decode_beta_max;
+  double decode_breakpoints[PDSIM_MAX_BREAKPOINTS];
+  double segment_growth_min, segment_growth_max;
+  double scaling_exponent;
+  double kv_bandwidth_bytes_per_sec;
+  double kv_latency_seconds;
+  double kv_reshard_penalty;
+  int64_t kv_bytes_per_token;
+  int64_t gpu_memory_capacity;
+  double history_weight;
+} pdsim_synth_spec;
+
+/* TraceStats (workload.hpp:66-76); name is informational. */
+typedef struct pdsim_trace_stats {
+  double mean_rounds;
+  int32_t fixed_rounds;
+  int32_t reserved;
+  double mean_prefill_len;
+  double mean_decode_len;
+  double length_cv;
+  double first_round_fraction;
+  double mean_interaction_delay;
+  double ttft_thres;
+  double itl_thres;
+} pdsim_trace_stats;
+
+/* Owned trace produced by the generator. */
+typedef struct pdsim_trace_buf pdsim_trace_buf;
+
+void pdsim_synth_spec_default(pdsim_synth_spec* spec);
+int pdsim_synth_profile(const pdsim_synth_spec* spec, uint64_t seed,
+                        pdsim_profile* out);
+int pdsim_profile_validate(const pdsim_profile* profile);
+int pdsim_preset_stats(const char* name, pdsim_trace_stats* out);
+int pdsim_gen_trace(const pdsim_trace_stats* stats, double arrival_rate,
+                    int32_t num_sessions, uint64_t seed, pdsim_trace_buf** out);
+/* Fills a view whose arrays stay owned by `buf`. */
+int pdsim_trace_buf_view(const pdsim_trace_buf* buf, pdsim_trace* view);
+void pdsim_trace_buf_free(pdsim_trace_buf* buf);
+int pdsim_trace_validate(const pdsim_trace* trace);
+
+/* Candidate enumeration in the reference order (planner.cpp:582-601,
+ * 625-655): every (x, y) degree->count map with x, y non-empty and
+ * sum(degree * count) <= total_gpus. Returns the count; writes up to
+ * `capacity` plans into `out` (may be NULL to query the count). */
+int64_t pdsim_enumerate_plans(const int32_t* degrees, int32_t n_degrees,
+                              int32_t total_gpus, pdsim_plan* out,
+                              int64_t capacity);
+
+/* Device-free CPU argmax helper used by multi-rank callers after the NCCL
+ * reduction: max count, ties -> smallest index, negative = invalid. */
+int32_t pdsim_argmax_candidates(const int64_t* candidate_slo_ok,
+                                int32_t n_candidates);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* PDSIM_GPU_H_ */

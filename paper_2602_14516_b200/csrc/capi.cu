@@ -1,0 +1,541 @@
+// capi.cu — C-ABI implementation (include/pdsim_gpu.h) and the replay kernels.
+//
+// Drop-in for pdsim::run (reference proj/src/sim_engine.cpp:676-681) and the
+// batched candidate x replica search composed from it. All
+// replays execute on the GPU; there is no host execution path: a missing or
+// non-sm_100 device is a PDSIM_ERR_CUDA failure.
+//
+// Kernels
+//   replay_kernel  : persistent; one warp per workspace slot pulls
+//                    (candidate, replica) pairs from an atomic queue and replays
+//                    each with pdg::Engine (engine.cuh); SLO counts are folded
+//                    into per-candidate int64 sums with integer atomics
+//                    (deterministic).
+//   argmax_kernel  : one warp; max Σslo_ok over valid candidates, ties to the
+//                    smallest enumeration index.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "pack.hpp"
+#include "pdsim_gpu.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+__constant__ pdsim_profile c_profile;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t reserve(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+namespace pdg {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace pdg
+
+struct pdsim_gpu_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+  // staged inputs
+  bool staged = false;
+  int32_t n_traces = 0, n_candidates = 0;
+  pdsim_profile profile{};
+  pdsim_sched_params params{};
+  std::vector<pdg::PackedTrace> packed;
+  std::vector<pdg::DevPlan> plans;
+  std::vector<int8_t> pair_invalid;  // [n_candidates * n_traces], host precheck
+  pdg::Caps caps{};
+  size_t slot_bytes = 0;
+  DevBuf d_trace_data, d_traces, d_plans, d_invalid;
+  // per-search buffers
+  DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
+  // single-run records
+  DevBuf d_dec, d_ttft, d_sess;
+};
+
+namespace {
+
+int set_err(pdsim_gpu_ctx* ctx, int code, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_err(pdsim_gpu_ctx* ctx, cudaError_t e, const char* what) {
+  return set_err(ctx, PDSIM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(ctx, expr)                                  \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_err(ctx, _e, #expr); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Kernels
+
+struct KernelArgs {
+  const pdg::DevTrace* traces;
+  const pdg::DevPlan* plans;
+  const int8_t* pair_invalid;  // [n_candidates * n_traces]
+  int32_t n_traces;
+  int32_t reserved;
+  int64_t pair_begin;
+  int64_t pair_end;
+  pdg::DevParams params;
+  pdg::Caps caps;
+  char* ws;
+  size_t slot_bytes;
+  unsigned long long* next_pair;
+  pdg::PairResult* results;            // [pair_end - pair_begin]
+  unsigned long long* cand_sum;        // [n_candidates]
+  int* cand_bad;                       // [n_candidates]
+  pdg::Records rec;                    // single-run records (one pair only)
+  uint64_t seed;
+};
+
+__global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
+  if ((threadIdx.x & 31) != 0) return;  // v1: lane 0 runs the serial replay
+  const int slot_id = blockIdx.x;
+  pdg::Slot slot;
+  pdg::slot_bytes(a.caps, &slot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
+  for (;;) {
+    const int64_t pair = static_cast<int64_t>(atomicAdd(a.next_pair, 1ull)) + a.pair_begin;
+    if (pair >= a.pair_end) break;
+    const int32_t c = static_cast<int32_t>(pair / a.n_traces);
+    const int32_t r = static_cast<int32_t>(pair % a.n_traces);
+    pdg::PairResult res;
+    memset(&res, 0, sizeof(res));
+    if (a.pair_invalid[pair]) {
+      res.status = PDSIM_PAIR_INVALID;
+      res.att.sessions_total = a.traces[r].S;
+    } else {
+      const pdg::DevTrace tr = a.traces[r];
+      const pdg::DevPlan pl = a.plans[c];
+      pdg::Engine eng(tr, pl, c_profile, a.params, a.caps, slot, a.rec, a.seed);
+      eng.run(&res);
+    }
+    a.results[pair - a.pair_begin] = res;
+    if (res.status != PDSIM_PAIR_OK) {
+      atomicOr(&a.cand_bad[c], 1);
+    } else {
+      atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+    }
+  }
+}
+
+// Packed key: (slo_ok + 1) << 32 | (0xffffffff - c); 0 = invalid. One max
+// reduction yields max count with ties to the smallest index.
+__global__ void argmax_kernel(const unsigned long long* cand_sum, const int* cand_bad, int n,
+                              unsigned long long* best) {
+  unsigned long long key = 0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    if (!cand_bad[c]) {
+      const unsigned long long k = ((cand_sum[c] + 1ull) << 32) | (0xffffffffull - static_cast<unsigned>(c));
+      key = k > key ? k : key;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long other = __shfl_down_sync(0xffffffffu, key, o);
+    key = other > key ? other : key;
+  }
+  __shared__ unsigned long long warp_best[32];
+  if ((threadIdx.x & 31) == 0) warp_best[threadIdx.x >> 5] = key;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long k = 0;
+    for (int w = 0; w < static_cast<int>((blockDim.x + 31) / 32); ++w) k = warp_best[w] > k ? warp_best[w] : k;
+    *best = k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host orchestration
+
+int check_ctx(pdsim_gpu_ctx* ctx) {
+  if (!ctx) return set_err(nullptr, PDSIM_ERR_CONFIG, "null context");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_err(ctx, e, "cudaSetDevice");
+  return PDSIM_OK;
+}
+
+int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_profile* profile,
+               const pdsim_sched_params* params, int64_t* h2d_bytes) {
+  if (!in || !profile || !params) return set_err(ctx, PDSIM_ERR_CONFIG, "null argument");
+  if (in->n_traces < 1 || in->n_candidates < 1 || !in->traces || !in->candidates) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "search: need at least one trace and one candidate");
+  }
+  ctx->staged = false;
+  pdg::HostError err;
+  // Reference validation order (sim_engine.cpp:115-122).
+  for (int r = 0; r < in->n_traces; ++r) {
+    if (!pdg::validate_params(*params, in->traces[r].ttft_thres, in->traces[r].itl_thres, &err)) {
+      return set_err(ctx, err.code, err.msg);
+    }
+  }
+  ctx->packed.assign(static_cast<size_t>(in->n_traces), pdg::PackedTrace());
+  bool any_sessions = false;
+  for (int r = 0; r < in->n_traces; ++r) {
+    if (!pdg::pack_trace(in->traces[r], &ctx->packed[static_cast<size_t>(r)], &err)) return set_err(ctx, err.code, err.msg);
+    any_sessions |= ctx->packed[static_cast<size_t>(r)].S > 0;
+  }
+  if (!pdg::validate_profile(*profile, &err)) return set_err(ctx, err.code, err.msg);
+  if (params->reorder && params->window > 8 && any_sessions) {
+    // reorder_and_dequeue throws at the first dequeue (reorder.cpp:86-90).
+    return set_err(ctx, PDSIM_ERR_CONFIG, "reorder: window must be <= 8");
+  }
+  ctx->plans.assign(static_cast<size_t>(in->n_candidates), pdg::DevPlan());
+  int pmax = 0, dmax = 1;
+  for (int c = 0; c < in->n_candidates; ++c) {
+    pdg::DevPlan& p = ctx->plans[static_cast<size_t>(c)];
+    memset(&p, 0, sizeof(p));
+    if (!pdg::pack_plan(in->candidates[c], *profile, &p, &err)) return set_err(ctx, err.code, err.msg);
+    pmax = std::max(pmax, p.P);
+    dmax = std::max(dmax, p.D);
+  }
+  ctx->pair_invalid.assign(static_cast<size_t>(in->n_candidates) * in->n_traces, 0);
+  for (int c = 0; c < in->n_candidates; ++c)
+    for (int r = 0; r < in->n_traces; ++r)
+      ctx->pair_invalid[static_cast<size_t>(c) * in->n_traces + r] =
+          pdg::precheck(ctx->packed[static_cast<size_t>(r)], ctx->plans[static_cast<size_t>(c)], *profile) ? 0 : 1;
+
+  std::vector<const pdg::PackedTrace*> tp;
+  for (auto& t : ctx->packed) tp.push_back(&t);
+  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params);
+  ctx->slot_bytes = pdg::slot_bytes(ctx->caps, nullptr, nullptr);
+  ctx->profile = *profile;
+  ctx->params = *params;
+  ctx->n_traces = in->n_traces;
+  ctx->n_candidates = in->n_candidates;
+
+  // H2D: trace arrays (one contiguous buffer), DevTrace table, plans, flags.
+  size_t total = 0;
+  for (auto& t : ctx->packed) total += pdg::align_up(t.device_bytes() + 8 * 256);
+  CU(ctx, ctx->d_trace_data.reserve(std::max<size_t>(total, 256)));
+  std::vector<pdg::DevTrace> dt(static_cast<size_t>(in->n_traces));
+  std::vector<char> host(std::max<size_t>(total, 256));
+  size_t off = 0;
+  char* dbase = ctx->d_trace_data.as<char>();
+  auto put = [&](const void* src, size_t bytes) -> void* {
+    void* dst = dbase + off;
+    if (bytes) memcpy(host.data() + off, src, bytes);
+    off = pdg::align_up(off + bytes);
+    return dst;
+  };
+  for (size_t r = 0; r < ctx->packed.size(); ++r) {
+    const pdg::PackedTrace& t = ctx->packed[r];
+    pdg::DevTrace& d = dt[r];
+    d.S = t.S;
+    d.R = t.R;
+    d.max_dec = t.max_dec;
+    d.reserved = 0;
+    d.ttft_thres = t.ttft_thres;
+    d.itl_thres = t.itl_thres;
+    d.arrival = static_cast<const double*>(put(t.arrival.data(), t.arrival.size() * 8));
+    d.round_off = static_cast<const int32_t*>(put(t.round_off.data(), t.round_off.size() * 4));
+    d.incr = static_cast<const int32_t*>(put(t.incr.data(), t.incr.size() * 4));
+    d.dec = static_cast<const int32_t*>(put(t.dec.data(), t.dec.size() * 4));
+    d.delay = static_cast<const double*>(put(t.delay.data(), t.delay.size() * 8));
+    d.sid = static_cast<const int64_t*>(put(t.sid.data(), t.sid.size() * 8));
+    d.rank = static_cast<const int32_t*>(put(t.rank.data(), t.rank.size() * 4));
+    d.by_rank = static_cast<const int32_t*>(put(t.by_rank.data(), t.by_rank.size() * 4));
+  }
+  CU(ctx, cudaMemcpyAsync(ctx->d_trace_data.p, host.data(), off, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, ctx->d_traces.reserve(sizeof(pdg::DevTrace) * dt.size()));
+  CU(ctx, cudaMemcpyAsync(ctx->d_traces.p, dt.data(), sizeof(pdg::DevTrace) * dt.size(), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  CU(ctx, ctx->d_plans.reserve(sizeof(pdg::DevPlan) * ctx->plans.size()));
+  CU(ctx, cudaMemcpyAsync(ctx->d_plans.p, ctx->plans.data(), sizeof(pdg::DevPlan) * ctx->plans.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, ctx->d_invalid.reserve(ctx->pair_invalid.size()));
+  CU(ctx, cudaMemcpyAsync(ctx->d_invalid.p, ctx->pair_invalid.data(), ctx->pair_invalid.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyToSymbolAsync(c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (h2d_bytes) {
+    *h2d_bytes = static_cast<int64_t>(off + sizeof(pdg::DevTrace) * dt.size() +
+                                      sizeof(pdg::DevPlan) * ctx->plans.size() + ctx->pair_invalid.size() +
+                                      sizeof(pdsim_profile));
+  }
+  ctx->staged = true;
+  return PDSIM_OK;
+}
+
+// Replays pairs [b, e) of the staged inputs; results land in host buffers.
+int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_search_output* out,
+                pdg::Records rec, pdg::PairResult* single_result) {
+  if (!ctx->staged) return set_err(ctx, PDSIM_ERR_CONFIG, "search: nothing staged");
+  const int64_t total = static_cast<int64_t>(ctx->n_traces) * ctx->n_candidates;
+  if (e < 0) e = total;
+  if (b < 0 || b > e || e > total) return set_err(ctx, PDSIM_ERR_CONFIG, "search: bad pair range");
+  const int64_t n = e - b;
+  const int C = ctx->n_candidates;
+
+  // Workspace slots: one warp each, at most 32 resident per SM, bounded by a
+  // memory budget.
+  size_t free_b = 0, total_b = 0;
+  CU(ctx, cudaMemGetInfo(&free_b, &total_b));
+  const size_t budget = std::min<size_t>(free_b / 2 + ctx->d_ws.bytes / 2, size_t(64) << 30);
+  int64_t slots = std::min<int64_t>(std::max<int64_t>(n, 1), static_cast<int64_t>(ctx->sm_count) * 32);
+  slots = std::min<int64_t>(slots, static_cast<int64_t>(budget / std::max<size_t>(ctx->slot_bytes, 1)));
+  if (slots < 1) return set_err(ctx, PDSIM_ERR_CUDA, "search: workspace of one slot exceeds device memory");
+  CU(ctx, ctx->d_ws.reserve(ctx->slot_bytes * static_cast<size_t>(slots)));
+  CU(ctx, ctx->d_results.reserve(sizeof(pdg::PairResult) * static_cast<size_t>(std::max<int64_t>(n, 1))));
+  CU(ctx, ctx->d_cand_sum.reserve(8 * static_cast<size_t>(C)));
+  CU(ctx, ctx->d_cand_bad.reserve(4 * static_cast<size_t>(C)));
+  CU(ctx, ctx->d_counter.reserve(8));
+  CU(ctx, ctx->d_best.reserve(8));
+
+  CU(ctx, cudaEventRecord(ctx->ev[0], ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->d_cand_sum.p, 0, 8 * static_cast<size_t>(C), ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->d_cand_bad.p, 0, 4 * static_cast<size_t>(C), ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->d_counter.p, 0, 8, ctx->stream));
+
+  KernelArgs a;
+  memset(&a, 0, sizeof(a));
+  a.traces = ctx->d_traces.as<pdg::DevTrace>();
+  a.plans = ctx->d_plans.as<pdg::DevPlan>();
+  a.pair_invalid = ctx->d_invalid.as<int8_t>();
+  a.n_traces = ctx->n_traces;
+  a.pair_begin = b;
+  a.pair_end = e;
+  a.params = pdg::to_dev_params(ctx->params);
+  a.caps = ctx->caps;
+  a.ws = ctx->d_ws.as<char>();
+  a.slot_bytes = ctx->slot_bytes;
+  a.next_pair = ctx->d_counter.as<unsigned long long>();
+  a.results = ctx->d_results.as<pdg::PairResult>();
+  a.cand_sum = ctx->d_cand_sum.as<unsigned long long>();
+  a.cand_bad = ctx->d_cand_bad.as<int>();
+  a.rec = rec;
+  a.seed = seed;
+  int64_t launches = 0;
+  CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
+  if (n > 0) {
+    replay_kernel<<<static_cast<unsigned>(slots), 32, 0, ctx->stream>>>(a);
+    ++launches;
+    CU(ctx, cudaGetLastError());
+  }
+  CU(ctx, cudaEventRecord(ctx->ev[2], ctx->stream));
+  argmax_kernel<<<1, 256, 0, ctx->stream>>>(ctx->d_cand_sum.as<unsigned long long>(), ctx->d_cand_bad.as<int>(), C,
+                                          ctx->d_best.as<unsigned long long>());
+  ++launches;
+  CU(ctx, cudaGetLastError());
+  CU(ctx, cudaEventRecord(ctx->ev[3], ctx->stream));
+
+  // D2H
+  std::vector<pdg::PairResult> res(static_cast<size_t>(n));
+  std::vector<unsigned long long> csum(static_cast<size_t>(C));
+  std::vector<int> cbad(static_cast<size_t>(C));
+  unsigned long long best = 0;
+  if (n > 0) {
+    CU(ctx, cudaMemcpyAsync(res.data(), ctx->d_results.p, sizeof(pdg::PairResult) * static_cast<size_t>(n),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CU(ctx, cudaMemcpyAsync(csum.data(), ctx->d_cand_sum.p, 8 * static_cast<size_t>(C), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CU(ctx, cudaMemcpyAsync(cbad.data(), ctx->d_cand_bad.p, 4 * static_cast<size_t>(C), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CU(ctx, cudaMemcpyAsync(&best, ctx->d_best.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  float k_ms = 0, d_ms = 0;
+  CU(ctx, cudaEventElapsedTime(&k_ms, ctx->ev[1], ctx->ev[2]));
+  CU(ctx, cudaEventElapsedTime(&d_ms, ctx->ev[0], ctx->ev[3]));
+
+  bool engine_error = false;
+  for (const auto& r : res) engine_error |= r.status == PDSIM_PAIR_ERROR;
+  if (out) {
+    for (int64_t k = 0; k < n; ++k) {
+      if (out->pair_attainment) out->pair_attainment[k] = res[static_cast<size_t>(k)].att;
+      if (out->pair_counters) out->pair_counters[k] = res[static_cast<size_t>(k)].ctr;
+      if (out->pair_status) out->pair_status[k] = static_cast<int8_t>(res[static_cast<size_t>(k)].status);
+    }
+    if (out->candidate_slo_ok) {
+      for (int c = 0; c < C; ++c) out->candidate_slo_ok[c] = cbad[c] ? -1 : static_cast<int64_t>(csum[c]);
+    }
+    out->best_candidate = best ? static_cast<int32_t>(0xffffffffull - (best & 0xffffffffull)) : -1;
+    out->best_slo_ok = best ? static_cast<int64_t>((best >> 32) - 1) : -1;
+    out->kernel_ms = k_ms;
+    out->device_ms = d_ms;
+    out->kernel_launches = launches;
+    out->d2h_bytes = static_cast<int64_t>(sizeof(pdg::PairResult) * static_cast<size_t>(n) + 12 * C + 8);
+  }
+  if (single_result && n == 1) *single_result = res[0];
+  if (engine_error) {
+    return set_err(ctx, PDSIM_ERR_INTERNAL, "engine capacity or invariant violated in at least one pair");
+  }
+  return PDSIM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pdsim_abi_version(void) { return PDSIM_ABI_VERSION; }
+
+const char* pdsim_last_error(void) { return g_last_error.c_str(); }
+
+int pdsim_gpu_create(int device, pdsim_gpu_ctx** out) {
+  if (!out) return set_err(nullptr, PDSIM_ERR_CONFIG, "null output pointer");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    return set_err(nullptr, PDSIM_ERR_CUDA,
+                   std::string("no CUDA device available (the replay engine has no CPU path): ") +
+                       (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0"));
+  }
+  if (device < 0 || device >= n) return set_err(nullptr, PDSIM_ERR_CUDA, "device index out of range");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return set_err(nullptr, PDSIM_ERR_CUDA, cudaGetErrorString(e));
+  if (prop.major != 10) {
+    return set_err(nullptr, PDSIM_ERR_CUDA,
+                   "device " + std::to_string(device) + " is sm_" + std::to_string(prop.major) +
+                       std::to_string(prop.minor) + "; this build targets sm_100a only");
+  }
+  std::unique_ptr<pdsim_gpu_ctx> ctx(new pdsim_gpu_ctx());
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  CU(ctx.get(), cudaSetDevice(device));
+  CU(ctx.get(), cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  for (auto& ev : ctx->ev) CU(ctx.get(), cudaEventCreate(&ev));
+  *out = ctx.release();
+  return PDSIM_OK;
+}
+
+void pdsim_gpu_destroy(pdsim_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* pdsim_gpu_last_error(const pdsim_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int pdsim_gpu_set_stream(pdsim_gpu_ctx* ctx, void* stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_stage(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_profile* profile,
+                    const pdsim_sched_params* params) {
+  if (int rc = check_ctx(ctx)) return rc;
+  return stage_impl(ctx, in, profile, params, nullptr);
+}
+
+int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin, int64_t pair_end, uint64_t seed,
+                            pdsim_search_output* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  pdg::Records rec{nullptr, nullptr, nullptr};
+  const int rc = search_impl(ctx, pair_begin, pair_end, seed, out, rec, nullptr);
+  if (out && rc == PDSIM_OK) out->h2d_bytes = 0;
+  return rc;
+}
+
+int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_profile* profile,
+                          const pdsim_sched_params* params, uint64_t seed, pdsim_search_output* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  int64_t h2d = 0;
+  if (int rc = stage_impl(ctx, in, profile, params, &h2d)) return rc;
+  pdg::Records rec{nullptr, nullptr, nullptr};
+  const int rc = search_impl(ctx, in->pair_begin, in->pair_end, seed, out, rec, nullptr);
+  if (out) out->h2d_bytes = h2d;
+  return rc;
+}
+
+int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan* plan,
+                  const pdsim_profile* profile, const pdsim_sched_params* params, uint64_t seed,
+                  pdsim_run_output* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!trace || !plan || !out) return set_err(ctx, PDSIM_ERR_CONFIG, "null argument");
+  pdsim_search_input in;
+  memset(&in, 0, sizeof(in));
+  in.n_traces = 1;
+  in.n_candidates = 1;
+  in.traces = trace;
+  in.candidates = plan;
+  in.pair_begin = 0;
+  in.pair_end = 1;
+  if (int rc = stage_impl(ctx, &in, profile, params, nullptr)) return rc;
+  if (ctx->pair_invalid[0]) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
+  }
+  const pdg::PackedTrace& t = ctx->packed[0];
+  pdg::Records rec{nullptr, nullptr, nullptr};
+  const size_t R = static_cast<size_t>(std::max(t.R, 1)), S = static_cast<size_t>(std::max(t.S, 1));
+  if (out->decisions) {
+    CU(ctx, ctx->d_dec.reserve(sizeof(pdsim_decision) * R));
+    rec.decisions = ctx->d_dec.as<pdsim_decision>();
+  }
+  if (out->ttft_samples) {
+    CU(ctx, ctx->d_ttft.reserve(sizeof(pdsim_ttft_sample) * R));
+    rec.ttft = ctx->d_ttft.as<pdsim_ttft_sample>();
+  }
+  if (out->sessions) {
+    CU(ctx, ctx->d_sess.reserve(sizeof(pdsim_session_outcome) * S));
+    rec.sessions = ctx->d_sess.as<pdsim_session_outcome>();
+  }
+  pdg::PairResult res;
+  memset(&res, 0, sizeof(res));
+  if (int rc = search_impl(ctx, 0, 1, seed, nullptr, rec, &res)) return rc;
+  out->n_decisions = res.n_decisions;
+  out->n_ttft = res.n_ttft;
+  out->n_sessions = res.att.sessions_completed;
+  out->counters = res.ctr;
+  out->attainment = res.att;
+  if (out->decisions && res.n_decisions > 0) {
+    CU(ctx, cudaMemcpyAsync(out->decisions, rec.decisions, sizeof(pdsim_decision) * res.n_decisions,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (out->ttft_samples && res.n_ttft > 0) {
+    CU(ctx, cudaMemcpyAsync(out->ttft_samples, rec.ttft, sizeof(pdsim_ttft_sample) * res.n_ttft,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (out->sessions && out->n_sessions > 0) {
+    CU(ctx, cudaMemcpyAsync(out->sessions, rec.sessions, sizeof(pdsim_session_outcome) * out->n_sessions,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  if (out->sessions) pdg::sort_outcomes(out->sessions, out->n_sessions);
+  return PDSIM_OK;
+}
+
+}  // extern "C"

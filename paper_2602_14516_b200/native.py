@@ -1,0 +1,268 @@
+"""Loader and thin Python mirror of the C-ABI (include/pdsim_gpu.h).
+
+The product is ``libpdsim_gpu.so`` (CUDA sm_100a kernels + host C++). This
+module only marshals arguments; every replay runs on the GPU. There is no CPU
+fallback: if the library or a B200 is missing, calls raise :class:`PdsimError`.
+
+Python names follow the reference's C++ API (proj/include/pdsim/*.hpp):
+``run`` (sim_engine.hpp:125-127), ``gen_trace`` / ``preset_stats``
+(workload.hpp:78-86), ``synth_profile`` (perf_model.hpp:141-142), and the
+batched ``plan_search`` added on top of them.
+"""
+import ctypes as C
+import os
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpdsim_gpu.so")
+
+_lib = None
+
+
+class PdsimError(RuntimeError):
+    """Raised for a non-zero status. ``code`` is the PDSIM_ERR_* value."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"pdsim error {code}: {msg}")
+        self.code = code
+
+
+class ConfigError(PdsimError):
+    pass
+
+
+class DomainError(PdsimError):
+    pass
+
+
+def lib():
+    """Loads libpdsim_gpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PdsimError(abi.ERR_CUDA, f"{LIB_PATH} not built (run __graft_entry__.build() or `make`)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.pdsim_abi_version.restype = C.c_int
+        L.pdsim_last_error.restype = C.c_char_p
+        L.pdsim_gpu_create.argtypes = [C.c_int, P(C.c_void_p)]
+        L.pdsim_gpu_destroy.argtypes = [C.c_void_p]
+        L.pdsim_gpu_last_error.argtypes = [C.c_void_p]
+        L.pdsim_gpu_last_error.restype = C.c_char_p
+        L.pdsim_gpu_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        L.pdsim_gpu_run.argtypes = [C.c_void_p, P(abi.Trace), P(abi.Plan), P(abi.Profile), P(abi.SchedParams),
+                                    C.c_uint64, P(abi.RunOutput)]
+        L.pdsim_gpu_plan_search.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams),
+                                            C.c_uint64, P(abi.SearchOutput)]
+        L.pdsim_gpu_stage.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams)]
+        L.pdsim_gpu_search_staged.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, P(abi.SearchOutput)]
+        L.pdsim_synth_spec_default.argtypes = [P(abi.SynthSpec)]
+        L.pdsim_synth_profile.argtypes = [P(abi.SynthSpec), C.c_uint64, P(abi.Profile)]
+        L.pdsim_profile_validate.argtypes = [P(abi.Profile)]
+        L.pdsim_preset_stats.argtypes = [C.c_char_p, P(abi.TraceStats)]
+        L.pdsim_gen_trace.argtypes = [P(abi.TraceStats), C.c_double, C.c_int32, C.c_uint64, P(C.c_void_p)]
+        L.pdsim_trace_buf_view.argtypes = [C.c_void_p, P(abi.Trace)]
+        L.pdsim_trace_buf_free.argtypes = [C.c_void_p]
+        L.pdsim_trace_validate.argtypes = [P(abi.Trace)]
+        L.pdsim_enumerate_plans.argtypes = [P(C.c_int32), C.c_int32, C.c_int32, P(abi.Plan), C.c_int64]
+        L.pdsim_enumerate_plans.restype = C.c_int64
+        L.pdsim_argmax_candidates.argtypes = [P(C.c_int64), C.c_int32]
+        L.pdsim_argmax_candidates.restype = C.c_int32
+        if L.pdsim_abi_version() != 1:
+            raise PdsimError(abi.ERR_INTERNAL, "ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def _raise(rc, msg):
+    msg = msg.decode() if isinstance(msg, bytes) else msg
+    if rc == abi.ERR_CONFIG:
+        raise ConfigError(rc, msg)
+    if rc == abi.ERR_DOMAIN:
+        raise DomainError(rc, msg)
+    raise PdsimError(rc, msg)
+
+
+def _check(rc, ctx=None):
+    if rc != 0:
+        L = lib()
+        _raise(rc, L.pdsim_gpu_last_error(ctx) if ctx else L.pdsim_last_error())
+
+
+# ---- host generators (reference RNG, host libm) -----------------------------
+
+def default_synth_spec():
+    s = abi.SynthSpec()
+    lib().pdsim_synth_spec_default(C.byref(s))
+    return s
+
+
+def synth_profile(spec=None, seed=7):
+    spec = spec or default_synth_spec()
+    out = abi.Profile()
+    _check(lib().pdsim_synth_profile(C.byref(spec), seed, C.byref(out)))
+    return out
+
+
+def preset_stats(name):
+    out = abi.TraceStats()
+    _check(lib().pdsim_preset_stats(name.encode(), C.byref(out)))
+    return out
+
+
+class TraceBuf:
+    """An owned generated trace; ``.view`` is the pdsim_trace over its arrays."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.view = abi.Trace()
+        _check(lib().pdsim_trace_buf_view(handle, C.byref(self.view)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.pdsim_trace_buf_free(self._h)
+            self._h = None
+
+
+def gen_trace(stats, arrival_rate, num_sessions, seed):
+    h = C.c_void_p()
+    _check(lib().pdsim_gen_trace(C.byref(stats), arrival_rate, num_sessions, seed, C.byref(h)))
+    return TraceBuf(h)
+
+
+def enumerate_plans(degrees, total_gpus):
+    ds = (C.c_int32 * len(degrees))(*degrees)
+    n = lib().pdsim_enumerate_plans(ds, len(degrees), total_gpus, None, 0)
+    if n < 0:
+        raise ConfigError(abi.ERR_CONFIG, "bad degree set")
+    out = (abi.Plan * max(n, 1))()
+    lib().pdsim_enumerate_plans(ds, len(degrees), total_gpus, out, n)
+    return list(out)[:n]
+
+
+# ---- device context -----------------------------------------------------------
+
+class RunResult:
+    """Mirror of SimResult (sim_engine.hpp:105-114) minus raw ITL samples."""
+
+    def __init__(self, out, dec, ttft, sess):
+        self.counters = out.counters
+        self.attainment = out.attainment
+        self.decisions = list(dec)[: out.n_decisions] if dec is not None else None
+        self.ttft_samples = list(ttft)[: out.n_ttft] if ttft is not None else None
+        self.sessions = list(sess)[: out.n_sessions] if sess is not None else None
+        self.n_decisions = out.n_decisions
+        self.n_ttft = out.n_ttft
+        self.n_sessions = out.n_sessions
+
+
+class SearchResult:
+    def __init__(self, out, att, ctr, st, cand, n_pairs):
+        self.best_candidate = out.best_candidate
+        self.best_slo_ok = out.best_slo_ok
+        self.kernel_ms = out.kernel_ms
+        self.device_ms = out.device_ms
+        self.kernel_launches = out.kernel_launches
+        self.h2d_bytes = out.h2d_bytes
+        self.d2h_bytes = out.d2h_bytes
+        self.pair_attainment = att
+        self.pair_counters = ctr
+        self.pair_status = st
+        self.candidate_slo_ok = cand
+        self.n_pairs = n_pairs
+
+
+def search_input(traces, plans, pair_begin=0, pair_end=-1):
+    tarr = (abi.Trace * len(traces))(*traces)
+    parr = (abi.Plan * len(plans))(*plans)
+    inp = abi.SearchInput(len(traces), len(plans), tarr, parr, pair_begin, pair_end)
+    inp._keep = (tarr, parr)
+    return inp
+
+
+class Context:
+    """A device context (pdsim_gpu_create). One per GPU / process."""
+
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        _check(lib().pdsim_gpu_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pdsim_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc):
+        _check(rc, self._h)
+
+    def set_stream(self, cuda_stream_ptr):
+        self._check(lib().pdsim_gpu_set_stream(self._h, C.c_void_p(cuda_stream_ptr or 0)))
+
+    def run(self, trace, plan, profile, params, seed, records=True):
+        """Drop-in for pdsim::run: one replay on the GPU."""
+        S, R = trace.n_sessions, trace.n_rounds
+        out = abi.RunOutput()
+        dec = ttft = sess = None
+        if records:
+            dec = (abi.Decision * max(R, 1))()
+            ttft = (abi.TtftSample * max(R, 1))()
+            sess = (abi.SessionOutcome * max(S, 1))()
+            out.decisions = C.cast(dec, C.POINTER(abi.Decision))
+            out.ttft_samples = C.cast(ttft, C.POINTER(abi.TtftSample))
+            out.sessions = C.cast(sess, C.POINTER(abi.SessionOutcome))
+        self._check(lib().pdsim_gpu_run(self._h, C.byref(trace), C.byref(plan), C.byref(profile),
+                                        C.byref(params), seed, C.byref(out)))
+        return RunResult(out, dec, ttft, sess)
+
+    def _outputs(self, n_pairs, n_cand):
+        att = (abi.Attainment * max(n_pairs, 1))()
+        ctr = (abi.Counters * max(n_pairs, 1))()
+        st = (C.c_int8 * max(n_pairs, 1))()
+        cand = (C.c_int64 * max(n_cand, 1))()
+        out = abi.SearchOutput(C.cast(att, C.POINTER(abi.Attainment)), C.cast(ctr, C.POINTER(abi.Counters)),
+                               C.cast(st, C.POINTER(C.c_int8)), C.cast(cand, C.POINTER(C.c_int64)))
+        return out, att, ctr, st, cand
+
+    def plan_search(self, traces, plans, profile, params, seed, pair_begin=0, pair_end=-1):
+        """Replays every (candidate, replica) pair in [pair_begin, pair_end)."""
+        inp = search_input(traces, plans, pair_begin, pair_end)
+        end = len(traces) * len(plans) if pair_end < 0 else pair_end
+        n = end - pair_begin
+        out, att, ctr, st, cand = self._outputs(n, len(plans))
+        self._check(lib().pdsim_gpu_plan_search(self._h, C.byref(inp), C.byref(profile), C.byref(params), seed,
+                                                C.byref(out)))
+        return SearchResult(out, att, ctr, st, cand, n)
+
+    def stage(self, traces, plans, profile, params):
+        inp = search_input(traces, plans)
+        self._check(lib().pdsim_gpu_stage(self._h, C.byref(inp), C.byref(profile), C.byref(params)))
+        self._staged = (len(traces), len(plans))
+
+    def search_staged(self, seed, pair_begin=0, pair_end=-1):
+        nt, nc = self._staged
+        end = nt * nc if pair_end < 0 else pair_end
+        n = end - pair_begin
+        out, att, ctr, st, cand = self._outputs(n, nc)
+        self._check(lib().pdsim_gpu_search_staged(self._h, pair_begin, pair_end, seed, C.byref(out)))
+        return SearchResult(out, att, ctr, st, cand, n)
+
+
+def argmax_candidates(candidate_slo_ok):
+    """Max Σslo_ok, ties to the smallest index, negatives (invalid) skipped."""
+    arr = (C.c_int64 * len(candidate_slo_ok))(*candidate_slo_ok)
+    return lib().pdsim_argmax_candidates(arr, len(candidate_slo_ok))

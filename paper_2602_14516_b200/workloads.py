@@ -1,0 +1,132 @@
+"""Pinned synthetic workloads for BASELINE.json configs C1-C5.
+
+The reference has no named model cost models, no PP dimension and no
+ReAct / mixed presets; this module is the repo's pinned mapping:
+
+* cost-model presets as SynthProfileSpec overrides (perf_model.hpp:110-139),
+  profile seed 7: ``llama3-8b`` = defaults with 131072 KV B/token,
+  ``qwen-32b`` = prefill/decode alpha/beta ranges x4 with 262144 B/token,
+  ``llama3-70b`` = ranges x8.75 with 327680 B/token;
+* degrees {1,2,4,8}: TP{1,2,4} x PP{1,2} folded into degree = TP*PP;
+* traces from the reference presets (workload.cpp:136-168) via gen_trace.
+
+All generation runs on the host through the product library's generators
+(bit-identical to the reference's, see tests/test_generators.py).
+"""
+from . import abi, native
+
+PROFILE_SEED = 7
+ENGINE_SEED = 1
+DEGREES = (1, 2, 4, 8)
+
+MODEL_PRESETS = {
+    "llama3-8b": dict(scale=1.0, kv_bytes_per_token=131072),
+    "qwen-32b": dict(scale=4.0, kv_bytes_per_token=262144),
+    "llama3-70b": dict(scale=8.75, kv_bytes_per_token=327680),
+}
+
+
+def model_spec(name):
+    p = MODEL_PRESETS[name]
+    s = native.default_synth_spec()
+    k = p["scale"]
+    for f in ("prefill_alpha_min", "prefill_alpha_max", "prefill_beta_min", "prefill_beta_max",
+              "decode_alpha_min", "decode_alpha_max", "decode_beta_min", "decode_beta_max"):
+        setattr(s, f, getattr(s, f) * k)
+    s.kv_bytes_per_token = p["kv_bytes_per_token"]
+    return s
+
+
+def model_profile(name):
+    return native.synth_profile(model_spec(name), PROFILE_SEED)
+
+
+def trace_stats(kind):
+    """toolbench / gaia / hotpotqa / dureader presets, plus the two
+    fixed-round variants the configs name."""
+    if kind == "toolbench-4fixed":  # C1: ReAct-style 4 fixed rounds
+        st = native.preset_stats("toolbench")
+        st.mean_rounds = 4.0
+        st.fixed_rounds = 1
+        return st
+    if kind == "hotpotqa-8fixed":  # C3: iterative RAG, 8 fixed rounds
+        st = native.preset_stats("hotpotqa")
+        st.mean_rounds = 8.0
+        st.fixed_rounds = 1
+        return st
+    return native.preset_stats(kind)
+
+
+class Workload:
+    def __init__(self, name, model, traces, plans, params, seed, total_gpus, desc):
+        self.name = name
+        self.model = model
+        self.profile = model_profile(model)
+        self.trace_bufs = traces
+        self.traces = [t.view for t in traces]
+        self.plans = plans
+        self.params = params
+        self.seed = seed
+        self.total_gpus = total_gpus
+        self.desc = desc
+
+    @property
+    def n_pairs(self):
+        return len(self.traces) * len(self.plans)
+
+    @property
+    def request_rounds(self):
+        """Σ over pairs of the trace's round count (the metric's unit)."""
+        return sum(t.n_rounds for t in self.traces) * len(self.plans)
+
+    def input_bytes(self, pair_begin=0, pair_end=-1):
+        """Algorithmic bytes: 24 B per round + 16 B per session, per pair
+        (Round = int64+int64+f64, workload.hpp:28-34; SessionSpec
+        arrival_time f64 + session_id int64, workload.hpp:36-39)."""
+        nt = len(self.traces)
+        end = self.n_pairs if pair_end < 0 else pair_end
+        per_trace = [24 * t.n_rounds + 16 * t.n_sessions for t in self.traces]
+        return sum(per_trace[p % nt] for p in range(pair_begin, end))
+
+    def rounds_in(self, pair_begin=0, pair_end=-1):
+        nt = len(self.traces)
+        end = self.n_pairs if pair_end < 0 else pair_end
+        return sum(self.traces[p % nt].n_rounds for p in range(pair_begin, end))
+
+
+def c1():
+    st = trace_stats("toolbench-4fixed")
+    tr = native.gen_trace(st, 8.0, 1000, 1)
+    plan = abi.make_plan({1: 2}, {1: 2})
+    return Workload("C1", "llama3-8b", [tr], [plan], abi.default_params(), ENGINE_SEED, 4,
+                    "llama3-8b, fixed P:2x1 D:2x1, toolbench 1k sessions x 4 fixed rounds @8/s, 1 replay")
+
+
+def c2(sessions=10000, rate=16.0, seed=5, total_gpus=8):
+    st = trace_stats("toolbench")
+    tr = native.gen_trace(st, rate, sessions, seed)
+    plans = native.enumerate_plans(DEGREES, total_gpus)
+    return Workload("C2", "llama3-8b", [tr], plans, abi.default_params(), ENGINE_SEED, total_gpus,
+                    f"llama3-8b, all {len(plans)} N={total_gpus} P/D plans over degrees {{1,2,4,8}}, "
+                    f"toolbench {sessions} sessions @{rate}/s")
+
+
+def c3(sessions=50000, rate=20.0, replicas=16, total_gpus=8):
+    st = trace_stats("hotpotqa-8fixed")
+    trs = [native.gen_trace(st, rate, sessions, s) for s in range(1, replicas + 1)]
+    plans = native.enumerate_plans(DEGREES, total_gpus)
+    return Workload("C3", "qwen-32b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
+                    f"qwen-32b, {len(plans)} plans x {replicas} hotpotqa-8-round replicas of {sessions} sessions")
+
+
+def c5(model="llama3-8b", rates=None, seeds=4, sessions=1000, total_gpus=8):
+    """One model slice of C5: toolbench 1k-session traces over rates x seeds."""
+    rates = rates or [1.0 + 0.5 * k for k in range(32)]
+    st = trace_stats("toolbench")
+    trs = [native.gen_trace(st, r, sessions, 1000 + s) for r in rates for s in range(seeds)]
+    plans = native.enumerate_plans(DEGREES, total_gpus)
+    return Workload("C5", model, trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
+                    f"{model}, {len(plans)} plans x {len(trs)} toolbench traces ({len(rates)} rates x {seeds} seeds)")
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C5": c5}

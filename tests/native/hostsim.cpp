@@ -1,0 +1,89 @@
+// tests/native/hostsim.cpp — TEST-ONLY host build of the device replay engine.
+//
+// Compiles paper_2602_14516_b200/csrc/engine.cuh for the CPU so the engine's
+// logic can be compared with the reference on every CPU test run (this
+// container has no GPU). It is not part of the product: nothing in the
+// package loads libhostsim.so, and the product's C-ABI has no CPU path.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "pack.hpp"
+#include "pdsim_gpu.h"
+
+namespace {
+thread_local std::string g_err;
+int fail(const pdg::HostError& e) {
+  g_err = e.msg;
+  return e.code;
+}
+}  // namespace
+
+extern "C" {
+
+const char* hostsim_last_error(void) { return g_err.c_str(); }
+
+// Same contract as pdsim_gpu_run.
+int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_profile* prof,
+                const pdsim_sched_params* params, uint64_t seed, pdsim_run_output* out) {
+  pdg::HostError err;
+  if (!pdg::validate_params(*params, trace->ttft_thres, trace->itl_thres, &err)) return fail(err);
+  pdg::PackedTrace t;
+  if (!pdg::pack_trace(*trace, &t, &err)) return fail(err);
+  if (!pdg::validate_profile(*prof, &err)) return fail(err);
+  if (params->reorder && params->window > 8 && t.S > 0) {
+    err.set(PDSIM_ERR_CONFIG, "reorder: window must be <= 8");
+    return fail(err);
+  }
+  pdg::DevPlan dp;
+  std::memset(&dp, 0, sizeof(dp));
+  if (!pdg::pack_plan(*plan, *prof, &dp, &err)) return fail(err);
+  if (!pdg::precheck(t, dp, *prof)) {
+    err.set(PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
+    return fail(err);
+  }
+  const pdg::Caps caps = pdg::compute_caps({&t}, dp.P, dp.D, *prof, *params);
+  std::vector<char> ws(pdg::slot_bytes(caps, nullptr, nullptr) + 256);
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws.data()) + 255) & ~uintptr_t(255));
+  pdg::Slot slot;
+  pdg::slot_bytes(caps, &slot, base);
+  pdg::DevTrace dt;
+  dt.S = t.S;
+  dt.R = t.R;
+  dt.max_dec = t.max_dec;
+  dt.reserved = 0;
+  dt.ttft_thres = t.ttft_thres;
+  dt.itl_thres = t.itl_thres;
+  dt.arrival = t.arrival.data();
+  dt.round_off = t.round_off.data();
+  dt.incr = t.incr.data();
+  dt.dec = t.dec.data();
+  dt.delay = t.delay.data();
+  dt.sid = t.sid.data();
+  dt.rank = t.rank.data();
+  dt.by_rank = t.by_rank.data();
+  const pdg::DevParams dprm = pdg::to_dev_params(*params);
+  pdg::Records rec{out->decisions, out->ttft_samples, out->sessions};
+  pdg::Engine eng(dt, dp, *prof, dprm, caps, slot, rec, seed);
+  pdg::PairResult res;
+  std::memset(&res, 0, sizeof(res));
+  eng.run(&res);
+  if (res.status != PDSIM_PAIR_OK) {
+    err.set(PDSIM_ERR_INTERNAL, "engine capacity or invariant violated");
+    return fail(err);
+  }
+  out->n_decisions = res.n_decisions;
+  out->n_ttft = res.n_ttft;
+  out->n_sessions = res.att.sessions_completed;
+  out->counters = res.ctr;
+  out->attainment = res.att;
+  if (out->sessions) pdg::sort_outcomes(out->sessions, out->n_sessions);
+  return PDSIM_OK;
+}
+
+}  // extern "C"
+
+extern "C" double hostsim_fold_repeat(double s, double g, uint64_t count) {
+  return pdg::fold_repeat(s, g, count);
+}

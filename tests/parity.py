@@ -1,0 +1,129 @@
+"""Parity helpers shared by the tests and __graft_entry__.smoke().
+
+Checkers (TEST INFRASTRUCTURE): the reference simulator itself
+(oracle/_ref/libpdsim_ref.so) when present, otherwise the plain-C
+restatement (oracle/build/liboracle.so). Both share the C-ABI POD types.
+"""
+import ctypes as C
+import os
+
+from paper_2602_14516_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HOSTSIM_PATH = os.path.join(ROOT, "tests", "native", "libhostsim.so")
+
+_hostsim = None
+
+
+def hostsim():
+    """TEST-ONLY host build of the device engine (tests/native/hostsim.cpp)."""
+    global _hostsim
+    if _hostsim is None:
+        L = C.CDLL(HOSTSIM_PATH)
+        P = C.POINTER
+        L.hostsim_run.argtypes = [P(abi.Trace), P(abi.Plan), P(abi.Profile), P(abi.SchedParams), C.c_uint64,
+                                  P(abi.RunOutput)]
+        L.hostsim_last_error.restype = C.c_char_p
+        L.hostsim_fold_repeat.argtypes = [C.c_double, C.c_double, C.c_uint64]
+        L.hostsim_fold_repeat.restype = C.c_double
+        _hostsim = L
+    return _hostsim
+
+
+class Run:
+    """Plain-Python view of a run's outputs, comparable field by field."""
+
+    def __init__(self, out, dec, ttft, sess):
+        self.counters = out.counters
+        self.attainment = out.attainment
+        self.n_decisions, self.n_ttft, self.n_sessions = out.n_decisions, out.n_ttft, out.n_sessions
+        self.decisions = list(dec)[: out.n_decisions] if dec is not None else []
+        self.ttft_samples = list(ttft)[: out.n_ttft] if ttft is not None else []
+        self.sessions = list(sess)[: out.n_sessions] if sess is not None else []
+
+
+def _alloc(trace):
+    S, R = max(trace.n_sessions, 1), max(trace.n_rounds, 1)
+    out = abi.RunOutput()
+    dec, ttft, sess = (abi.Decision * R)(), (abi.TtftSample * R)(), (abi.SessionOutcome * S)()
+    out.decisions = C.cast(dec, C.POINTER(abi.Decision))
+    out.ttft_samples = C.cast(ttft, C.POINTER(abi.TtftSample))
+    out.sessions = C.cast(sess, C.POINTER(abi.SessionOutcome))
+    return out, dec, ttft, sess
+
+
+class EngineError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def host_run(trace, plan, profile, params, seed):
+    out, dec, ttft, sess = _alloc(trace)
+    rc = hostsim().hostsim_run(C.byref(trace), C.byref(plan), C.byref(profile), C.byref(params), seed,
+                               C.byref(out))
+    if rc:
+        raise EngineError(rc, hostsim().hostsim_last_error().decode())
+    return Run(out, dec, ttft, sess)
+
+
+def oracle_kind():
+    from oracle import refbind
+    return "reference" if refbind.available() else "c-oracle"
+
+
+def oracle_run(trace, plan, profile, params, seed):
+    """The checker's run(): the reference itself when built, else the C oracle."""
+    from oracle import refbind
+    if refbind.available():
+        S, R = max(trace.n_sessions, 1), max(trace.n_rounds, 1)
+        out, _, _, _ = refbind.run(trace, plan, profile, params, seed, records=True)
+        dec = [out.decisions[i] for i in range(out.n_decisions)]
+        ttft = [out.ttft_samples[i] for i in range(out.n_ttft)]
+        sess = [out.sessions[i] for i in range(out.n_sessions)]
+        r = Run(out, None, None, None)
+        r.decisions, r.ttft_samples, r.sessions = dec, ttft, sess
+        return r
+    from oracle import cbind
+    return cbind.run(trace, plan, profile, params, seed)
+
+
+DEC_FIELDS = ("time", "session_id", "round", "local", "worker", "rationale", "has_estimate", "estimated_cost")
+TTFT_FIELDS = ("session_id", "round", "kind", "local", "created_time", "completion_time", "value")
+SESS_FIELDS = ("session_id", "arrival_time", "completion_time", "rounds", "admission_wait", "mean_itl",
+               "ttft_ok", "itl_ok", "slo_ok")
+CTR_FIELDS = ("tasks_created", "tasks_completed", "tokens_decoded", "kv_bytes_residual",
+              "max_postpone_observed", "events_in_order")
+ATT_FIELDS = ("sessions_completed", "slo_ok", "ttft_ok", "itl_ok")
+
+
+def _tup(rec, fields):
+    return tuple(getattr(rec, f) for f in fields)
+
+
+def diff_runs(got, want):
+    """Returns a list of human-readable mismatches (empty = bit-identical)."""
+    errs = []
+    for f in CTR_FIELDS:
+        if getattr(got.counters, f) != getattr(want.counters, f):
+            errs.append(f"counter {f}: {getattr(got.counters, f)} != {getattr(want.counters, f)}")
+    for f in ATT_FIELDS:
+        if getattr(got.attainment, f) != getattr(want.attainment, f):
+            errs.append(f"attainment {f}: {getattr(got.attainment, f)} != {getattr(want.attainment, f)}")
+    for name, fields in (("decisions", DEC_FIELDS), ("ttft_samples", TTFT_FIELDS), ("sessions", SESS_FIELDS)):
+        a, b = getattr(got, name), getattr(want, name)
+        if len(a) != len(b):
+            errs.append(f"{name}: {len(a)} records != {len(b)}")
+        for i, (x, y) in enumerate(zip(a, b)):
+            tx, ty = _tup(x, fields), _tup(y, fields)
+            if name == "decisions" and not x.has_estimate:
+                tx, ty = tx[:-1], ty[:-1]
+            if tx != ty:
+                errs.append(f"{name}[{i}]: {tx} != {ty}")
+                break
+    return errs
+
+
+def assert_same_run(got, want):
+    errs = diff_runs(got, want)
+    assert not errs, "\n".join(errs[:10])
