@@ -236,6 +236,8 @@ typedef struct pdsim_search_output {
   pdsim_counters* pair_counters;
   int8_t* pair_status;
   int64_t* candidate_slo_ok;
+  int64_t* pair_events;   /* diagnostics: dynamic events replayed per pair */
+  int64_t* pair_cycles;   /* diagnostics: SM clock ticks spent per pair */
   int32_t best_candidate;
   int32_t reserved;
   int64_t best_slo_ok;

@@ -173,6 +173,8 @@ class SearchOutput(C.Structure):
         ("pair_counters", C.POINTER(Counters)),
         ("pair_status", C.POINTER(C.c_int8)),
         ("candidate_slo_ok", C.POINTER(C.c_int64)),
+        ("pair_events", C.POINTER(C.c_int64)),
+        ("pair_cycles", C.POINTER(C.c_int64)),
         ("best_candidate", C.c_int32),
         ("reserved", C.c_int32),
         ("best_slo_ok", C.c_int64),

@@ -143,8 +143,10 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     } else {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
+      const long long t0 = clock64();
       pdg::Engine eng(tr, pl, c_profile, a.params, a.caps, slot, a.rec, a.seed);
       eng.run(&res);
+      res.cycles = clock64() - t0;
     }
     a.results[pair - a.pair_begin] = res;
     if (res.status != PDSIM_PAIR_OK) {
@@ -381,6 +383,8 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
       if (out->pair_attainment) out->pair_attainment[k] = res[static_cast<size_t>(k)].att;
       if (out->pair_counters) out->pair_counters[k] = res[static_cast<size_t>(k)].ctr;
       if (out->pair_status) out->pair_status[k] = static_cast<int8_t>(res[static_cast<size_t>(k)].status);
+      if (out->pair_events) out->pair_events[k] = res[static_cast<size_t>(k)].events;
+      if (out->pair_cycles) out->pair_cycles[k] = res[static_cast<size_t>(k)].cycles;
     }
     if (out->candidate_slo_ok) {
       for (int c = 0; c < C; ++c) out->candidate_slo_ok[c] = cbad[c] ? -1 : static_cast<int64_t>(csum[c]);

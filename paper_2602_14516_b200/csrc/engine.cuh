@@ -26,6 +26,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "exactsum.cuh"
 #include "fold.cuh"
 
 namespace pdg {
@@ -101,19 +102,28 @@ struct SessRt {
   int8_t reserved[7];
 };
 
+// A worker's task queue: ring counters + exact sum of the queued costs.
+struct TaskQueue {
+  ExactSum sum;
+  uint32_t qh, qt;
+  uint32_t reserved[2];
+};
+
 struct PrefillW {
+  TaskQueue q;
+  ExactSum tw;      // exact sum of the TTFT window
   int32_t deg;
-  uint32_t qh, qt;  // queue ring counters
   int32_t cur, stg;
+  uint32_t th, tt;  // TTFT window ring counters
+  int8_t computing, staged, pending, reserved;
   double cur_cost, stg_cost;
   double staged_ready;
-  int8_t computing, staged, pending, reserved;
-  uint32_t th, tt;  // TTFT window ring counters
 };
 
 struct DecodeW {
+  TaskQueue q;      // local prefill queue
+  ExactSum iw;      // exact sum of the ITL window (terms = samples)
   int32_t deg;
-  uint32_t qh, qt;
   int32_t cur;
   double cur_cost;
   int64_t kv_used;
@@ -123,7 +133,6 @@ struct DecodeW {
   int32_t steps;  // steps started
   int32_t fh_n;   // finisher-heap size
   uint32_t ih, it;  // ITL-run ring counters
-  int64_t itl_n;    // samples currently in the ITL window
 };
 
 // Capacities of one workspace slot (host-computed upper bounds).
@@ -199,12 +208,16 @@ struct Records {
   pdsim_session_outcome* sessions;  // [S], termination order
 };
 
+
 struct PairResult {
   pdsim_attainment att;
   pdsim_counters ctr;
   int64_t n_decisions;
   int64_t n_ttft;
-  int32_t status;  // PDSIM_PAIR_*
+  int64_t events;        // dynamic events processed (diagnostics)
+  int64_t cycles;        // device clock64() ticks for this pair (0 on host)
+  int64_t exact_folds;   // certified comparisons that fell back to a fold
+  int32_t status;        // PDSIM_PAIR_*
   int32_t reserved;
 };
 
@@ -214,6 +227,14 @@ struct RouteOut {
   int32_t rationale;
   int32_t has_est;
   double est;
+};
+
+// A routing cost estimate: exact value, or a certified bracket around the
+// reference's fold (exactsum.cuh).
+struct Est {
+  double lo, hi;
+  int32_t exact;
+  int32_t who;  // -1 local, else prefill worker index
 };
 
 class Engine {
@@ -238,6 +259,7 @@ class Engine {
         continue;
       }
       const Event ev = heap_pop();
+      ++events_;
       advance_to(ev.t);
       const uint32_t kind = static_cast<uint32_t>(ev.key >> 56);
       switch (kind) {
@@ -254,6 +276,8 @@ class Engine {
     out->ctr = ctr_;
     out->n_decisions = n_dec_;
     out->n_ttft = n_ttft_;
+    out->events = events_;
+    out->exact_folds = folds_;
     out->status = failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
   }
 
@@ -279,6 +303,8 @@ class Engine {
   pdsim_counters ctr_{};
   int64_t n_dec_ = 0;
   int64_t n_ttft_ = 0;
+  int64_t events_ = 0;
+  int64_t folds_ = 0;
 
   PDG_HD void fail() { failed_ = true; }
 
@@ -298,18 +324,22 @@ class Engine {
     mt64_seed(W.mt, &mt_idx_, seed_);
     for (int p = 0; p < PL.P; ++p) {
       PrefillW& w = W.pw[p];
+      w.q.sum.clear();
+      w.q.qh = w.q.qt = 0;
+      w.tw.clear();
       w.deg = PL.pdeg[p];
-      w.qh = w.qt = 0;
       w.cur = w.stg = -1;
+      w.th = w.tt = 0;
+      w.computing = w.staged = w.pending = 0;
       w.cur_cost = w.stg_cost = 0.0;
       w.staged_ready = 0.0;
-      w.computing = w.staged = w.pending = 0;
-      w.th = w.tt = 0;
     }
     for (int d = 0; d < PL.D; ++d) {
       DecodeW& w = W.dw[d];
+      w.q.sum.clear();
+      w.q.qh = w.q.qt = 0;
+      w.iw.clear();
       w.deg = PL.ddeg[d];
-      w.qh = w.qt = 0;
       w.cur = -1;
       w.cur_cost = 0.0;
       w.kv_used = 0;
@@ -319,7 +349,6 @@ class Engine {
       w.steps = 0;
       w.fh_n = 0;
       w.ih = w.it = 0;
-      w.itl_n = 0;
     }
   }
 
@@ -482,7 +511,7 @@ class Engine {
       }
       const double thr = dmul(PR.alpha, T.ttft_thres);
       for (int k = 0; k < n; ++k) {
-        if (ttft_query(order[k]) <= thr) {
+        if (ttft_has_slack(order[k], thr)) {
           r.local = 0;
           r.p = order[k];
           r.rationale = PDSIM_RATIONALE_SLACK_REMOTE;
@@ -490,62 +519,123 @@ class Engine {
         }
       }
     }
-    if (itl_query(s.bound) <= dmul(PR.beta, T.itl_thres)) {
+    if (itl_has_slack(s.bound, dmul(PR.beta, T.itl_thres))) {
       r.local = 1;
       r.p = -1;
       r.rationale = PDSIM_RATIONALE_SLACK_LOCAL;
       return r;
     }
+    // Cost comparison; ties prefer local, then the lowest worker index.
     r.local = 1;
     r.p = -1;
     r.rationale = PDSIM_RATIONALE_ARGMIN;
-    double best = estimate_local(i, s.bound);
+    Est best = est_local(i, s.bound);
     for (int p = 0; p < n; ++p) {
-      const double c = estimate_remote(i, p, s.bound);
-      if (c < best) {
+      Est c = est_remote(i, p, s.bound);
+      if (est_less(c, best, i, s.bound)) {
         best = c;
         r.local = 0;
         r.p = p;
       }
     }
     r.has_est = 1;
-    r.est = best;
+    if (REC.decisions && !best.exact) resolve(best, i, s.bound);
+    r.est = best.lo;
     return r;
   }
 
-  // estimate_local / estimate_remote (coordinator.cpp:74-100): sequential
-  // folds over the queued tasks' costs, head first.
-  PDG_HD double estimate_local(int32_t i, int d) const {
-    const DecodeW& w = W.dw[d];
-    double c = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    const double* qc = W.dq_c + static_cast<size_t>(d) * C.qcap;
+  // ---- routing estimates (coordinator.cpp:74-100) ----
+  // Exact sequential folds (the reference's arithmetic).
+  PDG_HD double fold_queue(const TaskQueue& q, const double* qc, double init) const {
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
-    for (uint32_t k = w.qh; k != w.qt; ++k) c = dadd(c, qc[k & mask]);
+    double c = init;
+    for (uint32_t k = q.qh; k != q.qt; ++k) c = dadd(c, qc[k & mask]);
     return c;
   }
-
-  PDG_HD double estimate_remote(int32_t i, int p, int d) const {
-    const PrefillW& w = W.pw[p];
-    const int dd = W.dw[d].deg;
+  PDG_HD double local_exact(int32_t i, int d) {
+    ++folds_;
+    const DecodeW& w = W.dw[d];
+    return fold_queue(w.q, W.dq_c + static_cast<size_t>(d) * C.qcap, t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg));
+  }
+  PDG_HD double remote_head(int32_t i, int p, int d) const {
+    const int pd = W.pw[p].deg, dd = W.dw[d].deg;
     const int32_t hist = W.sess[i].ctx;
     const int32_t incr = l_incr_of(i);
-    const double t_pre = t_prefill(hist, incr, w.deg);
-    const double legs = dadd(t_kv(hist, dd, w.deg), t_kv(incr, w.deg, dd));
-    double tq = 0.0;
-    const double* qc = W.pq_c + static_cast<size_t>(p) * C.qcap;
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
-    for (uint32_t k = w.qh; k != w.qt; ++k) tq = dadd(tq, qc[k & mask]);
-    return dadd(dadd(t_pre, legs), tq);
+    return dadd(t_prefill(hist, incr, pd), dadd(t_kv(hist, dd, pd), t_kv(incr, pd, dd)));
+  }
+  PDG_HD double remote_exact(int32_t i, int p, int d) {
+    ++folds_;
+    const double tq = fold_queue(W.pw[p].q, W.pq_c + static_cast<size_t>(p) * C.qcap, 0.0);
+    return dadd(remote_head(i, p, d), tq);
+  }
+  PDG_HD static Est exact_est(double v, int who) {
+    Est e;
+    e.lo = e.hi = v;
+    e.exact = 1;
+    e.who = who;
+    return e;
+  }
+  // head + fold(queue) of `len` non-negative terms, with exact queue sum.
+  PDG_HD static Est bracket_est(double head, const ExactSum& qs, int64_t nterms, int who) {
+    Est e;
+    const double v = dadd(head, fx_to_double(qs.sum));
+    const double m = fold_margin(nterms);
+    e.lo = v * (1.0 - m);
+    e.hi = v * (1.0 + m);
+    e.exact = 0;
+    e.who = who;
+    return e;
+  }
+  PDG_HD Est est_local(int32_t i, int d) {
+    const DecodeW& w = W.dw[d];
+    const uint32_t len = w.q.qt - w.q.qh;
+    const double own = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
+    if (len <= 2 || !w.q.sum.exact()) {
+      return exact_est(fold_queue(w.q, W.dq_c + static_cast<size_t>(d) * C.qcap, own), -1);
+    }
+    return bracket_est(own, w.q.sum, static_cast<int64_t>(len) + 1, -1);
+  }
+  PDG_HD Est est_remote(int32_t i, int p, int d) {
+    const PrefillW& w = W.pw[p];
+    const uint32_t len = w.q.qt - w.q.qh;
+    const double head = remote_head(i, p, d);
+    if (len <= 2 || !w.q.sum.exact()) {
+      return exact_est(dadd(head, fold_queue(w.q, W.pq_c + static_cast<size_t>(p) * C.qcap, 0.0)), p);
+    }
+    return bracket_est(head, w.q.sum, static_cast<int64_t>(len), p);
+  }
+  PDG_HD void resolve(Est& e, int32_t i, int d) {
+    if (e.exact) return;
+    const double v = e.who < 0 ? local_exact(i, d) : remote_exact(i, e.who, d);
+    e = exact_est(v, e.who);
+  }
+  // `c < b` on the reference's values.
+  PDG_HD bool est_less(Est& c, Est& b, int32_t i, int d) {
+    if (!(c.exact && b.exact)) {
+      if (c.hi < b.lo) return true;
+      if (c.lo >= b.hi) return false;
+      resolve(c, i, d);
+      resolve(b, i, d);
+    }
+    return c.lo < b.lo;
   }
 
   // ---- windowed statistics (coordinator.cpp:27-47) ----
+  PDG_HD void ttft_trim(PrefillW& w, const double* tt, const double* tv) {
+    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
+    const double cutoff = dsub(now_, PR.stat_window);
+    while (w.th != w.tt && tt[w.th & mask] <= cutoff) {
+      w.tw.remove(tv[w.th & mask]);
+      ++w.th;
+    }
+  }
+
   PDG_HD void ttft_add(int p, double v) {
     PrefillW& w = W.pw[p];
     const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
     double* tt = W.tw_t + static_cast<size_t>(p) * C.twcap;
     double* tv = W.tw_v + static_cast<size_t>(p) * C.twcap;
-    const double cutoff = dsub(now_, PR.stat_window);
-    while (w.th != w.tt && tt[w.th & mask] <= cutoff) ++w.th;
+    ttft_trim(w, tt, tv);
     if (w.tt - w.th >= static_cast<uint32_t>(C.twcap)) {
       fail();
       return;
@@ -553,32 +643,41 @@ class Engine {
     tt[w.tt & mask] = now_;
     tv[w.tt & mask] = v;
     ++w.tt;
+    w.tw.add(v);
   }
 
-  PDG_HD double ttft_query(int p) {
+  // query(now) <= thr, where query is the sequential windowed mean.
+  PDG_HD bool ttft_has_slack(int p, double thr) {
     PrefillW& w = W.pw[p];
-    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
     const double* tt = W.tw_t + static_cast<size_t>(p) * C.twcap;
     const double* tv = W.tw_v + static_cast<size_t>(p) * C.twcap;
-    const double cutoff = dsub(now_, PR.stat_window);
-    while (w.th != w.tt && tt[w.th & mask] <= cutoff) ++w.th;
-    if (w.th == w.tt) return 0.0;
+    ttft_trim(w, tt, tv);
+    if (w.th == w.tt) return 0.0 <= thr;  // empty window reads 0
+    const int dec = mean_le_certified(w.tw, thr);
+    if (dec >= 0) return dec == 1;
+    ++folds_;
+    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
     double sum = 0.0;
     for (uint32_t k = w.th; k != w.tt; ++k) sum = dadd(sum, tv[k & mask]);
-    return ddiv(sum, static_cast<double>(w.tt - w.th));
+    return ddiv(sum, static_cast<double>(w.tt - w.th)) <= thr;
+  }
+
+  PDG_HD void itl_trim(DecodeW& w, const double* it, const double* ig, const uint32_t* ic) {
+    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
+    const double cutoff = dsub(now_, PR.stat_window);
+    while (w.ih != w.it && it[w.ih & mask] <= cutoff) {
+      w.iw.remove(ig[w.ih & mask], ic[w.ih & mask]);
+      ++w.ih;
+    }
   }
 
   PDG_HD void itl_add(int d, double gap, uint32_t count) {
     DecodeW& w = W.dw[d];
     const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
     double* it = W.iw_t + static_cast<size_t>(d) * C.iwcap;
-    uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
     double* ig = W.iw_g + static_cast<size_t>(d) * C.iwcap;
-    const double cutoff = dsub(now_, PR.stat_window);
-    while (w.ih != w.it && it[w.ih & mask] <= cutoff) {
-      w.itl_n -= ic[w.ih & mask];
-      ++w.ih;
-    }
+    uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
+    itl_trim(w, it, ig, ic);
     if (w.it - w.ih >= static_cast<uint32_t>(C.iwcap)) {
       fail();
       return;
@@ -587,38 +686,51 @@ class Engine {
     ig[w.it & mask] = gap;
     ic[w.it & mask] = count;
     ++w.it;
-    w.itl_n += count;
+    w.iw.add(gap, count);
   }
 
-  PDG_HD double itl_query(int d) {
+  PDG_HD bool itl_has_slack(int d, double thr) {
     DecodeW& w = W.dw[d];
-    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
     const double* it = W.iw_t + static_cast<size_t>(d) * C.iwcap;
-    const uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
     const double* ig = W.iw_g + static_cast<size_t>(d) * C.iwcap;
-    const double cutoff = dsub(now_, PR.stat_window);
-    while (w.ih != w.it && it[w.ih & mask] <= cutoff) {
-      w.itl_n -= ic[w.ih & mask];
-      ++w.ih;
-    }
-    if (w.ih == w.it) return 0.0;
+    const uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
+    itl_trim(w, it, ig, ic);
+    if (w.ih == w.it) return 0.0 <= thr;
+    const int dec = mean_le_certified(w.iw, thr);
+    if (dec >= 0) return dec == 1;
+    ++folds_;
+    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
     double sum = 0.0;
     for (uint32_t k = w.ih; k != w.it; ++k) sum = fold_repeat(sum, ig[k & mask], ic[k & mask]);
-    return ddiv(sum, static_cast<double>(w.itl_n));
+    return ddiv(sum, static_cast<double>(w.iw.terms)) <= thr;
   }
 
   // ---- queues + reorder (reorder.cpp:76-146; select_next sim_engine.cpp:335-350) ----
-  // Dequeues the next task of a worker queue (ring `qs/qc`, counters qh/qt).
-  PDG_HD int32_t select_next(int32_t* qs, double* qc, uint32_t& qh, uint32_t qt, double* cost) {
+  PDG_HD bool queue_push(TaskQueue& q, int32_t* qs, double* qc, int32_t i, double cost) {
+    if (q.qt - q.qh >= static_cast<uint32_t>(C.qcap)) {
+      fail();
+      return false;
+    }
+    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+    qs[q.qt & mask] = i;
+    qc[q.qt & mask] = cost;
+    ++q.qt;
+    q.sum.add(cost);
+    return true;
+  }
+
+  // Dequeues the next task (after reordering the head window).
+  PDG_HD int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
     if (PR.reorder) {
-      const uint32_t len = qt - qh;
+      const uint32_t len = q.qt - q.qh;
       const int m = static_cast<int>(len < static_cast<uint32_t>(PR.window) ? len : PR.window);
-      if (m > 1) reorder_head(qs, qc, qh, m);
+      if (m > 1) reorder_head(qs, qc, q.qh, m);
     }
-    const int32_t i = qs[qh & mask];
-    *cost = qc[qh & mask];
-    ++qh;
+    const int32_t i = qs[q.qh & mask];
+    *cost = qc[q.qh & mask];
+    ++q.qh;
+    q.sum.remove(*cost);
     const int32_t pc = W.sess[i].postpone;
     if (pc > ctr_.max_postpone_observed) ctr_.max_postpone_observed = pc;
     return i;
@@ -642,6 +754,7 @@ class Engine {
     int perm[8], best[8];
     for (int k = 0; k < m; ++k) perm[k] = best[k] = k;
     int best_sat = count_satisfied(perm, m, hc, wait, thres);
+    if (best_sat == m) return;  // identity already satisfies every task: no strict improvement exists
     while (next_permutation(perm, m)) {
       bool allowed = true;
       for (int k = 0; k < m; ++k) {
@@ -655,6 +768,7 @@ class Engine {
       if (sat > best_sat) {
         best_sat = sat;
         for (int k = 0; k < m; ++k) best[k] = perm[k];
+        if (best_sat == m) break;  // cannot be strictly improved upon
       }
     }
     for (int k = 0; k < m; ++k) {
@@ -693,24 +807,12 @@ class Engine {
     return true;
   }
 
-  PDG_HD bool queue_push(int32_t* qs, double* qc, uint32_t qh, uint32_t& qt, int32_t i, double cost) {
-    if (qt - qh >= static_cast<uint32_t>(C.qcap)) {
-      fail();
-      return false;
-    }
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
-    qs[qt & mask] = i;
-    qc[qt & mask] = cost;
-    ++qt;
-    return true;
-  }
-
   // ---- prefill workers (sim_engine.cpp:354-453) ----
   PDG_HD void enqueue_remote(int p, int32_t i) {
     PrefillW& w = W.pw[p];
     const double cost = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    if (!queue_push(W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap,
-                    w.qh, w.qt, i, cost))
+    if (!queue_push(w.q, W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap, i,
+                    cost))
       return;
     try_stage(p);
     try_start_compute(p);
@@ -718,9 +820,9 @@ class Engine {
 
   PDG_HD void try_stage(int p) {
     PrefillW& w = W.pw[p];
-    if (w.staged || w.qh == w.qt) return;
-    w.stg = select_next(W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap,
-                        w.qh, w.qt, &w.stg_cost);
+    if (w.staged || w.q.qh == w.q.qt) return;
+    w.stg = select_next(w.q, W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap,
+                        &w.stg_cost);
     w.staged = 1;
     const int32_t hist = W.sess[w.stg].ctx;
     if (hist > 0) {
@@ -816,8 +918,8 @@ class Engine {
   PDG_HD void enqueue_local(int d, int32_t i) {
     DecodeW& w = W.dw[d];
     const double cost = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    if (!queue_push(W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap,
-                    w.qh, w.qt, i, cost))
+    if (!queue_push(w.q, W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap, i,
+                    cost))
       return;
     advance_decode(d);
   }
@@ -825,10 +927,10 @@ class Engine {
   PDG_HD void advance_decode(int d) {
     DecodeW& w = W.dw[d];
     if (w.stepping || w.prefilling) return;
-    if (w.qh != w.qt) {
+    if (w.q.qh != w.q.qt) {
       // Local prefill preempts decoding until the queue drains.
-      w.cur = select_next(W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap,
-                          w.qh, w.qt, &w.cur_cost);
+      w.cur = select_next(w.q, W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap,
+                          &w.cur_cost);
       w.prefilling = 1;
       schedule(dadd(now_, w.cur_cost), kPrefillDone, static_cast<uint32_t>(PL.P + d), 0u);
       return;
@@ -860,7 +962,11 @@ class Engine {
 
     bool any_terminated = false;
     uint64_t* fh = W.fh + static_cast<size_t>(d) * C.fcap;
-    while (w.fh_n > 0 && static_cast<int32_t>(fh[0] >> 32) == k) {
+    while (w.fh_n > 0 && static_cast<int32_t>(fh[0] >> 32) <= k) {
+      if (static_cast<int32_t>(fh[0] >> 32) < k) {  // a round end was missed: invariant broken
+        fail();
+        return;
+      }
       const uint32_t rank = static_cast<uint32_t>(fh[0]);
       fh_pop(d);
       const int32_t i = T.by_rank[rank];

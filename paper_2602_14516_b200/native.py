@@ -171,6 +171,7 @@ class SearchResult:
         self.pair_status = st
         self.candidate_slo_ok = cand
         self.n_pairs = n_pairs
+        self.pair_events, self.pair_cycles = out._diag
 
 
 def search_input(traces, plans, pair_begin=0, pair_end=-1):
@@ -234,8 +235,12 @@ class Context:
         ctr = (abi.Counters * max(n_pairs, 1))()
         st = (C.c_int8 * max(n_pairs, 1))()
         cand = (C.c_int64 * max(n_cand, 1))()
+        ev = (C.c_int64 * max(n_pairs, 1))()
+        cy = (C.c_int64 * max(n_pairs, 1))()
         out = abi.SearchOutput(C.cast(att, C.POINTER(abi.Attainment)), C.cast(ctr, C.POINTER(abi.Counters)),
-                               C.cast(st, C.POINTER(C.c_int8)), C.cast(cand, C.POINTER(C.c_int64)))
+                               C.cast(st, C.POINTER(C.c_int8)), C.cast(cand, C.POINTER(C.c_int64)),
+                               C.cast(ev, C.POINTER(C.c_int64)), C.cast(cy, C.POINTER(C.c_int64)))
+        out._diag = (ev, cy)
         return out, att, ctr, st, cand
 
     def plan_search(self, traces, plans, profile, params, seed, pair_begin=0, pair_end=-1):

@@ -1,0 +1,31 @@
+"""Per-pair GPU diagnostics for a workload: events and SM cycles per pair."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_14516_b200 import abi, native, workloads  # noqa: E402
+
+
+def main(cfg="C2"):
+    wl = workloads.CONFIGS[cfg]()
+    with native.Context(0) as ctx:
+        ctx.stage(wl.traces, wl.plans, wl.profile, wl.params)
+        ctx.search_staged(wl.seed)
+        t0 = time.time()
+        res = ctx.search_staged(wl.seed)
+        wall = time.time() - t0
+    rows = []
+    for p in range(res.n_pairs):
+        rows.append((res.pair_cycles[p], res.pair_events[p], p, abi.format_plan(wl.plans[p // len(wl.traces)])))
+    rows.sort(reverse=True)
+    out = {"config": cfg, "kernel_ms": res.kernel_ms, "wall_s": wall, "pairs": res.n_pairs,
+           "top": [{"cycles": c, "events": e, "ns_per_event_at_1.965GHz": c / 1.965 / max(e, 1), "pair": p,
+                    "plan": s} for c, e, p, s in rows[:10]],
+           "total_events": sum(r[1] for r in rows), "total_cycles": sum(r[0] for r in rows)}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
