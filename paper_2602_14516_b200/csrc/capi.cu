@@ -76,7 +76,8 @@ struct pdsim_gpu_ctx {
   std::vector<pdg::DevPlan> plans;
   std::vector<int8_t> pair_invalid;  // [n_candidates * n_traces], host precheck
   pdg::Caps caps{};
-  size_t slot_bytes = 0;
+  size_t slot_bytes = 0;   // global workspace per slot
+  size_t smem_bytes = 0;   // dynamic shared memory per slot (one warp / block)
   DevBuf d_trace_data, d_traces, d_plans, d_invalid;
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
@@ -117,6 +118,7 @@ struct KernelArgs {
   pdg::Caps caps;
   char* ws;
   size_t slot_bytes;
+  size_t smem_bytes;
   unsigned long long* next_pair;
   pdg::PairResult* results;            // [pair_end - pair_begin]
   unsigned long long* cand_sum;        // [n_candidates]
@@ -125,13 +127,20 @@ struct KernelArgs {
   uint64_t seed;
 };
 
+// One warp per block; the warp replays pairs pulled from an atomic queue.
 __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
-  if ((threadIdx.x & 31) != 0) return;  // v1: lane 0 runs the serial replay
+  extern __shared__ __align__(16) char smem[];
   const int slot_id = blockIdx.x;
-  pdg::Slot slot;
-  pdg::slot_bytes(a.caps, &slot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
+  pdg::GlobalSlot gslot;
+  pdg::global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
+  pdg::SmemSlot sslot;
+  pdg::smem_slot_bytes(a.caps, &sslot, smem);
+  const int lane = threadIdx.x & 31;
   for (;;) {
-    const int64_t pair = static_cast<int64_t>(atomicAdd(a.next_pair, 1ull)) + a.pair_begin;
+    unsigned long long ticket = 0;
+    if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    const int64_t pair = static_cast<int64_t>(ticket) + a.pair_begin;
     if (pair >= a.pair_end) break;
     const int32_t c = static_cast<int32_t>(pair / a.n_traces);
     const int32_t r = static_cast<int32_t>(pair % a.n_traces);
@@ -144,16 +153,19 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      pdg::Engine eng(tr, pl, c_profile, a.params, a.caps, slot, a.rec, a.seed);
+      pdg::Engine eng(tr, pl, c_profile, a.params, a.caps, sslot, gslot, a.rec, a.seed);
       eng.run(&res);
       res.cycles = clock64() - t0;
     }
-    a.results[pair - a.pair_begin] = res;
-    if (res.status != PDSIM_PAIR_OK) {
-      atomicOr(&a.cand_bad[c], 1);
-    } else {
-      atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+    if (lane == 0) {
+      a.results[pair - a.pair_begin] = res;
+      if (res.status != PDSIM_PAIR_OK) {
+        atomicOr(&a.cand_bad[c], 1);
+      } else {
+        atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+      }
     }
+    __syncwarp();
   }
 }
 
@@ -234,8 +246,14 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
 
   std::vector<const pdg::PackedTrace*> tp;
   for (auto& t : ctx->packed) tp.push_back(&t);
-  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params);
-  ctx->slot_bytes = pdg::slot_bytes(ctx->caps, nullptr, nullptr);
+  // Shared-memory budget per slot: generous when few pairs run at once.
+  const int64_t pairs = static_cast<int64_t>(in->n_traces) * in->n_candidates;
+  const size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
+                             : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
+                                                          : (size_t(12) << 10);
+  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params, smem_budget);
+  ctx->slot_bytes = pdg::global_slot_bytes(ctx->caps, nullptr, nullptr);
+  ctx->smem_bytes = pdg::smem_slot_bytes(ctx->caps, nullptr, nullptr);
   ctx->profile = *profile;
   ctx->params = *params;
   ctx->n_traces = in->n_traces;
@@ -310,7 +328,9 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   size_t free_b = 0, total_b = 0;
   CU(ctx, cudaMemGetInfo(&free_b, &total_b));
   const size_t budget = std::min<size_t>(free_b / 2 + ctx->d_ws.bytes / 2, size_t(64) << 30);
-  int64_t slots = std::min<int64_t>(std::max<int64_t>(n, 1), static_cast<int64_t>(ctx->sm_count) * 32);
+  const int64_t per_sm = std::max<int64_t>(
+      1, std::min<int64_t>(32, static_cast<int64_t>((size_t(227) << 10) / std::max<size_t>(ctx->smem_bytes, 1))));
+  int64_t slots = std::min<int64_t>(std::max<int64_t>(n, 1), static_cast<int64_t>(ctx->sm_count) * per_sm);
   slots = std::min<int64_t>(slots, static_cast<int64_t>(budget / std::max<size_t>(ctx->slot_bytes, 1)));
   if (slots < 1) return set_err(ctx, PDSIM_ERR_CUDA, "search: workspace of one slot exceeds device memory");
   CU(ctx, ctx->d_ws.reserve(ctx->slot_bytes * static_cast<size_t>(slots)));
@@ -337,6 +357,7 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.caps = ctx->caps;
   a.ws = ctx->d_ws.as<char>();
   a.slot_bytes = ctx->slot_bytes;
+  a.smem_bytes = ctx->smem_bytes;
   a.next_pair = ctx->d_counter.as<unsigned long long>();
   a.results = ctx->d_results.as<pdg::PairResult>();
   a.cand_sum = ctx->d_cand_sum.as<unsigned long long>();
@@ -346,7 +367,9 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   int64_t launches = 0;
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
-    replay_kernel<<<static_cast<unsigned>(slots), 32, 0, ctx->stream>>>(a);
+    CU(ctx, cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(ctx->smem_bytes)));
+    replay_kernel<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;
     CU(ctx, cudaGetLastError());
   }

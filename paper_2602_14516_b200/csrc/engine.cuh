@@ -1,28 +1,39 @@
-// engine.cuh — the replay of one (candidate plan, trace replica) pair.
+// engine.cuh — the replay of one (candidate plan, trace replica) pair by one
+// warp.
 //
 // Behavioural restatement, for B200, of the reference discrete-event engine
-// (proj/src/sim_engine.cpp:107-632) together with the routing
+// (proj/src/sim_engine.cpp:107-632) and of the routing
 // (proj/src/coordinator.cpp:27-171) and reordering (proj/src/reorder.cpp:44-146)
 // policies it calls. Every observable — routing decisions, TTFT samples,
-// session verdicts, counters — is reproduced bit-for-bit; the data structures
-// are re-designed for a GPU:
-//  * a task is identified by its session (each session has at most one task
-//    in flight), so queues and events carry 32-bit session indices;
-//  * the admission queue is the index range [adm_head, next_arrival) because
-//    sessions park in arrival order (sim_engine.cpp:240-267);
-//  * arrivals are not heap events: they are read in trace order and merged
-//    with the dynamic-event heap (kind 0 wins ties, sim_engine.cpp:48-74);
-//  * decode batches are never materialised: a session in the batch finishes
-//    its round at step join + decode_len - 1, so a per-worker min-heap keyed
-//    by (end_step, session-id rank) yields exactly the finishing cohort
-//    members in cohort order (sim_engine.cpp:514-517, 536-577) at O(log n)
-//    per round instead of O(batch) per token;
-//  * per-session ITL sums are folded at round end from a ring of step end
-//    times (every ITL gap of a step equals now - previous step end);
-//  * the ITL window keeps one (time, gap, count) run per step and folds it
-//    with fold_repeat() (fold.cuh), exact to the last bit.
-// The same source is compiled for the GPU (the product) and, in tests only,
-// for the host so the engine logic can be checked without a device.
+// session verdicts, counters — is reproduced bit-for-bit. The data layout is
+// re-designed for the GPU:
+//
+//  * Warp-uniform execution. All 32 lanes run the event loop in lock-step on
+//    identical scalar state (kept in registers); lanes split only where the
+//    work is parallel: the next-event reduction, window trimming (ballot),
+//    the reorder permutation search, routing estimates, the RNG twist.
+//    Shared/global stores of warp-uniform state are issued by lane 0 between
+//    __syncwarp()s.
+//  * Worker events (decode step / local prefill done, prefill compute done,
+//    history read) live in registers: slot s is owned by lane s % 32; the next
+//    event is a 5-step shuffle min over (time, kind<<58 | seq<<6 | slot).
+//    Only session events (interaction done, write-back) use a binary heap, in
+//    shared memory with a global-memory spill area.
+//  * Arrivals are read in trace order and merged (kind 0 wins ties).
+//  * A task is identified by its session (at most one task in flight each).
+//    The admission queue is the index range [adm_head, next_arrival).
+//  * Decode batches are never materialised: a member finishes its round at
+//    step join + decode_len - 1, so a per-worker min-heap keyed by
+//    (end_step, session-id rank) yields the finishing cohort members in cohort
+//    order; per-session ITL sums are folded at round end from a ring of step
+//    end times (every ITL gap of a step is now - previous step end).
+//  * Windowed statistics are lazily trimmed rings with exact 128-bit prefix
+//    sums, so `mean <= threshold` is decided in O(1) (exactsum.cuh); the
+//    sequential fold (fold.cuh for ITL runs) runs only inside the error band.
+//
+// The same source compiles for the GPU (the product; PDG_NL = 32 lanes) and,
+// in tests only, for the host (PDG_NL = 1) so the logic can be checked against
+// the reference without a device.
 #pragma once
 
 #include "common.cuh"
@@ -30,6 +41,90 @@
 #include "fold.cuh"
 
 namespace pdg {
+
+#if defined(__CUDA_ARCH__)
+#define PDG_NL 32
+#else
+#define PDG_NL 1
+#endif
+
+constexpr int kMaxSlots = 64;
+constexpr int kSlotsPerLane = kMaxSlots / PDG_NL;
+constexpr double kInf = __builtin_huge_val();
+
+PDG_HD int lane_id() {
+#if defined(__CUDA_ARCH__)
+  return static_cast<int>(threadIdx.x & 31u);
+#else
+  return 0;
+#endif
+}
+PDG_HD void warp_sync() {
+#if defined(__CUDA_ARCH__)
+  __syncwarp();
+#endif
+}
+PDG_HD uint64_t shfl_xor_u64(uint64_t v, int m) {
+#if defined(__CUDA_ARCH__)
+  return __shfl_xor_sync(0xffffffffu, static_cast<unsigned long long>(v), m);
+#else
+  (void)m;
+  return v;
+#endif
+}
+PDG_HD uint64_t shfl_u64(uint64_t v, int src) {
+#if defined(__CUDA_ARCH__)
+  return __shfl_sync(0xffffffffu, static_cast<unsigned long long>(v), src);
+#else
+  (void)src;
+  return v;
+#endif
+}
+PDG_HD double shfl_d(double v, int src) {
+#if defined(__CUDA_ARCH__)
+  return __shfl_sync(0xffffffffu, v, src);
+#else
+  (void)src;
+  return v;
+#endif
+}
+PDG_HD int shfl_i(int v, int src) {
+#if defined(__CUDA_ARCH__)
+  return __shfl_sync(0xffffffffu, v, src);
+#else
+  (void)src;
+  return v;
+#endif
+}
+PDG_HD uint32_t ballot(bool p) {
+#if defined(__CUDA_ARCH__)
+  return __ballot_sync(0xffffffffu, p);
+#else
+  return p ? 1u : 0u;
+#endif
+}
+PDG_HD int popc(uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  return __popc(b);
+#else
+  return __builtin_popcount(b);
+#endif
+}
+PDG_HD int first_zero(uint32_t bits) {  // index of the lowest clear bit (32 if none)
+  if (bits == 0xffffffffu) return 32;
+#if defined(__CUDA_ARCH__)
+  return __ffs(~bits) - 1;
+#else
+  return __builtin_ctz(~bits);
+#endif
+}
+PDG_HD double warp_min(double v) {
+  for (int m = PDG_NL / 2; m > 0; m >>= 1) {
+    const double o = bitsd(shfl_xor_u64(dbits(v), m));
+    if (o < v) v = o;
+  }
+  return v;
+}
 
 enum EventKind : uint32_t {
   kArrival = 0,
@@ -39,16 +134,21 @@ enum EventKind : uint32_t {
   kDecodeStep = 4,
 };
 
-struct Event {
-  double t;
-  uint64_t key;  // kind << 56 | seq  (sim_engine.cpp:68-74 total order)
-  uint32_t a;    // session index or worker id
-  uint32_t b;    // writeback: session index | 1<<31 ; history read: 0
-};
-
-PDG_HD bool ev_less(const Event& x, const Event& y) {
-  return x.t < y.t || (x.t == y.t && x.key < y.key);
+// Event order key (sim_engine.cpp:68-74): time first, then kind, then the
+// scheduling sequence number; the slot id rides in the low bits (never
+// decisive because seq is unique).
+PDG_HD uint64_t mk_key(uint32_t kind, uint64_t seq, uint32_t slot) {
+  return (static_cast<uint64_t>(kind) << 58) | (seq << 6) | slot;
 }
+PDG_HD bool before(double ta, uint64_t ka, double tb, uint64_t kb) { return ta < tb || (ta == tb && ka < kb); }
+
+// Session event (interaction done: a = session; write-back: a = session, b = prefill worker).
+struct HEv {
+  double t;
+  uint64_t key;
+  uint32_t a;
+  uint32_t b;
+};
 
 // Packed read-only trace (one per replica, shared by all candidates).
 struct DevTrace {
@@ -102,43 +202,53 @@ struct SessRt {
   int8_t reserved[7];
 };
 
-// A worker's task queue: ring counters + exact sum of the queued costs.
+// A worker's task queue (global ring) + exact sum of the queued costs.
 struct TaskQueue {
   ExactSum sum;
   uint32_t qh, qt;
   uint32_t reserved[2];
 };
 
-struct PrefillW {
+// Lazily trimmed window ring (global storage) + running prefix at the tail.
+struct WinState {
+  Pfx tail;
+  uint32_t head, end;
+  uint32_t reserved[2];
+};
+
+struct PrefillW {  // shared memory
   TaskQueue q;
-  ExactSum tw;      // exact sum of the TTFT window
+  WinState tw;  // TTFT window
   int32_t deg;
   int32_t cur, stg;
-  uint32_t th, tt;  // TTFT window ring counters
   int8_t computing, staged, pending, reserved;
   double cur_cost, stg_cost;
   double staged_ready;
 };
 
-struct DecodeW {
-  TaskQueue q;      // local prefill queue
-  ExactSum iw;      // exact sum of the ITL window (terms = samples)
-  int32_t deg;
-  int32_t cur;
-  double cur_cost;
+struct DecodeW {  // shared memory
+  TaskQueue q;  // local prefill queue
+  WinState iw;  // ITL window (runs)
   int64_t kv_used;
   int64_t kv_cap;
-  int8_t stepping, prefilling, reserved[2];
+  uint64_t fh_top;     // cached finisher-heap minimum (valid when fh_n > 0)
+  double cur_cost;
+  double last_step_t;  // end time of the previous step
+  double dur;          // cached t_decode(dur_cohort)
+  int32_t dur_cohort;
+  int32_t deg;
+  int32_t cur;
   int32_t batch_n, n_new, cohort_n, first_n;
   int32_t steps;  // steps started
   int32_t fh_n;   // finisher-heap size
-  uint32_t ih, it;  // ITL-run ring counters
+  int8_t stepping, prefilling, reserved[2];
 };
 
-// Capacities of one workspace slot (host-computed upper bounds).
+// Capacities (host-computed provable upper bounds, see pack.hpp).
 struct Caps {
   int32_t S;      // sessions
-  int32_t hcap;   // event heap
+  int32_t hcap;   // session-event heap (global spill capacity)
+  int32_t hs;     // session-event heap entries kept in shared memory
   int32_t qcap;   // per-worker task queue (power of 2)
   int32_t fcap;   // per-decode-worker finisher heap
   int32_t twcap;  // TTFT window ring (power of 2)
@@ -146,78 +256,100 @@ struct Caps {
   int32_t lcap;   // step-log ring (power of 2)
   int32_t pmax;
   int32_t dmax;
-  int32_t reserved;
 };
 
-// Pointers into one workspace slot.
-struct Slot {
-  SessRt* sess;
-  Event* heap;
-  uint64_t* mt;
+// Shared-memory part of a workspace slot.
+struct SmemSlot {
   PrefillW* pw;
   DecodeW* dw;
+  uint64_t* mt;    // 312 words
+  HEv* heap;       // [hs]
+  int32_t* order;  // [kMaxSlots] routing scan order scratch
+};
+
+// Global-memory part of a workspace slot.
+struct GlobalSlot {
+  SessRt* sess;
+  HEv* heap;  // spill area [hcap]
   int32_t* pq_s;
   double* pq_c;
-  double* tw_t;
-  double* tw_v;
   int32_t* dq_s;
   double* dq_c;
-  uint64_t* fh;
-  double* slog;
+  double* tw_t;
+  double* tw_v;
+  Pfx* tw_p;
   double* iw_t;
   double* iw_g;
   uint32_t* iw_c;
+  Pfx* iw_p;
+  uint64_t* fh;
+  double* slog;
 };
 
 PDG_HD size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+PDG_HD size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
-// Bytes of one slot and the carving of a base pointer into a Slot.
-PDG_HD size_t slot_bytes(const Caps& c, Slot* s, char* base) {
+PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = base ? base + off : nullptr;
+    off = align16(off + bytes);
+    return p;
+  };
+  SmemSlot t;
+  t.pw = reinterpret_cast<PrefillW*>(take(sizeof(PrefillW) * static_cast<size_t>(c.pmax > 0 ? c.pmax : 1)));
+  t.dw = reinterpret_cast<DecodeW*>(take(sizeof(DecodeW) * static_cast<size_t>(c.dmax)));
+  t.mt = reinterpret_cast<uint64_t*>(take(8 * 312));
+  t.heap = reinterpret_cast<HEv*>(take(sizeof(HEv) * static_cast<size_t>(c.hs)));
+  t.order = reinterpret_cast<int32_t*>(take(4 * kMaxSlots));
+  if (s) *s = t;
+  return off;
+}
+
+PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
   size_t off = 0;
   auto take = [&](size_t bytes) -> char* {
     char* p = base ? base + off : nullptr;
     off = align_up(off + bytes);
     return p;
   };
-  const size_t P = static_cast<size_t>(c.pmax), D = static_cast<size_t>(c.dmax);
-  Slot t;
+  const size_t P = static_cast<size_t>(c.pmax > 0 ? c.pmax : 1), D = static_cast<size_t>(c.dmax);
+  GlobalSlot t;
   t.sess = reinterpret_cast<SessRt*>(take(sizeof(SessRt) * static_cast<size_t>(c.S)));
-  t.heap = reinterpret_cast<Event*>(take(sizeof(Event) * static_cast<size_t>(c.hcap)));
-  t.mt = reinterpret_cast<uint64_t*>(take(8 * 313));
-  t.pw = reinterpret_cast<PrefillW*>(take(sizeof(PrefillW) * (P ? P : 1)));
-  t.dw = reinterpret_cast<DecodeW*>(take(sizeof(DecodeW) * D));
+  t.heap = reinterpret_cast<HEv*>(take(sizeof(HEv) * static_cast<size_t>(c.hcap)));
   t.pq_s = reinterpret_cast<int32_t*>(take(4 * P * static_cast<size_t>(c.qcap)));
   t.pq_c = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.qcap)));
-  t.tw_t = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
-  t.tw_v = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
   t.dq_s = reinterpret_cast<int32_t*>(take(4 * D * static_cast<size_t>(c.qcap)));
   t.dq_c = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.qcap)));
-  t.fh = reinterpret_cast<uint64_t*>(take(8 * D * static_cast<size_t>(c.fcap)));
-  t.slog = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.lcap)));
+  t.tw_t = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
+  t.tw_v = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
+  t.tw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * P * static_cast<size_t>(c.twcap)));
   t.iw_t = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.iwcap)));
   t.iw_g = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.iwcap)));
   t.iw_c = reinterpret_cast<uint32_t*>(take(4 * D * static_cast<size_t>(c.iwcap)));
+  t.iw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * D * static_cast<size_t>(c.iwcap)));
+  t.fh = reinterpret_cast<uint64_t*>(take(8 * D * static_cast<size_t>(c.fcap)));
+  t.slog = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.lcap)));
   if (s) *s = t;
   return off;
 }
 
 // Optional per-pair record outputs (drop-in SimResult vectors).
 struct Records {
-  pdsim_decision* decisions;      // [R]
-  pdsim_ttft_sample* ttft;        // [R]
+  pdsim_decision* decisions;        // [R]
+  pdsim_ttft_sample* ttft;          // [R]
   pdsim_session_outcome* sessions;  // [S], termination order
 };
-
 
 struct PairResult {
   pdsim_attainment att;
   pdsim_counters ctr;
   int64_t n_decisions;
   int64_t n_ttft;
-  int64_t events;        // dynamic events processed (diagnostics)
-  int64_t cycles;        // device clock64() ticks for this pair (0 on host)
-  int64_t exact_folds;   // certified comparisons that fell back to a fold
-  int32_t status;        // PDSIM_PAIR_*
+  int64_t events;       // dynamic events processed (diagnostics)
+  int64_t cycles;       // device clock64() ticks for this pair (0 on host)
+  int64_t exact_folds;  // certified comparisons that fell back to a fold
+  int32_t status;       // PDSIM_PAIR_*
   int32_t reserved;
 };
 
@@ -229,48 +361,101 @@ struct RouteOut {
   double est;
 };
 
-// A routing cost estimate: exact value, or a certified bracket around the
-// reference's fold (exactsum.cuh).
-struct Est {
-  double lo, hi;
-  int32_t exact;
-  int32_t who;  // -1 local, else prefill worker index
-};
+// k-th (0-based) lexicographic permutation of 0..m-1 (factorial number system).
+PDG_HD void unrank_perm(int64_t k, int m, int* perm) {
+  int avail[8];
+  int64_t fact[9];
+  fact[0] = 1;
+  for (int i = 1; i <= m; ++i) fact[i] = fact[i - 1] * i;
+  for (int i = 0; i < m; ++i) avail[i] = i;
+  int n = m;
+  for (int i = 0; i < m; ++i) {
+    const int64_t f = fact[m - 1 - i];
+    const int q = static_cast<int>(k / f);
+    k -= q * f;
+    perm[i] = avail[q];
+    for (int j = q; j + 1 < n; ++j) avail[j] = avail[j + 1];
+    --n;
+  }
+}
 
 class Engine {
  public:
-  PDG_HD Engine(const DevTrace& tr, const DevPlan& plan, const pdsim_profile& prof,
-                const DevParams& prm, const Caps& caps, const Slot& slot, Records rec,
-                uint64_t seed)
-      : T(tr), PL(plan), PF(prof), PR(prm), C(caps), W(slot), REC(rec), seed_(seed) {}
+  PDG_HD Engine(const DevTrace& tr, const DevPlan& plan, const pdsim_profile& prof, const DevParams& prm,
+                const Caps& caps, const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed)
+      : T(tr), PL(plan), PF(prof), PR(prm), C(caps), SM(sm), G(gm), REC(rec), seed_(seed) {}
 
   PDG_HD void run(PairResult* out) {
     init();
+    const int D = PL.D, P = PL.P;
     while (!failed_) {
-      const bool has_arr = next_arr_ < T.S;
-      const bool has_ev = hn_ > 0;
-      if (!has_arr && !has_ev) break;
-      if (has_arr && (!has_ev || T.arrival[next_arr_] <= W.heap[0].t)) {
-        // Arrivals carry kind 0 and seq = index, so they precede every dynamic
-        // event at an equal time (sim_engine.cpp:137-143, 68-74).
+      // Next worker event: min over the register-resident slots.
+      double bt = kInf;
+      uint64_t bk = ~0ull;
+      for (int j = 0; j < kSlotsPerLane; ++j) {
+        if (before(st_[j], sk_[j], bt, bk)) {
+          bt = st_[j];
+          bk = sk_[j];
+        }
+      }
+      for (int m = PDG_NL / 2; m > 0; m >>= 1) {
+        const double ot = bitsd(shfl_xor_u64(dbits(bt), m));
+        const uint64_t ok = shfl_xor_u64(bk, m);
+        if (before(ot, ok, bt, bk)) {
+          bt = ot;
+          bk = ok;
+        }
+      }
+      int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
+      if (hn_ > 0) {
+        const HEv* h = heap_base();
+        const double ht = h[0].t;
+        const uint64_t hk = h[0].key;
+        if (src < 0 || before(ht, hk, bt, bk)) {
+          bt = ht;
+          bk = hk;
+          src = 1;
+        }
+      }
+      // Arrivals carry kind 0 and seq = index: they precede every dynamic
+      // event at an equal time (sim_engine.cpp:137-143).
+      if (next_arr_ < T.S && (src < 0 || next_arr_t_ <= bt)) src = 2;
+      if (src < 0) break;
+      if (src == 2) {
         const int32_t i = next_arr_++;
-        advance_to(T.arrival[i]);
+        const double t = next_arr_t_;
+        if (next_arr_ < T.S) next_arr_t_ = T.arrival[next_arr_];
+        advance_to(t);
         on_arrival(i);
         continue;
       }
-      const Event ev = heap_pop();
       ++events_;
-      advance_to(ev.t);
-      const uint32_t kind = static_cast<uint32_t>(ev.key >> 56);
-      switch (kind) {
-        case kInteractionDone: on_interaction_done(static_cast<int32_t>(ev.a)); break;
-        case kKvTransferDone: on_kv_transfer_done(ev); break;
-        case kPrefillDone: on_prefill_done(static_cast<int32_t>(ev.a)); break;
-        case kDecodeStep: on_decode_step(static_cast<int32_t>(ev.a) - PL.P); break;
-        default: fail(); break;
+      advance_to(bt);
+      const uint32_t kind = static_cast<uint32_t>(bk >> 58);
+      if (src == 1) {
+        const HEv e = heap_pop();
+        if (kind == kInteractionDone) {
+          on_interaction_done(static_cast<int32_t>(e.a));
+        } else {
+          on_writeback(static_cast<int32_t>(e.a), static_cast<int>(e.b));
+        }
+        continue;
+      }
+      const int s = static_cast<int>(bk & 63u);
+      clear_slot(s);
+      if (s < D) {
+        if (kind == kDecodeStep) {
+          on_decode_step(s);
+        } else {
+          on_local_prefill_done(s);
+        }
+      } else if (s < D + P) {
+        on_prefill_done(s - D);
+      } else {
+        on_history_read(s - D - P);
       }
     }
-    for (int d = 0; d < PL.D; ++d) ctr_.kv_bytes_residual += W.dw[d].kv_used;
+    for (int d = 0; d < PL.D; ++d) ctr_.kv_bytes_residual += SM.dw[d].kv_used;
     out->att = att_;
     out->att.sessions_total = T.S;
     out->ctr = ctr_;
@@ -287,13 +472,17 @@ class Engine {
   const pdsim_profile& PF;
   const DevParams& PR;
   const Caps& C;
-  const Slot& W;
+  const SmemSlot& SM;
+  const GlobalSlot& G;
   Records REC;
   uint64_t seed_;
 
+  // Warp-uniform scalar state (registers).
   double now_ = 0.0;
+  double next_arr_t_ = 0.0;
   uint64_t seq_ = 0;
   int32_t hn_ = 0;
+  bool heap_spilled_ = false;
   int32_t next_arr_ = 0;
   int32_t adm_head_ = 0;
   int32_t rr_next_ = 0;
@@ -305,6 +494,9 @@ class Engine {
   int64_t n_ttft_ = 0;
   int64_t events_ = 0;
   int64_t folds_ = 0;
+  // Per-lane worker-event slots.
+  double st_[kSlotsPerLane];
+  uint64_t sk_[kSlotsPerLane];
 
   PDG_HD void fail() { failed_ = true; }
 
@@ -317,95 +509,202 @@ class Engine {
     now_ = 0.0;
     seq_ = static_cast<uint64_t>(T.S);  // arrivals took seq 0..S-1
     hn_ = 0;
+    heap_spilled_ = false;
     next_arr_ = 0;
+    next_arr_t_ = T.S > 0 ? T.arrival[0] : 0.0;
     adm_head_ = 0;
     rr_next_ = 0;
     ctr_.events_in_order = 1;
-    mt64_seed(W.mt, &mt_idx_, seed_);
-    for (int p = 0; p < PL.P; ++p) {
-      PrefillW& w = W.pw[p];
-      w.q.sum.clear();
-      w.q.qh = w.q.qt = 0;
-      w.tw.clear();
-      w.deg = PL.pdeg[p];
-      w.cur = w.stg = -1;
-      w.th = w.tt = 0;
-      w.computing = w.staged = w.pending = 0;
-      w.cur_cost = w.stg_cost = 0.0;
-      w.staged_ready = 0.0;
+    for (int j = 0; j < kSlotsPerLane; ++j) {
+      st_[j] = kInf;
+      sk_[j] = ~0ull;
     }
-    for (int d = 0; d < PL.D; ++d) {
-      DecodeW& w = W.dw[d];
-      w.q.sum.clear();
-      w.q.qh = w.q.qt = 0;
-      w.iw.clear();
-      w.deg = PL.ddeg[d];
-      w.cur = -1;
-      w.cur_cost = 0.0;
-      w.kv_used = 0;
-      w.kv_cap = static_cast<int64_t>(PF.degrees[w.deg]) * PF.gpu_memory_capacity;
-      w.stepping = w.prefilling = 0;
-      w.batch_n = w.n_new = w.cohort_n = w.first_n = 0;
-      w.steps = 0;
-      w.fh_n = 0;
-      w.ih = w.it = 0;
+    if (lane_id() == 0) {
+      uint32_t idx;
+      mt64_seed(SM.mt, &idx, seed_);
+      for (int p = 0; p < PL.P; ++p) {
+        PrefillW& w = SM.pw[p];
+        w.q.sum.clear();
+        w.q.qh = w.q.qt = 0;
+        w.tw.tail.clear();
+        w.tw.head = w.tw.end = 0;
+        w.deg = PL.pdeg[p];
+        w.cur = w.stg = -1;
+        w.computing = w.staged = w.pending = 0;
+        w.cur_cost = w.stg_cost = 0.0;
+        w.staged_ready = 0.0;
+      }
+      for (int d = 0; d < PL.D; ++d) {
+        DecodeW& w = SM.dw[d];
+        w.q.sum.clear();
+        w.q.qh = w.q.qt = 0;
+        w.iw.tail.clear();
+        w.iw.head = w.iw.end = 0;
+        w.kv_used = 0;
+        w.kv_cap = static_cast<int64_t>(PF.degrees[PL.ddeg[d]]) * PF.gpu_memory_capacity;
+        w.fh_top = 0;
+        w.cur_cost = 0.0;
+        w.last_step_t = 0.0;
+        w.dur = 0.0;
+        w.dur_cohort = -1;
+        w.deg = PL.ddeg[d];
+        w.cur = -1;
+        w.batch_n = w.n_new = w.cohort_n = w.first_n = 0;
+        w.steps = 0;
+        w.fh_n = 0;
+        w.stepping = w.prefilling = 0;
+      }
     }
+    mt_idx_ = Mt64::kN;
+    warp_sync();
   }
 
   // ---- cost model (perf_model.cpp:158-205) ----
   PDG_HD double t_prefill(int32_t l_hist, int32_t l_incr, int deg) const {
-    const double load = dadd(static_cast<double>(l_incr),
-                             dmul(PF.history_weight, static_cast<double>(l_hist)));
+    const double load = dadd(static_cast<double>(l_incr), dmul(PF.history_weight, static_cast<double>(l_hist)));
     return curve_eval(PF.prefill[deg], load);
-  }
-  PDG_HD double t_decode(int32_t batch, int deg) const {
-    return curve_eval(PF.decode[deg], static_cast<double>(batch));
   }
   PDG_HD double t_kv(int32_t l, int src, int dst) const {
     if (l == 0) return 0.0;
     return curve_eval(PF.kv[src][dst], static_cast<double>(l));
   }
 
-  PDG_HD int32_t round_index(int32_t i) const { return T.round_off[i] + W.sess[i].round - 1; }
-  PDG_HD int32_t l_incr_of(int32_t i) const { return T.incr[round_index(i)]; }
+  PDG_HD int32_t l_incr_of(int32_t i) const { return T.incr[T.round_off[i] + G.sess[i].round - 1]; }
   PDG_HD double created_of(int32_t i) const {
-    return W.sess[i].round == 1 ? T.arrival[i] : W.sess[i].t_enq;  // sim_engine.cpp:258, 283, 588
+    return G.sess[i].round == 1 ? T.arrival[i] : G.sess[i].t_enq;  // sim_engine.cpp:258, 283, 588
   }
 
-  // ---- event heap ----
-  PDG_HD void schedule(double t, uint32_t kind, uint32_t a, uint32_t b) {
+  // ---- RNG (coordinator.cpp:124-130): std::mt19937_64 in shared memory ----
+  PDG_HD uint64_t rng_next() {
+    if (mt_idx_ >= static_cast<uint32_t>(Mt64::kN)) {
+#if defined(__CUDA_ARCH__)
+      // Warp-parallel twist in three dependency phases: elements below 156
+      // read only old words; 156..310 read updated words i-156; 311 reads
+      // updated words 0 and 155.
+      uint64_t* mt = SM.mt;
+      const int lane = lane_id();
+      for (int base = 0; base < 156; base += 32) {
+        const int i = base + lane;
+        uint64_t v = 0;
+        if (i < 156) {
+          const uint64_t x = (mt[i] & Mt64::kUpper) | (mt[i + 1] & Mt64::kLower);
+          v = mt[i + 156] ^ (x >> 1) ^ ((x & 1ull) ? Mt64::kMatrix : 0ull);
+        }
+        __syncwarp();
+        if (i < 156) mt[i] = v;
+        __syncwarp();
+      }
+      for (int base = 156; base < 311; base += 32) {
+        const int i = base + lane;
+        uint64_t v = 0;
+        if (i < 311) {
+          const uint64_t x = (mt[i] & Mt64::kUpper) | (mt[i + 1] & Mt64::kLower);
+          v = mt[i - 156] ^ (x >> 1) ^ ((x & 1ull) ? Mt64::kMatrix : 0ull);
+        }
+        __syncwarp();
+        if (i < 311) mt[i] = v;
+        __syncwarp();
+      }
+      {
+        const uint64_t x = (mt[311] & Mt64::kUpper) | (mt[0] & Mt64::kLower);
+        const uint64_t v = mt[155] ^ (x >> 1) ^ ((x & 1ull) ? Mt64::kMatrix : 0ull);
+        __syncwarp();
+        if (lane == 0) mt[311] = v;
+        __syncwarp();
+      }
+#else
+      mt64_twist(SM.mt);
+#endif
+      mt_idx_ = 0;
+    }
+    return mt64_temper(SM.mt[mt_idx_++]);
+  }
+
+  // ---- worker-event slots (registers) ----
+  PDG_HD void set_slot(int s, double t, uint32_t kind) {
+    const uint64_t key = mk_key(kind, seq_++, static_cast<uint32_t>(s));
+    if (s % PDG_NL == lane_id()) {
+      const int j = s / PDG_NL;
+      for (int k = 0; k < kSlotsPerLane; ++k) {
+        if (k == j) {
+          st_[k] = t;
+          sk_[k] = key;
+        }
+      }
+    }
+  }
+  PDG_HD void clear_slot(int s) {
+    if (s % PDG_NL == lane_id()) {
+      const int j = s / PDG_NL;
+      for (int k = 0; k < kSlotsPerLane; ++k) {
+        if (k == j) {
+          st_[k] = kInf;
+          sk_[k] = ~0ull;
+        }
+      }
+    }
+  }
+  PDG_HD int slot_compute(int p) const { return PL.D + p; }
+  PDG_HD int slot_history(int p) const { return PL.D + PL.P + p; }
+
+  // ---- session-event heap (shared memory, global spill) ----
+  PDG_HD HEv* heap_base() const { return heap_spilled_ ? G.heap : SM.heap; }
+
+  PDG_HD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
+    HEv e;
+    e.t = t;
+    e.key = mk_key(kind, seq_++, 0);
+    e.a = a;
+    e.b = b;
+    if (!heap_spilled_ && hn_ >= C.hs) {
+      for (int k = lane_id(); k < hn_; k += PDG_NL) G.heap[k] = SM.heap[k];
+      warp_sync();
+      heap_spilled_ = true;
+    }
     if (hn_ >= C.hcap) {
       fail();
       return;
     }
-    Event e;
-    e.t = t;
-    e.key = (static_cast<uint64_t>(kind) << 56) | seq_++;
-    e.a = a;
-    e.b = b;
+    HEv* h = heap_base();
     int32_t i = hn_++;
     while (i > 0) {
       const int32_t par = (i - 1) >> 1;
-      if (!ev_less(e, W.heap[par])) break;
-      W.heap[i] = W.heap[par];
+      const HEv pe = h[par];
+      if (!before(e.t, e.key, pe.t, pe.key)) break;
+      warp_sync();
+      if (lane_id() == 0) h[i] = pe;
       i = par;
     }
-    W.heap[i] = e;
+    warp_sync();
+    if (lane_id() == 0) h[i] = e;
+    warp_sync();
   }
 
-  PDG_HD Event heap_pop() {
-    const Event top = W.heap[0];
-    const Event last = W.heap[--hn_];
+  PDG_HD HEv heap_pop() {
+    HEv* h = heap_base();
+    const HEv top = h[0];
+    const HEv last = h[--hn_];
     int32_t i = 0;
     for (;;) {
       int32_t c = 2 * i + 1;
       if (c >= hn_) break;
-      if (c + 1 < hn_ && ev_less(W.heap[c + 1], W.heap[c])) ++c;
-      if (!ev_less(W.heap[c], last)) break;
-      W.heap[i] = W.heap[c];
+      HEv ce = h[c];
+      if (c + 1 < hn_) {
+        const HEv c2 = h[c + 1];
+        if (before(c2.t, c2.key, ce.t, ce.key)) {
+          ++c;
+          ce = c2;
+        }
+      }
+      if (!before(ce.t, ce.key, last.t, last.key)) break;
+      warp_sync();
+      if (lane_id() == 0) h[i] = ce;
       i = c;
     }
-    if (hn_ > 0) W.heap[i] = last;
+    warp_sync();
+    if (hn_ > 0 && lane_id() == 0) h[i] = last;
+    warp_sync();
+    if (hn_ == 0) heap_spilled_ = false;
     return top;
   }
 
@@ -416,25 +715,39 @@ class Engine {
     adm_head_ = i + 1;
   }
 
-  PDG_HD bool try_admit(int32_t i) {
+  PDG_HD int bind_session() const {  // least KV bytes, lowest index on ties
     int best = 0;
+    int64_t bv = SM.dw[0].kv_used;
     for (int d = 1; d < PL.D; ++d) {
-      if (W.dw[d].kv_used < W.dw[best].kv_used) best = d;
+      const int64_t v = SM.dw[d].kv_used;
+      if (v < bv) {
+        bv = v;
+        best = d;
+      }
     }
-    const DecodeW& w = W.dw[best];
+    return best;
+  }
+
+  PDG_HD bool try_admit(int32_t i) {
+    const int best = bind_session();
+    const DecodeW& w = SM.dw[best];
     const int64_t first = static_cast<int64_t>(T.incr[T.round_off[i]]) * PF.kv_bytes_per_token;
     if (w.kv_used + first > w.kv_cap) return false;
-    SessRt& s = W.sess[i];
-    s.bound = static_cast<int8_t>(best);
-    s.bind_time = now_;
-    s.round = 1;
-    s.ctx = 0;
-    s.itl_sum = 0.0;
-    s.itl_cnt = 0;
-    s.join = 0;
-    s.postpone = 0;
-    s.ttft_bad = 0;
-    start_round(i);
+    SessRt& s = G.sess[i];
+    warp_sync();
+    if (lane_id() == 0) {
+      s.bound = static_cast<int8_t>(best);
+      s.bind_time = now_;
+      s.round = 1;
+      s.ctx = 0;
+      s.itl_sum = 0.0;
+      s.itl_cnt = 0;
+      s.join = 0;
+      s.postpone = 0;
+      s.ttft_bad = 0;
+    }
+    warp_sync();
+    start_round(i, 1, best, 0);
     return true;
   }
 
@@ -443,18 +756,23 @@ class Engine {
   }
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
-  PDG_HD void start_round(int32_t i) {
-    SessRt& s = W.sess[i];
-    s.t_enq = now_;
-    s.postpone = 0;
+  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx) {
+    SessRt& s = G.sess[i];
+    warp_sync();
+    if (lane_id() == 0) {
+      s.t_enq = now_;
+      s.postpone = 0;
+    }
+    warp_sync();
     ++ctr_.tasks_created;
-    const RouteOut r = decide(i);
-    if (REC.decisions) {
+    const int32_t incr = T.incr[T.round_off[i] + round - 1];
+    const RouteOut r = decide(i, bound, ctx, incr);
+    if (REC.decisions && lane_id() == 0) {
       pdsim_decision& d = REC.decisions[n_dec_];
       d.time = now_;
       d.session_id = T.sid[i];
-      d.round = s.round;
-      d.worker = r.local ? PL.P + s.bound : r.p;
+      d.round = round;
+      d.worker = r.local ? PL.P + bound : r.p;
       d.local = static_cast<int8_t>(r.local);
       d.rationale = static_cast<int8_t>(r.rationale);
       d.has_estimate = static_cast<int8_t>(r.has_est);
@@ -463,13 +781,13 @@ class Engine {
     }
     ++n_dec_;
     if (r.local) {
-      enqueue_local(s.bound, i);
+      enqueue_local(bound, i, ctx, incr);
     } else {
-      enqueue_remote(r.p, i);
+      enqueue_remote(r.p, i, ctx, incr);
     }
   }
 
-  PDG_HD RouteOut decide(int32_t i) {
+  PDG_HD RouteOut decide(int32_t i, int bound, int32_t ctx, int32_t incr) {
     RouteOut r;
     r.local = 1;
     r.p = -1;
@@ -490,272 +808,364 @@ class Engine {
       r.rationale = PDSIM_RATIONALE_FORCED_REMOTE;
       return r;
     }
-    return route(i);
-  }
-
-  // Coordinator::route (coordinator.cpp:115-171).
-  PDG_HD RouteOut route(int32_t i) {
-    const SessRt& s = W.sess[i];
-    const int n = PL.P;
-    RouteOut r;
-    r.has_est = 0;
-    r.est = 0.0;
-    if (n > 0) {
-      int order[PDSIM_MAX_WORKERS];
-      for (int k = 0; k < n; ++k) order[k] = k;
-      for (int k = n - 1; k > 0; --k) {
-        const int j = static_cast<int>(mt64_next(W.mt, &mt_idx_) % static_cast<uint64_t>(k + 1));
-        const int tmp = order[k];
-        order[k] = order[j];
-        order[j] = tmp;
-      }
-      const double thr = dmul(PR.alpha, T.ttft_thres);
-      for (int k = 0; k < n; ++k) {
-        if (ttft_has_slack(order[k], thr)) {
-          r.local = 0;
-          r.p = order[k];
-          r.rationale = PDSIM_RATIONALE_SLACK_REMOTE;
-          return r;
-        }
-      }
-    }
-    if (itl_has_slack(s.bound, dmul(PR.beta, T.itl_thres))) {
-      r.local = 1;
-      r.p = -1;
-      r.rationale = PDSIM_RATIONALE_SLACK_LOCAL;
-      return r;
-    }
-    // Cost comparison; ties prefer local, then the lowest worker index.
-    r.local = 1;
-    r.p = -1;
-    r.rationale = PDSIM_RATIONALE_ARGMIN;
-    Est best = est_local(i, s.bound);
-    for (int p = 0; p < n; ++p) {
-      Est c = est_remote(i, p, s.bound);
-      if (est_less(c, best, i, s.bound)) {
-        best = c;
-        r.local = 0;
-        r.p = p;
-      }
-    }
-    r.has_est = 1;
-    if (REC.decisions && !best.exact) resolve(best, i, s.bound);
-    r.est = best.lo;
+    route(bound, ctx, incr, &r);
     return r;
   }
 
+  // Coordinator::route (coordinator.cpp:115-171).
+  PDG_HD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
+    const int n = PL.P;
+    if (n > 0) {
+      int32_t* order = SM.order;
+      warp_sync();
+      if (lane_id() == 0) {
+        for (int k = 0; k < n; ++k) order[k] = k;
+      }
+      warp_sync();
+      for (int k = n - 1; k > 0; --k) {
+        const int j = static_cast<int>(rng_next() % static_cast<uint64_t>(k + 1));
+        const int a = order[k], b = order[j];
+        warp_sync();
+        if (lane_id() == 0) {
+          order[k] = b;
+          order[j] = a;
+        }
+        warp_sync();
+      }
+      const double thr = dmul(PR.alpha, T.ttft_thres);
+      for (int k = 0; k < n; ++k) {
+        const int p = order[k];
+        if (ttft_has_slack(p, thr)) {
+          r->local = 0;
+          r->p = p;
+          r->rationale = PDSIM_RATIONALE_SLACK_REMOTE;
+          return;
+        }
+      }
+    }
+    if (itl_has_slack(bound, dmul(PR.beta, T.itl_thres))) {
+      r->local = 1;
+      r->p = -1;
+      r->rationale = PDSIM_RATIONALE_SLACK_LOCAL;
+      return;
+    }
+    r->rationale = PDSIM_RATIONALE_ARGMIN;
+    argmin_route(bound, ctx, incr, r);
+  }
+
   // ---- routing estimates (coordinator.cpp:74-100) ----
-  // Exact sequential folds (the reference's arithmetic).
   PDG_HD double fold_queue(const TaskQueue& q, const double* qc, double init) const {
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
     double c = init;
     for (uint32_t k = q.qh; k != q.qt; ++k) c = dadd(c, qc[k & mask]);
     return c;
   }
-  PDG_HD double local_exact(int32_t i, int d) {
-    ++folds_;
-    const DecodeW& w = W.dw[d];
-    return fold_queue(w.q, W.dq_c + static_cast<size_t>(d) * C.qcap, t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg));
-  }
-  PDG_HD double remote_head(int32_t i, int p, int d) const {
-    const int pd = W.pw[p].deg, dd = W.dw[d].deg;
-    const int32_t hist = W.sess[i].ctx;
-    const int32_t incr = l_incr_of(i);
-    return dadd(t_prefill(hist, incr, pd), dadd(t_kv(hist, dd, pd), t_kv(incr, pd, dd)));
-  }
-  PDG_HD double remote_exact(int32_t i, int p, int d) {
-    ++folds_;
-    const double tq = fold_queue(W.pw[p].q, W.pq_c + static_cast<size_t>(p) * C.qcap, 0.0);
-    return dadd(remote_head(i, p, d), tq);
-  }
-  PDG_HD static Est exact_est(double v, int who) {
-    Est e;
-    e.lo = e.hi = v;
-    e.exact = 1;
-    e.who = who;
-    return e;
-  }
-  // head + fold(queue) of `len` non-negative terms, with exact queue sum.
-  PDG_HD static Est bracket_est(double head, const ExactSum& qs, int64_t nterms, int who) {
-    Est e;
-    const double v = dadd(head, fx_to_double(qs.sum));
-    const double m = fold_margin(nterms);
-    e.lo = v * (1.0 - m);
-    e.hi = v * (1.0 + m);
-    e.exact = 0;
-    e.who = who;
-    return e;
-  }
-  PDG_HD Est est_local(int32_t i, int d) {
-    const DecodeW& w = W.dw[d];
+  // Estimate of candidate c (-1 local, else prefill worker c): the exact
+  // reference value, or a certified bracket [lo, hi] around it.
+  PDG_HD void estimate(int d, int32_t ctx, int32_t incr, int c, bool force_exact, double* lo, double* hi,
+                       bool* exact) const {
+    if (c < 0) {
+      const DecodeW& w = SM.dw[d];
+      const uint32_t len = w.q.qt - w.q.qh;
+      const double own = t_prefill(ctx, incr, w.deg);
+      if (force_exact || len <= 2 || !w.q.sum.exact()) {
+        *lo = *hi = fold_queue(w.q, G.dq_c + static_cast<size_t>(d) * C.qcap, own);
+        *exact = true;
+        return;
+      }
+      const double v = dadd(own, fx_to_double(w.q.sum.sum));
+      const double m = fold_margin(static_cast<int64_t>(len) + 1);
+      *lo = v * (1.0 - m);
+      *hi = v * (1.0 + m);
+      *exact = false;
+      return;
+    }
+    const PrefillW& w = SM.pw[c];
+    const int pd = w.deg, dd = SM.dw[d].deg;
     const uint32_t len = w.q.qt - w.q.qh;
-    const double own = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    if (len <= 2 || !w.q.sum.exact()) {
-      return exact_est(fold_queue(w.q, W.dq_c + static_cast<size_t>(d) * C.qcap, own), -1);
+    const double head = dadd(t_prefill(ctx, incr, pd), dadd(t_kv(ctx, dd, pd), t_kv(incr, pd, dd)));
+    if (force_exact || len <= 2 || !w.q.sum.exact()) {
+      *lo = *hi = dadd(head, fold_queue(w.q, G.pq_c + static_cast<size_t>(c) * C.qcap, 0.0));
+      *exact = true;
+      return;
     }
-    return bracket_est(own, w.q.sum, static_cast<int64_t>(len) + 1, -1);
+    const double v = dadd(head, fx_to_double(w.q.sum.sum));
+    const double m = fold_margin(static_cast<int64_t>(len));
+    *lo = v * (1.0 - m);
+    *hi = v * (1.0 + m);
+    *exact = false;
   }
-  PDG_HD Est est_remote(int32_t i, int p, int d) {
-    const PrefillW& w = W.pw[p];
-    const uint32_t len = w.q.qt - w.q.qh;
-    const double head = remote_head(i, p, d);
-    if (len <= 2 || !w.q.sum.exact()) {
-      return exact_est(dadd(head, fold_queue(w.q, W.pq_c + static_cast<size_t>(p) * C.qcap, 0.0)), p);
+
+  // Lines 6-9 of Alg. 1: best = local; for i: if (cost_i < best) take i.
+  // The strict-< scan ends on the FIRST candidate (local first, then the
+  // lowest worker index) holding the minimum value. Lanes estimate remote
+  // candidates in parallel; a candidate whose bracket starts above the
+  // smallest upper bound cannot win, and exact folds run only when two or
+  // more candidates remain in contention.
+  PDG_HD void argmin_route(int d, int32_t ctx, int32_t incr, RouteOut* r) {
+    constexpr int kPer = (kMaxSlots + PDG_NL - 1) / PDG_NL;
+    const int n = PL.P;
+    const int lane = lane_id();
+    double llo, lhi;
+    bool lex;
+    estimate(d, ctx, incr, -1, false, &llo, &lhi, &lex);
+    double rlo[kPer], rhi[kPer];
+    bool rex[kPer];
+    double min_hi = lhi;
+    for (int k = 0; k < kPer; ++k) {
+      const int c = lane + k * PDG_NL;
+      rlo[k] = kInf;
+      rhi[k] = kInf;
+      rex[k] = true;
+      if (c < n) estimate(d, ctx, incr, c, false, &rlo[k], &rhi[k], &rex[k]);
+      if (rhi[k] < min_hi) min_hi = rhi[k];
     }
-    return bracket_est(head, w.q.sum, static_cast<int64_t>(len), p);
-  }
-  PDG_HD void resolve(Est& e, int32_t i, int d) {
-    if (e.exact) return;
-    const double v = e.who < 0 ? local_exact(i, d) : remote_exact(i, e.who, d);
-    e = exact_est(v, e.who);
-  }
-  // `c < b` on the reference's values.
-  PDG_HD bool est_less(Est& c, Est& b, int32_t i, int d) {
-    if (!(c.exact && b.exact)) {
-      if (c.hi < b.lo) return true;
-      if (c.lo >= b.hi) return false;
-      resolve(c, i, d);
-      resolve(b, i, d);
+    min_hi = warp_min(min_hi);
+    const bool lcan = llo <= min_hi;
+    int count = lcan ? 1 : 0;
+    bool can[kPer];
+    for (int k = 0; k < kPer; ++k) {
+      can[k] = (lane + k * PDG_NL) < n && rlo[k] <= min_hi;
+      count += popc(ballot(can[k]));
     }
-    return c.lo < b.lo;
+    int winner;
+    double est;
+    bool est_exact;
+    if (count >= 2) {
+      if (lcan && !lex) {
+        ++folds_;
+        estimate(d, ctx, incr, -1, true, &llo, &lhi, &lex);
+      }
+      double v = lcan ? llo : kInf;
+      for (int k = 0; k < kPer; ++k) {
+        if (can[k] && !rex[k]) estimate(d, ctx, incr, lane + k * PDG_NL, true, &rlo[k], &rhi[k], &rex[k]);
+        if (can[k] && rlo[k] < v) v = rlo[k];
+      }
+      v = warp_min(v);
+      winner = -2;
+      if (lcan && llo == v) winner = -1;
+      for (int k = 0; k < kPer && winner == -2; ++k) {
+        const uint32_t b = ballot(can[k] && rlo[k] == v);
+        if (b) winner = k * PDG_NL + first_zero(~b);
+      }
+      est = v;
+      est_exact = true;
+    } else if (lcan) {
+      winner = -1;
+      est = llo;
+      est_exact = lex;
+    } else {
+      winner = -2;
+      for (int k = 0; k < kPer && winner == -2; ++k) {
+        const uint32_t b = ballot(can[k]);
+        if (b) winner = k * PDG_NL + first_zero(~b);
+      }
+      if (winner < 0) {  // no contender at all: impossible, keep state consistent
+        fail();
+        winner = -1;
+      }
+      const int owner = winner % PDG_NL, kk = winner / PDG_NL;
+      double lo = kInf;
+      int ex = 1;
+      for (int k = 0; k < kPer; ++k) {
+        if (k == kk) {
+          lo = rlo[k];
+          ex = rex[k] ? 1 : 0;
+        }
+      }
+      est = shfl_d(lo, owner);
+      est_exact = shfl_i(ex, owner) != 0;
+    }
+    if (!est_exact && REC.decisions) {
+      double a, b;
+      bool e;
+      estimate(d, ctx, incr, winner, true, &a, &b, &e);
+      est = a;
+    }
+    r->local = winner < 0 ? 1 : 0;
+    r->p = winner < 0 ? -1 : winner;
+    r->has_est = 1;
+    r->est = est;
   }
 
   // ---- windowed statistics (coordinator.cpp:27-47) ----
-  PDG_HD void ttft_trim(PrefillW& w, const double* tt, const double* tv) {
-    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
+  // Drops entries with time <= now - window from the head (times are
+  // non-decreasing, so expired entries form a prefix): one ballot per 32.
+  PDG_HD void window_trim(WinState& w, const double* times, uint32_t mask) {
     const double cutoff = dsub(now_, PR.stat_window);
-    while (w.th != w.tt && tt[w.th & mask] <= cutoff) {
-      w.tw.remove(tv[w.th & mask]);
-      ++w.th;
+    uint32_t head = w.head;
+    const uint32_t end = w.end;
+    while (head != end) {
+      const uint32_t off = static_cast<uint32_t>(lane_id());
+      const bool in = off < end - head;
+      const bool expired = in && times[(head + off) & mask] <= cutoff;
+      const int n = first_zero(ballot(expired));
+      head += static_cast<uint32_t>(n);
+      if (n < PDG_NL) break;
     }
+    warp_sync();
+    if (lane_id() == 0) w.head = head;
+    warp_sync();
+  }
+
+  PDG_HD bool window_room(WinState& w, const double* times, uint32_t cap) {
+    if (w.end - w.head >= cap - 1) {
+      window_trim(w, times, cap - 1);
+      if (w.end - w.head >= cap - 1) {
+        fail();
+        return false;
+      }
+    }
+    return true;
   }
 
   PDG_HD void ttft_add(int p, double v) {
-    PrefillW& w = W.pw[p];
+    PrefillW& w = SM.pw[p];
+    const size_t base = static_cast<size_t>(p) * C.twcap;
     const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
-    double* tt = W.tw_t + static_cast<size_t>(p) * C.twcap;
-    double* tv = W.tw_v + static_cast<size_t>(p) * C.twcap;
-    ttft_trim(w, tt, tv);
-    if (w.tt - w.th >= static_cast<uint32_t>(C.twcap)) {
-      fail();
-      return;
+    if (!window_room(w.tw, G.tw_t + base, static_cast<uint32_t>(C.twcap))) return;
+    const uint32_t k = w.tw.end & mask;
+    const Pfx cur = w.tw.tail;
+    Pfx next = cur;
+    next.add(v, 1);
+    warp_sync();
+    if (lane_id() == 0) {
+      G.tw_t[base + k] = now_;
+      G.tw_v[base + k] = v;
+      G.tw_p[base + k] = cur;
+      w.tw.tail = next;
+      ++w.tw.end;
     }
-    tt[w.tt & mask] = now_;
-    tv[w.tt & mask] = v;
-    ++w.tt;
-    w.tw.add(v);
+    warp_sync();
   }
 
-  // query(now) <= thr, where query is the sequential windowed mean.
+  // query(now) <= thr with the sequential windowed mean's semantics.
   PDG_HD bool ttft_has_slack(int p, double thr) {
-    PrefillW& w = W.pw[p];
-    const double* tt = W.tw_t + static_cast<size_t>(p) * C.twcap;
-    const double* tv = W.tw_v + static_cast<size_t>(p) * C.twcap;
-    ttft_trim(w, tt, tv);
-    if (w.th == w.tt) return 0.0 <= thr;  // empty window reads 0
-    const int dec = mean_le_certified(w.tw, thr);
+    PrefillW& w = SM.pw[p];
+    const size_t base = static_cast<size_t>(p) * C.twcap;
+    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
+    window_trim(w.tw, G.tw_t + base, mask);
+    const uint32_t head = w.tw.head, end = w.tw.end;
+    if (head == end) return 0.0 <= thr;  // an empty window reads 0
+    const Pfx hp = G.tw_p[base + (head & mask)];
+    const int dec = window_mean_le(w.tw.tail, hp, thr);
     if (dec >= 0) return dec == 1;
     ++folds_;
-    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
     double sum = 0.0;
-    for (uint32_t k = w.th; k != w.tt; ++k) sum = dadd(sum, tv[k & mask]);
-    return ddiv(sum, static_cast<double>(w.tt - w.th)) <= thr;
-  }
-
-  PDG_HD void itl_trim(DecodeW& w, const double* it, const double* ig, const uint32_t* ic) {
-    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
-    const double cutoff = dsub(now_, PR.stat_window);
-    while (w.ih != w.it && it[w.ih & mask] <= cutoff) {
-      w.iw.remove(ig[w.ih & mask], ic[w.ih & mask]);
-      ++w.ih;
-    }
+    for (uint32_t k = head; k != end; ++k) sum = dadd(sum, G.tw_v[base + (k & mask)]);
+    return ddiv(sum, static_cast<double>(end - head)) <= thr;
   }
 
   PDG_HD void itl_add(int d, double gap, uint32_t count) {
-    DecodeW& w = W.dw[d];
+    DecodeW& w = SM.dw[d];
+    const size_t base = static_cast<size_t>(d) * C.iwcap;
     const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
-    double* it = W.iw_t + static_cast<size_t>(d) * C.iwcap;
-    double* ig = W.iw_g + static_cast<size_t>(d) * C.iwcap;
-    uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
-    itl_trim(w, it, ig, ic);
-    if (w.it - w.ih >= static_cast<uint32_t>(C.iwcap)) {
-      fail();
-      return;
+    if (!window_room(w.iw, G.iw_t + base, static_cast<uint32_t>(C.iwcap))) return;
+    const uint32_t k = w.iw.end & mask;
+    const Pfx cur = w.iw.tail;
+    Pfx next = cur;
+    next.add(gap, count);
+    warp_sync();
+    if (lane_id() == 0) {
+      G.iw_t[base + k] = now_;
+      G.iw_g[base + k] = gap;
+      G.iw_c[base + k] = count;
+      G.iw_p[base + k] = cur;
+      w.iw.tail = next;
+      ++w.iw.end;
     }
-    it[w.it & mask] = now_;
-    ig[w.it & mask] = gap;
-    ic[w.it & mask] = count;
-    ++w.it;
-    w.iw.add(gap, count);
+    warp_sync();
   }
 
   PDG_HD bool itl_has_slack(int d, double thr) {
-    DecodeW& w = W.dw[d];
-    const double* it = W.iw_t + static_cast<size_t>(d) * C.iwcap;
-    const double* ig = W.iw_g + static_cast<size_t>(d) * C.iwcap;
-    const uint32_t* ic = W.iw_c + static_cast<size_t>(d) * C.iwcap;
-    itl_trim(w, it, ig, ic);
-    if (w.ih == w.it) return 0.0 <= thr;
-    const int dec = mean_le_certified(w.iw, thr);
+    DecodeW& w = SM.dw[d];
+    const size_t base = static_cast<size_t>(d) * C.iwcap;
+    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
+    window_trim(w.iw, G.iw_t + base, mask);
+    const uint32_t head = w.iw.head, end = w.iw.end;
+    if (head == end) return 0.0 <= thr;
+    const Pfx hp = G.iw_p[base + (head & mask)];
+    const int dec = window_mean_le(w.iw.tail, hp, thr);
     if (dec >= 0) return dec == 1;
     ++folds_;
-    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
     double sum = 0.0;
-    for (uint32_t k = w.ih; k != w.it; ++k) sum = fold_repeat(sum, ig[k & mask], ic[k & mask]);
-    return ddiv(sum, static_cast<double>(w.iw.terms)) <= thr;
+    for (uint32_t k = head; k != end; ++k) sum = fold_repeat(sum, G.iw_g[base + (k & mask)], G.iw_c[base + (k & mask)]);
+    return ddiv(sum, static_cast<double>(w.iw.tail.terms - hp.terms)) <= thr;
   }
 
   // ---- queues + reorder (reorder.cpp:76-146; select_next sim_engine.cpp:335-350) ----
   PDG_HD bool queue_push(TaskQueue& q, int32_t* qs, double* qc, int32_t i, double cost) {
-    if (q.qt - q.qh >= static_cast<uint32_t>(C.qcap)) {
+    const uint32_t qh = q.qh, qt = q.qt;
+    if (qt - qh >= static_cast<uint32_t>(C.qcap)) {
       fail();
       return false;
     }
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
-    qs[q.qt & mask] = i;
-    qc[q.qt & mask] = cost;
-    ++q.qt;
-    q.sum.add(cost);
+    ExactSum ns = q.sum;
+    ns.add(cost);
+    warp_sync();
+    if (lane_id() == 0) {
+      qs[qt & mask] = i;
+      qc[qt & mask] = cost;
+      q.sum = ns;
+      q.qt = qt + 1;
+    }
+    warp_sync();
     return true;
   }
 
   // Dequeues the next task (after reordering the head window).
   PDG_HD int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+    const uint32_t qh = q.qh;
     if (PR.reorder) {
-      const uint32_t len = q.qt - q.qh;
-      const int m = static_cast<int>(len < static_cast<uint32_t>(PR.window) ? len : PR.window);
-      if (m > 1) reorder_head(qs, qc, q.qh, m);
+      const uint32_t len = q.qt - qh;
+      const int m = static_cast<int>(len < static_cast<uint32_t>(PR.window) ? len : static_cast<uint32_t>(PR.window));
+      if (m > 1) reorder_head(qs, qc, qh, m);
     }
-    const int32_t i = qs[q.qh & mask];
-    *cost = qc[q.qh & mask];
-    ++q.qh;
-    q.sum.remove(*cost);
-    const int32_t pc = W.sess[i].postpone;
+    const int32_t i = qs[qh & mask];
+    *cost = qc[qh & mask];
+    ExactSum ns = q.sum;
+    ns.remove(*cost);
+    const int32_t pc = G.sess[i].postpone;
+    warp_sync();
+    if (lane_id() == 0) {
+      q.sum = ns;
+      q.qh = qh + 1;
+    }
+    warp_sync();
     if (pc > ctr_.max_postpone_observed) ctr_.max_postpone_observed = pc;
     return i;
   }
 
   // Exhaustive search over the lexicographic permutations of the first m
-  // queued tasks; strict improvements only; capped tasks cannot be pushed
-  // back (reorder.cpp:93-138).
+  // queued tasks with strict improvements only: the winner is the
+  // lexicographically first permutation with the maximum count among the
+  // allowed ones (the identity is always allowed); capped tasks cannot be
+  // pushed back (reorder.cpp:93-138). Lanes evaluate permutations in parallel.
   PDG_HD void reorder_head(int32_t* qs, double* qc, uint32_t qh, int m) {
     const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
     int32_t hs[8];
     double hc[8], wait[8];
-    int8_t pc[8];
+    int pc[8];
     for (int k = 0; k < m; ++k) {
       hs[k] = qs[(qh + k) & mask];
       hc[k] = qc[(qh + k) & mask];
-      wait[k] = dsub(now_, W.sess[hs[k]].t_enq);
-      pc[k] = W.sess[hs[k]].postpone;
+      const SessRt& s = G.sess[hs[k]];
+      wait[k] = dsub(now_, s.t_enq);
+      pc[k] = s.postpone;
     }
     const double thres = T.ttft_thres;
-    int perm[8], best[8];
-    for (int k = 0; k < m; ++k) perm[k] = best[k] = k;
-    int best_sat = count_satisfied(perm, m, hc, wait, thres);
-    if (best_sat == m) return;  // identity already satisfies every task: no strict improvement exists
-    while (next_permutation(perm, m)) {
+    int perm[8];
+    for (int k = 0; k < m; ++k) perm[k] = k;
+    const int id_sat = count_satisfied(perm, m, hc, wait, thres);
+    if (id_sat == m) return;  // the identity already satisfies every task
+    int64_t nperm = 1;
+    for (int k = 2; k <= m; ++k) nperm *= k;
+    int best_sat = id_sat;
+    int64_t best_r = 0;
+    for (int64_t r = 1 + lane_id(); r < nperm; r += PDG_NL) {
+      unrank_perm(r, m, perm);
       bool allowed = true;
       for (int k = 0; k < m; ++k) {
         if (k > perm[k] && pc[perm[k]] >= PR.window) {
@@ -765,22 +1175,34 @@ class Engine {
       }
       if (!allowed) continue;
       const int sat = count_satisfied(perm, m, hc, wait, thres);
-      if (sat > best_sat) {
+      if (sat > best_sat) {  // per lane: smallest rank with a strict maximum
         best_sat = sat;
-        for (int k = 0; k < m; ++k) best[k] = perm[k];
-        if (best_sat == m) break;  // cannot be strictly improved upon
+        best_r = r;
       }
     }
-    for (int k = 0; k < m; ++k) {
-      const int p = best[k];
-      if (k > p) ++W.sess[hs[p]].postpone;
-      qs[(qh + k) & mask] = hs[p];
-      qc[(qh + k) & mask] = hc[p];
+    for (int s = PDG_NL / 2; s > 0; s >>= 1) {
+      const int os = shfl_i(best_sat, lane_id() ^ s);
+      const int64_t orr = static_cast<int64_t>(shfl_u64(static_cast<uint64_t>(best_r), lane_id() ^ s));
+      if (os > best_sat || (os == best_sat && orr < best_r)) {
+        best_sat = os;
+        best_r = orr;
+      }
     }
+    if (best_r == 0) return;
+    unrank_perm(best_r, m, perm);
+    warp_sync();
+    if (lane_id() == 0) {
+      for (int k = 0; k < m; ++k) {
+        const int p = perm[k];
+        if (k > p) ++G.sess[hs[p]].postpone;
+        qs[(qh + k) & mask] = hs[p];
+        qc[(qh + k) & mask] = hc[p];
+      }
+    }
+    warp_sync();
   }
 
-  PDG_HD static int count_satisfied(const int* perm, int m, const double* hc,
-                                    const double* wait, double thres) {
+  PDG_HD static int count_satisfied(const int* perm, int m, const double* hc, const double* wait, double thres) {
     double elapsed = 0.0;
     int sat = 0;
     for (int k = 0; k < m; ++k) {
@@ -790,108 +1212,95 @@ class Engine {
     return sat;
   }
 
-  PDG_HD static bool next_permutation(int* a, int n) {
-    int i = n - 2;
-    while (i >= 0 && a[i] >= a[i + 1]) --i;
-    if (i < 0) return false;
-    int j = n - 1;
-    while (a[j] <= a[i]) --j;
-    int t = a[i];
-    a[i] = a[j];
-    a[j] = t;
-    for (int l = i + 1, r = n - 1; l < r; ++l, --r) {
-      t = a[l];
-      a[l] = a[r];
-      a[r] = t;
-    }
-    return true;
-  }
-
   // ---- prefill workers (sim_engine.cpp:354-453) ----
-  PDG_HD void enqueue_remote(int p, int32_t i) {
-    PrefillW& w = W.pw[p];
-    const double cost = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    if (!queue_push(w.q, W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap, i,
-                    cost))
+  PDG_HD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
+    PrefillW& w = SM.pw[p];
+    const double cost = t_prefill(ctx, incr, w.deg);
+    if (!queue_push(w.q, G.pq_s + static_cast<size_t>(p) * C.qcap, G.pq_c + static_cast<size_t>(p) * C.qcap, i, cost))
       return;
     try_stage(p);
     try_start_compute(p);
   }
 
   PDG_HD void try_stage(int p) {
-    PrefillW& w = W.pw[p];
+    PrefillW& w = SM.pw[p];
     if (w.staged || w.q.qh == w.q.qt) return;
-    w.stg = select_next(w.q, W.pq_s + static_cast<size_t>(p) * C.qcap, W.pq_c + static_cast<size_t>(p) * C.qcap,
-                        &w.stg_cost);
-    w.staged = 1;
-    const int32_t hist = W.sess[w.stg].ctx;
+    double cost;
+    const int32_t stg = select_next(w.q, G.pq_s + static_cast<size_t>(p) * C.qcap,
+                                    G.pq_c + static_cast<size_t>(p) * C.qcap, &cost);
+    const int32_t hist = G.sess[stg].ctx;
+    double ready = now_;
     if (hist > 0) {
       // Lazy history read from the bound decode worker (sim_engine.cpp:368-383).
-      const int dd = W.dw[W.sess[w.stg].bound].deg;
-      w.staged_ready = dadd(now_, t_kv(hist, dd, w.deg));
-      w.pending = 1;
-      schedule(w.staged_ready, kKvTransferDone, static_cast<uint32_t>(p), 0u);
-    } else {
-      w.staged_ready = now_;
-      w.pending = 0;
+      const int dd = SM.dw[G.sess[stg].bound].deg;
+      ready = dadd(now_, t_kv(hist, dd, w.deg));
     }
+    warp_sync();
+    if (lane_id() == 0) {
+      w.stg = stg;
+      w.stg_cost = cost;
+      w.staged = 1;
+      w.staged_ready = ready;
+      w.pending = hist > 0 ? 1 : 0;
+    }
+    warp_sync();
+    if (hist > 0) set_slot(slot_history(p), ready, kKvTransferDone);
   }
 
   PDG_HD void try_start_compute(int p) {
-    PrefillW& w = W.pw[p];
+    PrefillW& w = SM.pw[p];
     if (w.computing || !w.staged || w.pending || w.staged_ready > now_) return;
-    w.cur = w.stg;
-    w.cur_cost = w.stg_cost;
-    w.staged = 0;
-    w.computing = 1;
-    schedule(dadd(now_, w.cur_cost), kPrefillDone, static_cast<uint32_t>(p), 0u);
+    const double done = dadd(now_, w.stg_cost);
+    warp_sync();
+    if (lane_id() == 0) {
+      w.cur = w.stg;
+      w.cur_cost = w.stg_cost;
+      w.staged = 0;
+      w.computing = 1;
+    }
+    warp_sync();
+    set_slot(slot_compute(p), done, kPrefillDone);
     try_stage(p);  // the next task's history read overlaps this compute
   }
 
-  PDG_HD void on_prefill_done(int32_t worker) {
-    if (worker < PL.P) {
-      const int p = worker;
-      PrefillW& w = W.pw[p];
-      w.computing = 0;
-      const int32_t i = w.cur;
-      const int dd = W.dw[W.sess[i].bound].deg;
-      schedule(dadd(now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(p),
-               static_cast<uint32_t>(i) | 0x80000000u);
-      try_stage(p);
-      try_start_compute(p);
-    } else {
-      const int d = worker - PL.P;
-      DecodeW& w = W.dw[d];
-      w.prefilling = 0;
-      complete_task(w.cur, true, -1, d);
-      advance_decode(d);
-    }
+  PDG_HD void on_prefill_done(int p) {
+    PrefillW& w = SM.pw[p];
+    const int32_t i = w.cur;
+    warp_sync();
+    if (lane_id() == 0) w.computing = 0;
+    warp_sync();
+    const int dd = SM.dw[G.sess[i].bound].deg;
+    heap_push(dadd(now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
+              static_cast<uint32_t>(p));
+    try_stage(p);
+    try_start_compute(p);
   }
 
-  PDG_HD void on_kv_transfer_done(const Event& ev) {
-    const int p = static_cast<int>(ev.a);
-    if (!(ev.b & 0x80000000u)) {  // history read landed
-      W.pw[p].pending = 0;
-      try_start_compute(p);
-      return;
-    }
-    const int32_t i = static_cast<int32_t>(ev.b & 0x7fffffffu);
-    const int d = W.sess[i].bound;
+  PDG_HD void on_history_read(int p) {
+    warp_sync();
+    if (lane_id() == 0) SM.pw[p].pending = 0;
+    warp_sync();
+    try_start_compute(p);
+  }
+
+  PDG_HD void on_writeback(int32_t i, int p) {
+    const int d = G.sess[i].bound;
     complete_task(i, false, p, d);
     advance_decode(d);
   }
 
   // complete_task (sim_engine.cpp:458-484).
   PDG_HD void complete_task(int32_t i, bool local, int p, int d) {
-    SessRt& s = W.sess[i];
-    const double created = created_of(i);
+    SessRt& s = G.sess[i];
+    const int round = s.round;
+    const double created = round == 1 ? T.arrival[i] : s.t_enq;
     const double value = dsub(now_, created);
     if (!local) ttft_add(p, value);  // decode workers' TTFT windows are never queried
-    if (REC.ttft) {
+    if (REC.ttft && lane_id() == 0) {
       pdsim_ttft_sample& o = REC.ttft[n_ttft_];
       o.session_id = T.sid[i];
-      o.round = s.round;
-      o.kind = s.round == 1 ? 0 : 1;
+      o.round = round;
+      o.kind = round == 1 ? 0 : 1;
       o.local = local ? 1 : 0;
       o.reserved[0] = o.reserved[1] = 0;
       o.created_time = created;
@@ -899,94 +1308,134 @@ class Engine {
       o.value = value;
     }
     ++n_ttft_;
-    if (value > T.ttft_thres) s.ttft_bad = 1;
-    const int32_t incr = l_incr_of(i);
-    s.ctx += incr;
-    DecodeW& w = W.dw[d];
-    w.kv_used += static_cast<int64_t>(incr) * PF.kv_bytes_per_token;
-    // Join the decode batch: first token in the next step started.
-    s.join = w.steps;
-    const int32_t dec = T.dec[round_index(i)];
-    fh_push(d, (static_cast<uint64_t>(static_cast<uint32_t>(w.steps + dec - 1)) << 32) |
-                   static_cast<uint32_t>(T.rank[i]));
-    ++w.batch_n;
-    ++w.n_new;
+    const int32_t ridx = T.round_off[i] + round - 1;
+    const int32_t incr = T.incr[ridx];
+    const int32_t dec = T.dec[ridx];
+    DecodeW& w = SM.dw[d];
+    const int32_t join = w.steps;  // first token in the next step started
+    const uint64_t key =
+        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(T.rank[i]);
+    warp_sync();
+    if (lane_id() == 0) {
+      if (value > T.ttft_thres) s.ttft_bad = 1;
+      s.ctx += incr;
+      s.join = join;
+      w.kv_used += static_cast<int64_t>(incr) * PF.kv_bytes_per_token;
+      ++w.batch_n;
+      ++w.n_new;
+    }
+    warp_sync();
+    fh_push(d, key);
     ++ctr_.tasks_completed;
   }
 
   // ---- decode workers (sim_engine.cpp:488-583) ----
-  PDG_HD void enqueue_local(int d, int32_t i) {
-    DecodeW& w = W.dw[d];
-    const double cost = t_prefill(W.sess[i].ctx, l_incr_of(i), w.deg);
-    if (!queue_push(w.q, W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap, i,
-                    cost))
+  PDG_HD void enqueue_local(int d, int32_t i, int32_t ctx, int32_t incr) {
+    DecodeW& w = SM.dw[d];
+    const double cost = t_prefill(ctx, incr, w.deg);
+    if (!queue_push(w.q, G.dq_s + static_cast<size_t>(d) * C.qcap, G.dq_c + static_cast<size_t>(d) * C.qcap, i, cost))
       return;
     advance_decode(d);
   }
 
   PDG_HD void advance_decode(int d) {
-    DecodeW& w = W.dw[d];
+    DecodeW& w = SM.dw[d];
     if (w.stepping || w.prefilling) return;
     if (w.q.qh != w.q.qt) {
       // Local prefill preempts decoding until the queue drains.
-      w.cur = select_next(w.q, W.dq_s + static_cast<size_t>(d) * C.qcap, W.dq_c + static_cast<size_t>(d) * C.qcap,
-                          &w.cur_cost);
-      w.prefilling = 1;
-      schedule(dadd(now_, w.cur_cost), kPrefillDone, static_cast<uint32_t>(PL.P + d), 0u);
+      double cost;
+      const int32_t cur = select_next(w.q, G.dq_s + static_cast<size_t>(d) * C.qcap,
+                                      G.dq_c + static_cast<size_t>(d) * C.qcap, &cost);
+      warp_sync();
+      if (lane_id() == 0) {
+        w.cur = cur;
+        w.cur_cost = cost;
+        w.prefilling = 1;
+      }
+      warp_sync();
+      set_slot(d, dadd(now_, cost), kPrefillDone);
       return;
     }
-    if (w.batch_n > 0) {
-      w.cohort_n = w.batch_n;
-      w.first_n = w.n_new;
-      w.n_new = 0;
-      ++w.steps;
-      w.stepping = 1;
-      schedule(dadd(now_, t_decode(w.cohort_n, w.deg)), kDecodeStep, static_cast<uint32_t>(PL.P + d), 0u);
+    const int32_t batch = w.batch_n;
+    if (batch > 0) {
+      double dur = w.dur;
+      if (w.dur_cohort != batch) dur = curve_eval(PF.decode[w.deg], static_cast<double>(batch));
+      const int32_t first = w.n_new;
+      warp_sync();
+      if (lane_id() == 0) {
+        w.dur = dur;
+        w.dur_cohort = batch;
+        w.cohort_n = batch;
+        w.first_n = first;
+        w.n_new = 0;
+        ++w.steps;
+        w.stepping = 1;
+      }
+      warp_sync();
+      set_slot(d, dadd(now_, dur), kDecodeStep);
     }
   }
 
+  PDG_HD void on_local_prefill_done(int d) {
+    DecodeW& w = SM.dw[d];
+    const int32_t i = w.cur;
+    warp_sync();
+    if (lane_id() == 0) w.prefilling = 0;
+    warp_sync();
+    complete_task(i, true, -1, d);
+    advance_decode(d);
+  }
+
   PDG_HD void on_decode_step(int d) {
-    DecodeW& w = W.dw[d];
-    w.stepping = 0;
+    DecodeW& w = SM.dw[d];
     const int32_t k = w.steps - 1;  // index of the step that just ended
+    const int32_t cohort = w.cohort_n;
+    const int32_t n_itl = cohort - w.first_n;
+    const double prev = w.last_step_t;
     const uint32_t lmask = static_cast<uint32_t>(C.lcap - 1);
-    double* slog = W.slog + static_cast<size_t>(d) * C.lcap;
-    slog[static_cast<uint32_t>(k) & lmask] = now_;
-    const int32_t n_itl = w.cohort_n - w.first_n;
-    if (n_itl > 0) {
-      const double gap = dsub(now_, slog[static_cast<uint32_t>(k - 1) & lmask]);
-      itl_add(d, gap, static_cast<uint32_t>(n_itl));
+    double* slog = G.slog + static_cast<size_t>(d) * C.lcap;
+    warp_sync();
+    if (lane_id() == 0) {
+      slog[static_cast<uint32_t>(k) & lmask] = now_;
+      w.stepping = 0;
+      w.last_step_t = now_;
+      w.kv_used += static_cast<int64_t>(cohort) * PF.kv_bytes_per_token;
     }
-    ctr_.tokens_decoded += w.cohort_n;
-    w.kv_used += static_cast<int64_t>(w.cohort_n) * PF.kv_bytes_per_token;
+    warp_sync();
+    if (n_itl > 0) itl_add(d, dsub(now_, prev), static_cast<uint32_t>(n_itl));
+    ctr_.tokens_decoded += cohort;
 
     bool any_terminated = false;
-    uint64_t* fh = W.fh + static_cast<size_t>(d) * C.fcap;
-    while (w.fh_n > 0 && static_cast<int32_t>(fh[0] >> 32) <= k) {
-      if (static_cast<int32_t>(fh[0] >> 32) < k) {  // a round end was missed: invariant broken
+    while (!failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
+      if (static_cast<int32_t>(w.fh_top >> 32) < k) {  // a round end was missed
         fail();
         return;
       }
-      const uint32_t rank = static_cast<uint32_t>(fh[0]);
+      const uint32_t rank = static_cast<uint32_t>(w.fh_top);
       fh_pop(d);
       const int32_t i = T.by_rank[rank];
-      SessRt& s = W.sess[i];
-      const int32_t ridx = round_index(i);
+      SessRt& s = G.sess[i];
+      const int32_t ridx = T.round_off[i] + s.round - 1;
       const int32_t dec = T.dec[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
       for (int32_t j = s.join + 1; j <= k; ++j) {
         sum = dadd(sum, dsub(slog[static_cast<uint32_t>(j) & lmask], slog[static_cast<uint32_t>(j - 1) & lmask]));
       }
-      s.itl_sum = sum;
-      s.itl_cnt += dec - 1;
-      s.ctx += dec;
-      --w.batch_n;
-      if (s.round == T.round_off[i + 1] - T.round_off[i]) {
+      const bool last = s.round == T.round_off[i + 1] - T.round_off[i];
+      warp_sync();
+      if (lane_id() == 0) {
+        s.itl_sum = sum;
+        s.itl_cnt += dec - 1;
+        s.ctx += dec;
+        --w.batch_n;
+      }
+      warp_sync();
+      if (last) {
         terminate_session(i, d);
         any_terminated = true;
       } else {
-        schedule(dadd(now_, T.delay[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
+        heap_push(dadd(now_, T.delay[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
       }
     }
     if (any_terminated) admit_waiting();
@@ -994,70 +1443,104 @@ class Engine {
   }
 
   PDG_HD void on_interaction_done(int32_t i) {
-    ++W.sess[i].round;
-    start_round(i);
+    SessRt& s = G.sess[i];
+    const int round = s.round + 1;
+    const int bound = s.bound;
+    const int32_t ctx = s.ctx;
+    warp_sync();
+    if (lane_id() == 0) s.round = static_cast<int16_t>(round);
+    warp_sync();
+    start_round(i, round, bound, ctx);
   }
 
   // terminate_session + slo_verdict (sim_engine.cpp:591-607, 668-674).
   PDG_HD void terminate_session(int32_t i, int d) {
-    SessRt& s = W.sess[i];
-    W.dw[d].kv_used -= static_cast<int64_t>(s.ctx) * PF.kv_bytes_per_token;
-    const double mean_itl = s.itl_cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(s.itl_cnt)) : 0.0;
+    SessRt& s = G.sess[i];
+    const int32_t ctx = s.ctx;
+    const int32_t cnt = s.itl_cnt;
+    const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
     const bool ttft_ok = !s.ttft_bad;
-    const bool itl_ok = s.itl_cnt == 0 || mean_itl <= T.itl_thres;
+    const bool itl_ok = cnt == 0 || mean_itl <= T.itl_thres;
     const bool slo_ok = ttft_ok && itl_ok;
-    if (REC.sessions) {
-      pdsim_session_outcome& o = REC.sessions[att_.sessions_completed];
-      o.session_id = T.sid[i];
-      o.arrival_time = T.arrival[i];
-      o.completion_time = now_;
-      o.admission_wait = dsub(s.bind_time, T.arrival[i]);
-      o.mean_itl = mean_itl;
-      o.rounds = T.round_off[i + 1] - T.round_off[i];
-      o.ttft_ok = ttft_ok;
-      o.itl_ok = itl_ok;
-      o.slo_ok = slo_ok;
-      o.reserved = 0;
+    warp_sync();
+    if (lane_id() == 0) {
+      SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PF.kv_bytes_per_token;
+      if (REC.sessions) {
+        pdsim_session_outcome& o = REC.sessions[att_.sessions_completed];
+        o.session_id = T.sid[i];
+        o.arrival_time = T.arrival[i];
+        o.completion_time = now_;
+        o.admission_wait = dsub(s.bind_time, T.arrival[i]);
+        o.mean_itl = mean_itl;
+        o.rounds = T.round_off[i + 1] - T.round_off[i];
+        o.ttft_ok = ttft_ok;
+        o.itl_ok = itl_ok;
+        o.slo_ok = slo_ok;
+        o.reserved = 0;
+      }
     }
+    warp_sync();
     ++att_.sessions_completed;
     att_.slo_ok += slo_ok;
     att_.ttft_ok += ttft_ok;
     att_.itl_ok += itl_ok;
   }
 
-  // ---- finisher heap: u64 keys (end_step << 32 | id rank), min at [0] ----
+  // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
   PDG_HD void fh_push(int d, uint64_t key) {
-    DecodeW& w = W.dw[d];
-    if (w.fh_n >= C.fcap) {
+    DecodeW& w = SM.dw[d];
+    const int32_t n = w.fh_n;
+    if (n >= C.fcap) {
       fail();
       return;
     }
-    uint64_t* h = W.fh + static_cast<size_t>(d) * C.fcap;
-    int32_t i = w.fh_n++;
-    while (i > 0) {
-      const int32_t par = (i - 1) >> 1;
-      if (h[par] <= key) break;
-      h[i] = h[par];
-      i = par;
+    uint64_t* h = G.fh + static_cast<size_t>(d) * C.fcap;
+    const uint64_t top = w.fh_top;
+    warp_sync();
+    if (lane_id() == 0) {
+      int32_t i = n;
+      while (i > 0) {
+        const int32_t par = (i - 1) >> 1;
+        const uint64_t pv = h[par];
+        if (pv <= key) break;
+        h[i] = pv;
+        i = par;
+      }
+      h[i] = key;
+      w.fh_n = n + 1;
+      if (n == 0 || key < top) w.fh_top = key;
     }
-    h[i] = key;
+    warp_sync();
   }
 
   PDG_HD void fh_pop(int d) {
-    DecodeW& w = W.dw[d];
-    uint64_t* h = W.fh + static_cast<size_t>(d) * C.fcap;
-    const uint64_t last = h[--w.fh_n];
-    const int32_t n = w.fh_n;
-    int32_t i = 0;
-    for (;;) {
-      int32_t c = 2 * i + 1;
-      if (c >= n) break;
-      if (c + 1 < n && h[c + 1] < h[c]) ++c;
-      if (h[c] >= last) break;
-      h[i] = h[c];
-      i = c;
+    DecodeW& w = SM.dw[d];
+    uint64_t* h = G.fh + static_cast<size_t>(d) * C.fcap;
+    warp_sync();
+    if (lane_id() == 0) {
+      const int32_t n = w.fh_n - 1;
+      const uint64_t last = h[n];
+      int32_t i = 0;
+      for (;;) {
+        int32_t c = 2 * i + 1;
+        if (c >= n) break;
+        uint64_t cv = h[c];
+        if (c + 1 < n) {
+          const uint64_t cv2 = h[c + 1];
+          if (cv2 < cv) {
+            ++c;
+            cv = cv2;
+          }
+        }
+        if (cv >= last) break;
+        h[i] = cv;
+        i = c;
+      }
+      if (n > 0) h[i] = last;
+      w.fh_n = n;
+      w.fh_top = n > 0 ? h[0] : 0;
     }
-    if (n > 0) h[i] = last;
+    warp_sync();
   }
 };
 

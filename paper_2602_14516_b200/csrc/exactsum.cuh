@@ -102,11 +102,39 @@ PDG_HD int mean_le_certified(const ExactSum& s, double thr) {
   return -1;
 }
 
-// Bracket of a fold value: either exact (lo == hi == value) or [lo, hi].
-struct Bracket {
-  double lo, hi;
-  int32_t exact;
-  int32_t known;  // lo/hi valid
+// Running prefix of a lazily trimmed window: the window's exact sum is the
+// difference of two prefixes. Sums wrap modulo 2^128 (unsigned arithmetic),
+// which keeps every in-window difference exact.
+typedef unsigned __int128 ufx_t;
+
+struct Pfx {
+  ufx_t sum;
+  int64_t terms;
+  int32_t inexact;
+  int32_t reserved;
+
+  PDG_HD void clear() {
+    sum = 0;
+    terms = 0;
+    inexact = 0;
+    reserved = 0;
+  }
+  PDG_HD void add(double x, int64_t count) {
+    fx_t f;
+    if (!to_fx(x, &f)) ++inexact;
+    sum += static_cast<ufx_t>(f) * static_cast<ufx_t>(count);
+    terms += count;
+  }
 };
+
+// Decides fl(fold / n) <= thr for the window [head, tail) given both prefixes.
+PDG_HD int window_mean_le(const Pfx& tail, const Pfx& head, double thr) {
+  ExactSum s;
+  s.sum = static_cast<fx_t>(tail.sum - head.sum);
+  s.terms = tail.terms - head.terms;
+  s.inexact = tail.inexact - head.inexact;
+  s.reserved = 0;
+  return mean_le_certified(s, thr);
+}
 
 }  // namespace pdg

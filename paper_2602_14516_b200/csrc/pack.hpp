@@ -270,6 +270,9 @@ inline bool pack_plan(const pdsim_plan& p, const pdsim_profile& prof, DevPlan* o
   }
   if (D == 0) return err->set(PDSIM_ERR_CONFIG, "plan: at least one decode replica is required");
   if (P + D > PDSIM_MAX_WORKERS) return err->set(PDSIM_ERR_CONFIG, "plan: more than PDSIM_MAX_WORKERS replicas");
+  if (D + 2 * P > kMaxSlots) {
+    return err->set(PDSIM_ERR_CONFIG, "plan: decode + 2 x prefill replicas exceeds the engine's 64 event slots");
+  }
   out->P = P;
   out->D = D;
   return true;
@@ -321,7 +324,7 @@ inline double curve_max_upto(const pdsim_curve& c, double hi) {
 // Workspace capacities: provable upper bounds for every ring and heap of a
 // replay.
 inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax, int dmax,
-                         const pdsim_profile& prof, const pdsim_sched_params& prm) {
+                         const pdsim_profile& prof, const pdsim_sched_params& prm, size_t smem_budget = 0) {
   Caps c{};
   int64_t S = 1, R = 1, maxdec = 1, maxincr = 1, tdec = 1;
   for (const PackedTrace* t : traces) {
@@ -352,10 +355,22 @@ inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax
   c.pmax = std::max(pmax, 0);
   c.dmax = std::max(dmax, 1);
   c.hcap = static_cast<int32_t>(S + 2 * c.pmax + c.dmax + 8);
+  // Session-event heap entries kept in shared memory (the rest spills).
+  c.hs = 1;
+  {
+    Caps probe = c;
+    probe.hs = 0;
+    const size_t fixed = smem_slot_bytes(probe, nullptr, nullptr);
+    const size_t budget = smem_budget ? smem_budget : (size_t(48) << 10);
+    const size_t room = budget > fixed ? (budget - fixed) / sizeof(HEv) : 1;
+    c.hs = static_cast<int32_t>(std::max<size_t>(1, std::min<size_t>(room, static_cast<size_t>(c.hcap))));
+  }
   c.qcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(S, 2)));
   c.fcap = static_cast<int32_t>(std::max<int64_t>(S, 2));
-  c.twcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(tw, 2)));
-  c.iwcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(iw, 2)));
+  // Windows are trimmed lazily (at queries, or when full): twice the
+  // in-window bound keeps forced trims rare.
+  c.twcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(2 * tw + 2, 4)));
+  c.iwcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(2 * iw + 2, 4)));
   c.lcap = static_cast<int32_t>(pow2_at_least(maxdec + 2));
   return c;
 }

@@ -14,6 +14,7 @@
 
 namespace {
 thread_local std::string g_err;
+size_t g_smem_budget = 0;  // 0: the device default; small values force heap spills
 int fail(const pdg::HostError& e) {
   g_err = e.msg;
   return e.code;
@@ -43,11 +44,16 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
     err.set(PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
     return fail(err);
   }
-  const pdg::Caps caps = pdg::compute_caps({&t}, dp.P, dp.D, *prof, *params);
-  std::vector<char> ws(pdg::slot_bytes(caps, nullptr, nullptr) + 256);
-  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws.data()) + 255) & ~uintptr_t(255));
-  pdg::Slot slot;
-  pdg::slot_bytes(caps, &slot, base);
+  const pdg::Caps caps = pdg::compute_caps({&t}, dp.P, dp.D, *prof, *params, g_smem_budget);
+  std::vector<char> gws(pdg::global_slot_bytes(caps, nullptr, nullptr) + 256);
+  std::vector<char> sws(pdg::smem_slot_bytes(caps, nullptr, nullptr) + 256);
+  auto align = [](std::vector<char>& v) {
+    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(v.data()) + 255) & ~uintptr_t(255));
+  };
+  pdg::GlobalSlot gslot;
+  pdg::global_slot_bytes(caps, &gslot, align(gws));
+  pdg::SmemSlot sslot;
+  pdg::smem_slot_bytes(caps, &sslot, align(sws));
   pdg::DevTrace dt;
   dt.S = t.S;
   dt.R = t.R;
@@ -65,7 +71,7 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   dt.by_rank = t.by_rank.data();
   const pdg::DevParams dprm = pdg::to_dev_params(*params);
   pdg::Records rec{out->decisions, out->ttft_samples, out->sessions};
-  pdg::Engine eng(dt, dp, *prof, dprm, caps, slot, rec, seed);
+  pdg::Engine eng(dt, dp, *prof, dprm, caps, sslot, gslot, rec, seed);
   pdg::PairResult res;
   std::memset(&res, 0, sizeof(res));
   eng.run(&res);
@@ -83,6 +89,8 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
 }
 
 }  // extern "C"
+
+extern "C" void hostsim_set_smem_budget(size_t bytes) { g_smem_budget = bytes; }
 
 extern "C" double hostsim_fold_repeat(double s, double g, uint64_t count) {
   return pdg::fold_repeat(s, g, count);

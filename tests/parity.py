@@ -127,3 +127,111 @@ def diff_runs(got, want):
 def assert_same_run(got, want):
     errs = diff_runs(got, want)
     assert not errs, "\n".join(errs[:10])
+
+
+# ---- canonical digests (golden fixtures) ------------------------------------
+
+def _fnv(text):
+    h = 1469598103934665603
+    for c in text.encode():
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
+def _fmt(v):
+    return float(v).hex() if isinstance(v, float) else str(int(v))
+
+
+def record_lines(run):
+    """Canonical text of every record (floats as exact hex)."""
+    dec = []
+    for d in run.decisions:
+        f = [d.time, d.session_id, d.round, d.local, d.worker, d.rationale, d.has_estimate]
+        if d.has_estimate:
+            f.append(d.estimated_cost)
+        dec.append(",".join(_fmt(x) for x in f))
+    ttft = [",".join(_fmt(getattr(t, k)) for k in TTFT_FIELDS) for t in run.ttft_samples]
+    sess = [",".join(_fmt(getattr(s, k)) for k in SESS_FIELDS) for s in run.sessions]
+    return dec, ttft, sess
+
+
+def digest(run):
+    dec, ttft, sess = record_lines(run)
+    return {
+        "counters": {f: int(getattr(run.counters, f)) for f in CTR_FIELDS},
+        "attainment": {f: int(getattr(run.attainment, f)) for f in ATT_FIELDS},
+        "decisions": _fnv("\n".join(dec)),
+        "ttft_samples": _fnv("\n".join(ttft)),
+        "sessions": _fnv("\n".join(sess)),
+    }
+
+
+def trace_digest(view):
+    import numpy as np
+    S, R = view.n_sessions, view.n_rounds
+    parts = [np.ctypeslib.as_array(view.session_id, (S,)).tobytes(),
+             np.ctypeslib.as_array(view.arrival_time, (S,)).tobytes(),
+             np.ctypeslib.as_array(view.round_offset, (S + 1,)).tobytes(),
+             np.ctypeslib.as_array(view.incr_input_len, (R,)).tobytes(),
+             np.ctypeslib.as_array(view.decode_len, (R,)).tobytes(),
+             np.ctypeslib.as_array(view.interaction_delay, (R,)).tobytes()]
+    import hashlib
+    h = hashlib.sha256()
+    for p in parts:
+        h.update(p)
+    h.update(float(view.ttft_thres).hex().encode() + float(view.itl_thres).hex().encode())
+    return h.hexdigest()[:16]
+
+
+def profile_digest(profile):
+    import hashlib
+    return hashlib.sha256(bytes(profile)).hexdigest()[:16]
+
+
+# ---- golden case inputs ---------------------------------------------------------
+
+def build_case(case):
+    """Materialises a golden case's inputs with the product generators."""
+    from paper_2602_14516_b200 import native
+    spec = native.default_synth_spec()
+    for k, v in case.get("spec", {}).items():
+        if k == "degrees":
+            spec.n_degrees = len(v)
+            for i, d in enumerate(v):
+                spec.degrees[i] = d
+        else:
+            setattr(spec, k, v)
+    prof = native.synth_profile(spec, case["profile_seed"])
+    if "sessions_manual" in case:
+        trace = manual_trace(case["sessions_manual"], case["slo"])
+    else:
+        st = native.preset_stats(case["preset"])
+        for k, v in case.get("stats", {}).items():
+            setattr(st, k, v)
+        trace = native.gen_trace(st, case["rate"], case["n"], case["gen_seed"])
+    plan = abi.make_plan({int(k): v for k, v in case["x"].items()}, {int(k): v for k, v in case["y"].items()})
+    params = abi.default_params(**case.get("params", {}))
+    return trace, plan, prof, params
+
+
+class ManualTrace:
+    def __init__(self, sessions, slo):
+        sid, arr, off, inc, dec, dl = [], [], [0], [], [], []
+        for s in sessions:
+            sid.append(s["id"])
+            arr.append(s["arrival"])
+            for r in s["rounds"]:
+                inc.append(r[0])
+                dec.append(r[1])
+                dl.append(r[2])
+            off.append(len(inc))
+        self._arrays = [(C.c_int64 * max(len(sid), 1))(*sid), (C.c_double * max(len(arr), 1))(*arr),
+                        (C.c_int64 * len(off))(*off), (C.c_int64 * max(len(inc), 1))(*inc),
+                        (C.c_int64 * max(len(dec), 1))(*dec), (C.c_double * max(len(dl), 1))(*dl)]
+        a = self._arrays
+        self.view = abi.Trace(len(sid), len(inc), a[0], a[1], a[2], a[3], a[4], a[5], slo[0], slo[1])
+
+
+def manual_trace(sessions, slo):
+    return ManualTrace(sessions, slo)
