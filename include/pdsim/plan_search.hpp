@@ -1,0 +1,45 @@
+// pdsim/plan_search.hpp — the batched replay search (new; the reference has
+// no batched API — its "batch" is the serial sweep loop, pdsim.cpp:547-586):
+// every candidate x replica pair replayed on the GPU, SLO attainment scored
+// per pair, argmax over candidates (max total slo_ok, ties -> smallest index).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "pdsim/perf_model.hpp"
+#include "pdsim/planner.hpp"
+#include "pdsim/sim_engine.hpp"
+#include "pdsim/workload.hpp"
+
+namespace pdsim {
+
+struct PairAttainment {
+  std::int64_t sessions_total = 0;
+  std::int64_t sessions_completed = 0;
+  std::int64_t slo_ok = 0;
+  std::int64_t ttft_ok = 0;
+  std::int64_t itl_ok = 0;
+  bool valid = true;  // false: run() would throw ConfigError (e.g. KV precheck)
+};
+
+struct SearchOptions {
+  int device = -1;             // -1: $PDSIM_DEVICE or 0
+  std::int64_t pair_begin = 0;  // shard [pair_begin, pair_end) of c * replicas + r
+  std::int64_t pair_end = -1;
+};
+
+struct SearchResult {
+  int best_candidate = -1;  // argmax; -1 when no candidate is valid
+  std::int64_t best_slo_ok = -1;
+  std::vector<std::int64_t> candidate_slo_ok;  // -1 marks an invalid candidate
+  std::vector<PairAttainment> pairs;
+  double kernel_ms = 0.0;
+  double device_ms = 0.0;
+};
+
+SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<DeploymentPlan>& candidates,
+                         const PerfProfile& profile, const SchedulerParams& params, std::uint64_t engine_seed,
+                         const SearchOptions& options = {});
+
+}  // namespace pdsim

@@ -129,4 +129,11 @@ def c5(model="llama3-8b", rates=None, seeds=4, sessions=1000, total_gpus=8):
                     f"{model}, {len(plans)} plans x {len(trs)} toolbench traces ({len(rates)} rates x {seeds} seeds)")
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C5": c5}
+def c2_small():
+    """C2 with a 2000-session trace (profiling / quick checks only)."""
+    wl = c2(sessions=2000)
+    wl.name = "C2s"
+    return wl
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C5": c5}

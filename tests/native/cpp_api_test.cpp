@@ -1,0 +1,127 @@
+// tests/native/cpp_api_test.cpp — exercises the C++ drop-in API
+// (include/pdsim/*.hpp) the way the reference's own suites do
+// (proj/tests/sim_engine_test.cpp): closed-form timelines, conservation,
+// determinism, config errors, and a small batched search. Needs a B200.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "pdsim/errors.hpp"
+#include "pdsim/plan_search.hpp"
+#include "pdsim/planner.hpp"
+#include "pdsim/sim_engine.hpp"
+#include "pdsim/workload.hpp"
+
+using namespace pdsim;
+
+static int failures = 0;
+#define CHECK(c)                                                   \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      ++failures;                                                  \
+    }                                                              \
+  } while (0)
+
+static bool near(double a, double b) { return std::fabs(a - b) <= 1e-12 * std::max(1.0, std::fabs(b)); }
+
+static DeploymentPlan simple_plan(int prefill, int decode, int degree = 1) {
+  DeploymentPlan plan;
+  if (prefill > 0) plan.x[degree] = prefill;
+  plan.y[degree] = decode;
+  plan.feasible = true;
+  plan.gpus_used = plan.gpus();
+  return plan;
+}
+
+int main() {
+  const PerfProfile p = synth_profile(SynthProfileSpec{}, 4);
+  Trace t;
+  t.name = "manual";
+  t.slo = {5.0, 0.5};
+  SessionSpec s;
+  s.session_id = 0;
+  s.arrival_time = 0.0;
+  s.rounds = {{700, 3, 0.5}, {250, 2, 0.0}};
+  t.sessions.push_back(s);
+
+  // Remote path timeline (sim_engine_test.cpp:75-119).
+  SchedulerParams remote;
+  remote.routing = RoutingMode::kAlwaysRemote;
+  const SimResult r = run(t, simple_plan(1, 1), p, remote, 1);
+  const ParallelismStrategy th{1};
+  const double td = t_decode(p, 1, th);
+  const double t1 = t_prefill(p, 0, 700, th) + t_kv(p, 700, th, th);
+  const double i1 = t1 + 3.0 * td + 0.5;
+  const double t2 = t_kv(p, 703, th, th) + t_prefill(p, 703, 250, th) + t_kv(p, 250, th, th);
+  const double end = i1 + t2 + 2.0 * td;
+  CHECK(r.ttft_samples.size() == 2);
+  CHECK(near(r.ttft_samples[0].value, t1));
+  CHECK(near(r.ttft_samples[1].value, t2));
+  CHECK(r.sessions.size() == 1 && near(r.sessions[0].completion_time, end));
+  CHECK(r.counters.tokens_decoded == 5 && r.counters.kv_bytes_residual == 0);
+
+  // Idle-cluster TTFT equals the estimate exactly (sim_engine_test.cpp:269-294).
+  Trace one = t;
+  one.sessions[0].rounds = {{500, 2, 0.0}};
+  const SimResult rr = run(one, simple_plan(1, 1), p, remote, 1);
+  CHECK(rr.ttft_samples[0].value == t_prefill(p, 0, 500, th) + t_kv(p, 500, th, th));
+
+  // Conservation on a generated workload (sim_engine_test.cpp:141-167).
+  const Trace gen = gen_trace(preset_stats("toolbench"), 6.0, 300, 21);
+  std::int64_t rounds = 0, decode = 0;
+  for (const SessionSpec& x : gen.sessions) {
+    rounds += static_cast<std::int64_t>(x.rounds.size());
+    decode += x.total_decode();
+  }
+  for (RoutingMode mode : {RoutingMode::kAdaptive, RoutingMode::kAlwaysRemote, RoutingMode::kAlwaysLocal}) {
+    SchedulerParams prm;
+    prm.routing = mode;
+    const SimResult g = run(gen, simple_plan(2, 2), p, prm, 5);
+    CHECK(g.sessions.size() == 300);
+    CHECK(g.counters.tasks_created == rounds && g.counters.tasks_completed == rounds);
+    CHECK(g.counters.tokens_decoded == decode && g.counters.kv_bytes_residual == 0);
+    CHECK(static_cast<std::int64_t>(g.decisions.size()) == rounds);
+  }
+
+  // Determinism (sim_engine_test.cpp:169-179).
+  const Trace gaia = gen_trace(preset_stats("gaia"), 4.0, 150, 8);
+  const SimResult a = run(gaia, simple_plan(2, 2), p, SchedulerParams{}, 33);
+  const SimResult b = run(gaia, simple_plan(2, 2), p, SchedulerParams{}, 33);
+  CHECK(a.decisions.size() == b.decisions.size());
+  for (size_t k = 0; k < a.decisions.size() && k < b.decisions.size(); ++k) {
+    CHECK(a.decisions[k].time == b.decisions[k].time && a.decisions[k].worker == b.decisions[k].worker);
+  }
+
+  // Validation (sim_engine_test.cpp:306-331).
+  bool threw = false;
+  try {
+    DeploymentPlan no_decode;
+    no_decode.x[1] = 1;
+    no_decode.feasible = true;
+    no_decode.gpus_used = 1;
+    run(t, no_decode, p, SchedulerParams{}, 1);
+  } catch (const ConfigError&) {
+    threw = true;
+  }
+  CHECK(threw);
+
+  // Batched search over the 13 N=4 candidates.
+  const std::vector<DeploymentPlan> cands = enumerate_plans({1, 2, 4, 8}, 4);
+  CHECK(cands.size() == 13);
+  const SearchResult sr = plan_search({gen}, cands, p, SchedulerParams{}, 1);
+  CHECK(sr.best_candidate >= 0 && sr.pairs.size() == 13);
+  std::int64_t best = -1;
+  for (size_t c = 0; c < cands.size(); ++c) {
+    const SimResult one_run = run(gen, cands[c], p, SchedulerParams{}, 1);
+    std::int64_t ok = 0;
+    for (const SessionOutcome& o : one_run.sessions) ok += o.slo_ok;
+    CHECK(ok == sr.candidate_slo_ok[c]);
+    if (ok > best) best = ok;
+  }
+  CHECK(sr.best_slo_ok == best);
+
+  std::printf("cpp_api_test: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
+  return failures ? 1 : 0;
+}

@@ -1,0 +1,90 @@
+"""World-size-2 gloo test of the sharded search host logic: two ranks each
+replay half of the pairs (with the CPU checker standing in for the GPU
+engine) and the all-reduced argmax equals the single-process search."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2602_14516_b200 import abi, distributed, native
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _inputs():
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    traces = [native.gen_trace(native.preset_stats("toolbench"), 14.0, 120, s) for s in (1, 2)]
+    plans = native.enumerate_plans([1, 2, 4, 8], 4)
+    return prof, traces, plans
+
+
+def _shard_counts(b, e, prof, traces, plans):
+    """CPU checker for one shard: per-candidate slo_ok (-1 invalid)."""
+    from tests import parity
+    nt = len(traces)
+    out = [0] * len(plans)
+    for p in range(b, e):
+        c, r = divmod(p, nt)
+        try:
+            run = parity.oracle_run(traces[r].view, plans[c], prof, abi.default_params(), 1)
+            if out[c] >= 0:
+                out[c] += run.attainment.slo_ok
+        except Exception:
+            out[c] = -1
+    return out
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prof, traces, plans = _inputs()
+    n_pairs = len(traces) * len(plans)
+    best, cnt, totals = distributed.sharded_search(
+        lambda b, e: _shard_counts(b, e, prof, traces, plans), n_pairs, rank, world)
+    q.put((rank, best, cnt, totals.tolist()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_argmax_matches_single_process():
+    prof, traces, plans = _inputs()
+    n_pairs = len(traces) * len(plans)
+    full = _shard_counts(0, n_pairs, prof, traces, plans)
+    want_best = max(range(len(full)), key=lambda c: (full[c], -c))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, best, cnt, totals in res:
+        assert totals == full
+        assert best == want_best
+        assert cnt == full[want_best]
+
+
+def test_shard_ranges_partition_the_pairs():
+    for n in (1, 7, 169, 2704):
+        for world in (1, 2, 3, 8):
+            spans = [distributed.shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_argmax_ties_and_invalid():
+    t = torch.tensor([5, 7, -1, 7, 3])
+    assert distributed.argmax(t) == (1, 7)
+    assert distributed.argmax(torch.tensor([-1, -1])) == (-1, -1)
