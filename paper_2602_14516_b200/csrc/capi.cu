@@ -30,8 +30,6 @@ namespace {
 
 thread_local std::string g_last_error;
 
-__constant__ pdsim_profile c_profile;
-
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -153,7 +151,7 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      pdg::Engine eng(tr, pl, c_profile, a.params, a.caps, sslot, gslot, a.rec, a.seed);
+      pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed);
       eng.run(&res);
       res.cycles = clock64() - t0;
     }
@@ -301,7 +299,7 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   CU(ctx, ctx->d_invalid.reserve(ctx->pair_invalid.size()));
   CU(ctx, cudaMemcpyAsync(ctx->d_invalid.p, ctx->pair_invalid.data(), ctx->pair_invalid.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyToSymbolAsync(c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice,
+  CU(ctx, cudaMemcpyToSymbolAsync(pdg::c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice,
                                   ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (h2d_bytes) {

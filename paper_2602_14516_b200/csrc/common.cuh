@@ -10,8 +10,10 @@
 
 #if defined(__CUDACC__)
 #define PDG_HD __host__ __device__ __forceinline__
+#define PDG_COLD __host__ __device__ __noinline__  // cold paths: keep the hot loop small
 #else
 #define PDG_HD inline
+#define PDG_COLD inline
 #endif
 
 namespace pdg {

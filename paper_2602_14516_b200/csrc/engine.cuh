@@ -258,8 +258,11 @@ struct Caps {
   int32_t dmax;
 };
 
+struct EngState;
+
 // Shared-memory part of a workspace slot.
 struct SmemSlot {
+  EngState* es;
   PrefillW* pw;
   DecodeW* dw;
   uint64_t* mt;    // 312 words
@@ -289,6 +292,8 @@ struct GlobalSlot {
 PDG_HD size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 PDG_HD size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
+constexpr size_t kEngStateBytes = 2048;  // >= sizeof(EngState), checked below
+
 PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
   size_t off = 0;
   auto take = [&](size_t bytes) -> char* {
@@ -297,6 +302,7 @@ PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
     return p;
   };
   SmemSlot t;
+  t.es = reinterpret_cast<EngState*>(take(kEngStateBytes));
   t.pw = reinterpret_cast<PrefillW*>(take(sizeof(PrefillW) * static_cast<size_t>(c.pmax > 0 ? c.pmax : 1)));
   t.dw = reinterpret_cast<DecodeW*>(take(sizeof(DecodeW) * static_cast<size_t>(c.dmax)));
   t.mt = reinterpret_cast<uint64_t*>(take(8 * 312));
@@ -379,23 +385,86 @@ PDG_HD void unrank_perm(int64_t k, int m, int* perm) {
   }
 }
 
+// All mutable engine state of one warp-slot lives in shared memory (one
+// instance per warp); the Engine object itself is a single pointer, so the
+// compiler keeps nothing of it on the stack. Warp-uniform fields are written
+// with the same value by every lane.
+struct EngState {
+  DevTrace T;
+  DevPlan PL;
+  DevParams PR;
+  Caps C;
+  SmemSlot SM;
+  GlobalSlot G;
+  Records REC;
+  uint64_t seed_;
+  double now_;
+  double next_arr_t_;
+  uint64_t seq_;
+  int32_t hn_;
+  int32_t heap_spilled_;
+  int32_t next_arr_;
+  int32_t adm_head_;
+  int32_t rr_next_;
+  uint32_t mt_idx_;
+  int32_t failed_;
+  int32_t nslots_;
+  pdsim_attainment att_;
+  pdsim_counters ctr_;
+  int64_t n_dec_;
+  int64_t n_ttft_;
+  int64_t events_;
+  int64_t folds_;
+  double st_[kMaxSlots];    // worker-event slot times (+inf when empty)
+  uint64_t sk_[kMaxSlots];  // worker-event slot keys
+};
+
+#if defined(__CUDACC__)
+__constant__ pdsim_profile c_profile;  // the cost model, broadcast from the constant cache
+#endif
+inline const pdsim_profile*& host_profile() {  // host (test) builds only
+  static thread_local const pdsim_profile* p = nullptr;
+  return p;
+}
+#if defined(__CUDA_ARCH__)
+#define PDG_PROF c_profile
+#else
+#define PDG_PROF (*host_profile())
+#endif
+
+static_assert(sizeof(EngState) <= kEngStateBytes, "EngState outgrew its shared-memory reservation");
+
 class Engine {
  public:
-  PDG_HD Engine(const DevTrace& tr, const DevPlan& plan, const pdsim_profile& prof, const DevParams& prm,
-                const Caps& caps, const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed)
-      : T(tr), PL(plan), PF(prof), PR(prm), C(caps), SM(sm), G(gm), REC(rec), seed_(seed) {}
+  // `es` must point at this warp's EngState (shared memory on the device).
+  PDG_HD Engine(EngState* es, const DevTrace& tr, const DevPlan& plan, const DevParams& prm, const Caps& caps,
+                const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed)
+      : s_(es) {
+    s_->T = tr;
+    s_->PL = plan;
+    s_->PR = prm;
+    s_->C = caps;
+    s_->SM = sm;
+    s_->G = gm;
+    s_->REC = rec;
+    s_->seed_ = seed;
+    warp_sync();
+  }
 
   PDG_HD void run(PairResult* out) {
     init();
-    const int D = PL.D, P = PL.P;
-    while (!failed_) {
-      // Next worker event: min over the register-resident slots.
+    const int D = s_->PL.D, P = s_->PL.P;
+    const int nslots = s_->nslots_;
+    while (!s_->failed_) {
+      // Next worker event: min over the slot table (lanes split the slots).
       double bt = kInf;
       uint64_t bk = ~0ull;
-      for (int j = 0; j < kSlotsPerLane; ++j) {
-        if (before(st_[j], sk_[j], bt, bk)) {
-          bt = st_[j];
-          bk = sk_[j];
+      for (int j = lane_id(); j < nslots; j += PDG_NL) {
+        const double t = s_->st_[j];
+        const uint64_t k = s_->sk_[j];
+        if (before(t, k, bt, bk)) {
+          bt = t;
+          bk = k;
         }
       }
       for (int m = PDG_NL / 2; m > 0; m >>= 1) {
@@ -407,7 +476,7 @@ class Engine {
         }
       }
       int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
-      if (hn_ > 0) {
+      if (s_->hn_ > 0) {
         const HEv* h = heap_base();
         const double ht = h[0].t;
         const uint64_t hk = h[0].key;
@@ -419,17 +488,17 @@ class Engine {
       }
       // Arrivals carry kind 0 and seq = index: they precede every dynamic
       // event at an equal time (sim_engine.cpp:137-143).
-      if (next_arr_ < T.S && (src < 0 || next_arr_t_ <= bt)) src = 2;
+      if (s_->next_arr_ < s_->T.S && (src < 0 || s_->next_arr_t_ <= bt)) src = 2;
       if (src < 0) break;
       if (src == 2) {
-        const int32_t i = next_arr_++;
-        const double t = next_arr_t_;
-        if (next_arr_ < T.S) next_arr_t_ = T.arrival[next_arr_];
+        const int32_t i = s_->next_arr_++;
+        const double t = s_->next_arr_t_;
+        if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = s_->T.arrival[s_->next_arr_];
         advance_to(t);
         on_arrival(i);
         continue;
       }
-      ++events_;
+      ++s_->events_;
       advance_to(bt);
       const uint32_t kind = static_cast<uint32_t>(bk >> 58);
       if (src == 1) {
@@ -455,99 +524,82 @@ class Engine {
         on_history_read(s - D - P);
       }
     }
-    for (int d = 0; d < PL.D; ++d) ctr_.kv_bytes_residual += SM.dw[d].kv_used;
-    out->att = att_;
-    out->att.sessions_total = T.S;
-    out->ctr = ctr_;
-    out->n_decisions = n_dec_;
-    out->n_ttft = n_ttft_;
-    out->events = events_;
-    out->exact_folds = folds_;
-    out->status = failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
+    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += s_->SM.dw[d].kv_used;
+    out->att = s_->att_;
+    out->att.sessions_total = s_->T.S;
+    out->ctr = s_->ctr_;
+    out->n_decisions = s_->n_dec_;
+    out->n_ttft = s_->n_ttft_;
+    out->events = s_->events_;
+    out->exact_folds = s_->folds_;
+    out->status = s_->failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
   }
 
  private:
-  const DevTrace& T;
-  const DevPlan& PL;
-  const pdsim_profile& PF;
-  const DevParams& PR;
-  const Caps& C;
-  const SmemSlot& SM;
-  const GlobalSlot& G;
-  Records REC;
-  uint64_t seed_;
+  EngState* s_;
 
-  // Warp-uniform scalar state (registers).
-  double now_ = 0.0;
-  double next_arr_t_ = 0.0;
-  uint64_t seq_ = 0;
-  int32_t hn_ = 0;
-  bool heap_spilled_ = false;
-  int32_t next_arr_ = 0;
-  int32_t adm_head_ = 0;
-  int32_t rr_next_ = 0;
-  uint32_t mt_idx_ = 0;
-  bool failed_ = false;
-  pdsim_attainment att_{};
-  pdsim_counters ctr_{};
-  int64_t n_dec_ = 0;
-  int64_t n_ttft_ = 0;
-  int64_t events_ = 0;
-  int64_t folds_ = 0;
-  // Per-lane worker-event slots.
-  double st_[kSlotsPerLane];
-  uint64_t sk_[kSlotsPerLane];
-
-  PDG_HD void fail() { failed_ = true; }
+  PDG_HD void fail() { s_->failed_ = 1; }
 
   PDG_HD void advance_to(double t) {
-    if (t < now_) ctr_.events_in_order = 0;  // sim_engine.cpp:148-150
-    now_ = t;
+    if (t < s_->now_) s_->ctr_.events_in_order = 0;  // sim_engine.cpp:148-150
+    s_->now_ = t;
   }
 
-  PDG_HD void init() {
-    now_ = 0.0;
-    seq_ = static_cast<uint64_t>(T.S);  // arrivals took seq 0..S-1
-    hn_ = 0;
-    heap_spilled_ = false;
-    next_arr_ = 0;
-    next_arr_t_ = T.S > 0 ? T.arrival[0] : 0.0;
-    adm_head_ = 0;
-    rr_next_ = 0;
-    ctr_.events_in_order = 1;
-    for (int j = 0; j < kSlotsPerLane; ++j) {
-      st_[j] = kInf;
-      sk_[j] = ~0ull;
+  PDG_COLD void init() {
+    s_->now_ = 0.0;
+    s_->seq_ = static_cast<uint64_t>(s_->T.S);  // arrivals took seq 0..S-1
+    s_->hn_ = 0;
+    s_->heap_spilled_ = false;
+    s_->next_arr_ = 0;
+    s_->next_arr_t_ = s_->T.S > 0 ? s_->T.arrival[0] : 0.0;
+    s_->adm_head_ = 0;
+    s_->rr_next_ = 0;
+    s_->ctr_.events_in_order = 1;
+    s_->nslots_ = s_->PL.D + 2 * s_->PL.P;
+    s_->failed_ = 0;
+    s_->heap_spilled_ = 0;
+    s_->mt_idx_ = 0;
+    s_->att_ = pdsim_attainment{};
+    s_->ctr_ = pdsim_counters{};
+    s_->n_dec_ = 0;
+    s_->n_ttft_ = 0;
+    s_->events_ = 0;
+    s_->folds_ = 0;
+    s_->ctr_.events_in_order = 1;
+    for (int j = lane_id(); j < kMaxSlots; j += PDG_NL) {
+      s_->st_[j] = kInf;
+      s_->sk_[j] = ~0ull;
     }
+    warp_sync();
     if (lane_id() == 0) {
       uint32_t idx;
-      mt64_seed(SM.mt, &idx, seed_);
-      for (int p = 0; p < PL.P; ++p) {
-        PrefillW& w = SM.pw[p];
+      mt64_seed(s_->SM.mt, &idx, s_->seed_);
+      for (int p = 0; p < s_->PL.P; ++p) {
+        PrefillW& w = s_->SM.pw[p];
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.tw.tail.clear();
         w.tw.head = w.tw.end = 0;
-        w.deg = PL.pdeg[p];
+        w.deg = s_->PL.pdeg[p];
         w.cur = w.stg = -1;
         w.computing = w.staged = w.pending = 0;
         w.cur_cost = w.stg_cost = 0.0;
         w.staged_ready = 0.0;
       }
-      for (int d = 0; d < PL.D; ++d) {
-        DecodeW& w = SM.dw[d];
+      for (int d = 0; d < s_->PL.D; ++d) {
+        DecodeW& w = s_->SM.dw[d];
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.iw.tail.clear();
         w.iw.head = w.iw.end = 0;
         w.kv_used = 0;
-        w.kv_cap = static_cast<int64_t>(PF.degrees[PL.ddeg[d]]) * PF.gpu_memory_capacity;
+        w.kv_cap = static_cast<int64_t>(PDG_PROF.degrees[s_->PL.ddeg[d]]) * PDG_PROF.gpu_memory_capacity;
         w.fh_top = 0;
         w.cur_cost = 0.0;
         w.last_step_t = 0.0;
         w.dur = 0.0;
         w.dur_cohort = -1;
-        w.deg = PL.ddeg[d];
+        w.deg = s_->PL.ddeg[d];
         w.cur = -1;
         w.batch_n = w.n_new = w.cohort_n = w.first_n = 0;
         w.steps = 0;
@@ -555,33 +607,33 @@ class Engine {
         w.stepping = w.prefilling = 0;
       }
     }
-    mt_idx_ = Mt64::kN;
+    s_->mt_idx_ = Mt64::kN;
     warp_sync();
   }
 
   // ---- cost model (perf_model.cpp:158-205) ----
   PDG_HD double t_prefill(int32_t l_hist, int32_t l_incr, int deg) const {
-    const double load = dadd(static_cast<double>(l_incr), dmul(PF.history_weight, static_cast<double>(l_hist)));
-    return curve_eval(PF.prefill[deg], load);
+    const double load = dadd(static_cast<double>(l_incr), dmul(PDG_PROF.history_weight, static_cast<double>(l_hist)));
+    return curve_eval(PDG_PROF.prefill[deg], load);
   }
   PDG_HD double t_kv(int32_t l, int src, int dst) const {
     if (l == 0) return 0.0;
-    return curve_eval(PF.kv[src][dst], static_cast<double>(l));
+    return curve_eval(PDG_PROF.kv[src][dst], static_cast<double>(l));
   }
 
-  PDG_HD int32_t l_incr_of(int32_t i) const { return T.incr[T.round_off[i] + G.sess[i].round - 1]; }
+  PDG_HD int32_t l_incr_of(int32_t i) const { return s_->T.incr[s_->T.round_off[i] + s_->G.sess[i].round - 1]; }
   PDG_HD double created_of(int32_t i) const {
-    return G.sess[i].round == 1 ? T.arrival[i] : G.sess[i].t_enq;  // sim_engine.cpp:258, 283, 588
+    return s_->G.sess[i].round == 1 ? s_->T.arrival[i] : s_->G.sess[i].t_enq;  // sim_engine.cpp:258, 283, 588
   }
 
   // ---- RNG (coordinator.cpp:124-130): std::mt19937_64 in shared memory ----
-  PDG_HD uint64_t rng_next() {
-    if (mt_idx_ >= static_cast<uint32_t>(Mt64::kN)) {
+  PDG_COLD uint64_t rng_next() {
+    if (s_->mt_idx_ >= static_cast<uint32_t>(Mt64::kN)) {
 #if defined(__CUDA_ARCH__)
       // Warp-parallel twist in three dependency phases: elements below 156
       // read only old words; 156..310 read updated words i-156; 311 reads
       // updated words 0 and 155.
-      uint64_t* mt = SM.mt;
+      uint64_t* mt = s_->SM.mt;
       const int lane = lane_id();
       for (int base = 0; base < 156; base += 32) {
         const int i = base + lane;
@@ -613,60 +665,48 @@ class Engine {
         __syncwarp();
       }
 #else
-      mt64_twist(SM.mt);
+      mt64_twist(s_->SM.mt);
 #endif
-      mt_idx_ = 0;
+      s_->mt_idx_ = 0;
     }
-    return mt64_temper(SM.mt[mt_idx_++]);
+    return mt64_temper(s_->SM.mt[s_->mt_idx_++]);
   }
 
   // ---- worker-event slots (registers) ----
   PDG_HD void set_slot(int s, double t, uint32_t kind) {
-    const uint64_t key = mk_key(kind, seq_++, static_cast<uint32_t>(s));
-    if (s % PDG_NL == lane_id()) {
-      const int j = s / PDG_NL;
-      for (int k = 0; k < kSlotsPerLane; ++k) {
-        if (k == j) {
-          st_[k] = t;
-          sk_[k] = key;
-        }
-      }
-    }
+    const uint64_t seq = s_->seq_;
+    const uint64_t key = mk_key(kind, seq, static_cast<uint32_t>(s));
+    s_->seq_ = seq + 1;
+    s_->st_[s] = t;
+    s_->sk_[s] = key;
   }
   PDG_HD void clear_slot(int s) {
-    if (s % PDG_NL == lane_id()) {
-      const int j = s / PDG_NL;
-      for (int k = 0; k < kSlotsPerLane; ++k) {
-        if (k == j) {
-          st_[k] = kInf;
-          sk_[k] = ~0ull;
-        }
-      }
-    }
+    s_->st_[s] = kInf;
+    s_->sk_[s] = ~0ull;
   }
-  PDG_HD int slot_compute(int p) const { return PL.D + p; }
-  PDG_HD int slot_history(int p) const { return PL.D + PL.P + p; }
+  PDG_HD int slot_compute(int p) const { return s_->PL.D + p; }
+  PDG_HD int slot_history(int p) const { return s_->PL.D + s_->PL.P + p; }
 
   // ---- session-event heap (shared memory, global spill) ----
-  PDG_HD HEv* heap_base() const { return heap_spilled_ ? G.heap : SM.heap; }
+  PDG_HD HEv* heap_base() const { return s_->heap_spilled_ ? s_->G.heap : s_->SM.heap; }
 
-  PDG_HD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
+  PDG_COLD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
     HEv e;
     e.t = t;
-    e.key = mk_key(kind, seq_++, 0);
+    e.key = mk_key(kind, s_->seq_++, 0);
     e.a = a;
     e.b = b;
-    if (!heap_spilled_ && hn_ >= C.hs) {
-      for (int k = lane_id(); k < hn_; k += PDG_NL) G.heap[k] = SM.heap[k];
+    if (!s_->heap_spilled_ && s_->hn_ >= s_->C.hs) {
+      for (int k = lane_id(); k < s_->hn_; k += PDG_NL) s_->G.heap[k] = s_->SM.heap[k];
       warp_sync();
-      heap_spilled_ = true;
+      s_->heap_spilled_ = true;
     }
-    if (hn_ >= C.hcap) {
+    if (s_->hn_ >= s_->C.hcap) {
       fail();
       return;
     }
     HEv* h = heap_base();
-    int32_t i = hn_++;
+    int32_t i = s_->hn_++;
     while (i > 0) {
       const int32_t par = (i - 1) >> 1;
       const HEv pe = h[par];
@@ -680,16 +720,16 @@ class Engine {
     warp_sync();
   }
 
-  PDG_HD HEv heap_pop() {
+  PDG_COLD HEv heap_pop() {
     HEv* h = heap_base();
     const HEv top = h[0];
-    const HEv last = h[--hn_];
+    const HEv last = h[--s_->hn_];
     int32_t i = 0;
     for (;;) {
       int32_t c = 2 * i + 1;
-      if (c >= hn_) break;
+      if (c >= s_->hn_) break;
       HEv ce = h[c];
-      if (c + 1 < hn_) {
+      if (c + 1 < s_->hn_) {
         const HEv c2 = h[c + 1];
         if (before(c2.t, c2.key, ce.t, ce.key)) {
           ++c;
@@ -702,24 +742,24 @@ class Engine {
       i = c;
     }
     warp_sync();
-    if (hn_ > 0 && lane_id() == 0) h[i] = last;
+    if (s_->hn_ > 0 && lane_id() == 0) h[i] = last;
     warp_sync();
-    if (hn_ == 0) heap_spilled_ = false;
+    if (s_->hn_ == 0) s_->heap_spilled_ = false;
     return top;
   }
 
   // ---- admission (sim_engine.cpp:240-267; bind_session coordinator.cpp:60-72) ----
   PDG_HD void on_arrival(int32_t i) {
-    if (adm_head_ < i) return;  // queue non-empty: park behind the head
-    if (!try_admit(i)) return;  // parked: adm_head_ == i
-    adm_head_ = i + 1;
+    if (s_->adm_head_ < i) return;  // queue non-empty: park behind the head
+    if (!try_admit(i)) return;  // parked: s_->adm_head_ == i
+    s_->adm_head_ = i + 1;
   }
 
   PDG_HD int bind_session() const {  // least KV bytes, lowest index on ties
     int best = 0;
-    int64_t bv = SM.dw[0].kv_used;
-    for (int d = 1; d < PL.D; ++d) {
-      const int64_t v = SM.dw[d].kv_used;
+    int64_t bv = s_->SM.dw[0].kv_used;
+    for (int d = 1; d < s_->PL.D; ++d) {
+      const int64_t v = s_->SM.dw[d].kv_used;
       if (v < bv) {
         bv = v;
         best = d;
@@ -728,16 +768,16 @@ class Engine {
     return best;
   }
 
-  PDG_HD bool try_admit(int32_t i) {
+  PDG_COLD bool try_admit(int32_t i) {
     const int best = bind_session();
-    const DecodeW& w = SM.dw[best];
-    const int64_t first = static_cast<int64_t>(T.incr[T.round_off[i]]) * PF.kv_bytes_per_token;
+    const DecodeW& w = s_->SM.dw[best];
+    const int64_t first = static_cast<int64_t>(s_->T.incr[s_->T.round_off[i]]) * PDG_PROF.kv_bytes_per_token;
     if (w.kv_used + first > w.kv_cap) return false;
-    SessRt& s = G.sess[i];
+    SessRt& s = s_->G.sess[i];
     warp_sync();
     if (lane_id() == 0) {
       s.bound = static_cast<int8_t>(best);
-      s.bind_time = now_;
+      s.bind_time = s_->now_;
       s.round = 1;
       s.ctx = 0;
       s.itl_sum = 0.0;
@@ -752,34 +792,34 @@ class Engine {
   }
 
   PDG_HD void admit_waiting() {
-    while (adm_head_ < next_arr_ && try_admit(adm_head_)) ++adm_head_;
+    while (s_->adm_head_ < s_->next_arr_ && try_admit(s_->adm_head_)) ++s_->adm_head_;
   }
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
-  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx) {
-    SessRt& s = G.sess[i];
+  PDG_COLD void start_round(int32_t i, int round, int bound, int32_t ctx) {
+    SessRt& s = s_->G.sess[i];
     warp_sync();
     if (lane_id() == 0) {
-      s.t_enq = now_;
+      s.t_enq = s_->now_;
       s.postpone = 0;
     }
     warp_sync();
-    ++ctr_.tasks_created;
-    const int32_t incr = T.incr[T.round_off[i] + round - 1];
+    ++s_->ctr_.tasks_created;
+    const int32_t incr = s_->T.incr[s_->T.round_off[i] + round - 1];
     const RouteOut r = decide(i, bound, ctx, incr);
-    if (REC.decisions && lane_id() == 0) {
-      pdsim_decision& d = REC.decisions[n_dec_];
-      d.time = now_;
-      d.session_id = T.sid[i];
+    if (s_->REC.decisions && lane_id() == 0) {
+      pdsim_decision& d = s_->REC.decisions[s_->n_dec_];
+      d.time = s_->now_;
+      d.session_id = s_->T.sid[i];
       d.round = round;
-      d.worker = r.local ? PL.P + bound : r.p;
+      d.worker = r.local ? s_->PL.P + bound : r.p;
       d.local = static_cast<int8_t>(r.local);
       d.rationale = static_cast<int8_t>(r.rationale);
       d.has_estimate = static_cast<int8_t>(r.has_est);
       for (int k = 0; k < 5; ++k) d.reserved[k] = 0;
       d.estimated_cost = r.has_est ? r.est : 0.0;
     }
-    ++n_dec_;
+    ++s_->n_dec_;
     if (r.local) {
       enqueue_local(bound, i, ctx, incr);
     } else {
@@ -793,18 +833,18 @@ class Engine {
     r.p = -1;
     r.has_est = 0;
     r.est = 0.0;
-    if (PR.routing == PDSIM_ROUTING_ALWAYS_LOCAL) {
+    if (s_->PR.routing == PDSIM_ROUTING_ALWAYS_LOCAL) {
       r.rationale = PDSIM_RATIONALE_FORCED_LOCAL;
       return r;
     }
-    if (PR.routing == PDSIM_ROUTING_ALWAYS_REMOTE) {
-      if (PL.P == 0) {
+    if (s_->PR.routing == PDSIM_ROUTING_ALWAYS_REMOTE) {
+      if (s_->PL.P == 0) {
         r.rationale = PDSIM_RATIONALE_FORCED_LOCAL;
         return r;
       }
       r.local = 0;
-      r.p = rr_next_;
-      rr_next_ = (rr_next_ + 1) % PL.P;
+      r.p = s_->rr_next_;
+      s_->rr_next_ = (s_->rr_next_ + 1) % s_->PL.P;
       r.rationale = PDSIM_RATIONALE_FORCED_REMOTE;
       return r;
     }
@@ -813,10 +853,10 @@ class Engine {
   }
 
   // Coordinator::route (coordinator.cpp:115-171).
-  PDG_HD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
-    const int n = PL.P;
+  PDG_COLD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
+    const int n = s_->PL.P;
     if (n > 0) {
-      int32_t* order = SM.order;
+      int32_t* order = s_->SM.order;
       warp_sync();
       if (lane_id() == 0) {
         for (int k = 0; k < n; ++k) order[k] = k;
@@ -832,7 +872,7 @@ class Engine {
         }
         warp_sync();
       }
-      const double thr = dmul(PR.alpha, T.ttft_thres);
+      const double thr = dmul(s_->PR.alpha, s_->T.ttft_thres);
       for (int k = 0; k < n; ++k) {
         const int p = order[k];
         if (ttft_has_slack(p, thr)) {
@@ -843,7 +883,7 @@ class Engine {
         }
       }
     }
-    if (itl_has_slack(bound, dmul(PR.beta, T.itl_thres))) {
+    if (itl_has_slack(bound, dmul(s_->PR.beta, s_->T.itl_thres))) {
       r->local = 1;
       r->p = -1;
       r->rationale = PDSIM_RATIONALE_SLACK_LOCAL;
@@ -855,7 +895,7 @@ class Engine {
 
   // ---- routing estimates (coordinator.cpp:74-100) ----
   PDG_HD double fold_queue(const TaskQueue& q, const double* qc, double init) const {
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     double c = init;
     for (uint32_t k = q.qh; k != q.qt; ++k) c = dadd(c, qc[k & mask]);
     return c;
@@ -865,11 +905,11 @@ class Engine {
   PDG_HD void estimate(int d, int32_t ctx, int32_t incr, int c, bool force_exact, double* lo, double* hi,
                        bool* exact) const {
     if (c < 0) {
-      const DecodeW& w = SM.dw[d];
+      const DecodeW& w = s_->SM.dw[d];
       const uint32_t len = w.q.qt - w.q.qh;
       const double own = t_prefill(ctx, incr, w.deg);
       if (force_exact || len <= 2 || !w.q.sum.exact()) {
-        *lo = *hi = fold_queue(w.q, G.dq_c + static_cast<size_t>(d) * C.qcap, own);
+        *lo = *hi = fold_queue(w.q, s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, own);
         *exact = true;
         return;
       }
@@ -880,12 +920,12 @@ class Engine {
       *exact = false;
       return;
     }
-    const PrefillW& w = SM.pw[c];
-    const int pd = w.deg, dd = SM.dw[d].deg;
+    const PrefillW& w = s_->SM.pw[c];
+    const int pd = w.deg, dd = s_->SM.dw[d].deg;
     const uint32_t len = w.q.qt - w.q.qh;
     const double head = dadd(t_prefill(ctx, incr, pd), dadd(t_kv(ctx, dd, pd), t_kv(incr, pd, dd)));
     if (force_exact || len <= 2 || !w.q.sum.exact()) {
-      *lo = *hi = dadd(head, fold_queue(w.q, G.pq_c + static_cast<size_t>(c) * C.qcap, 0.0));
+      *lo = *hi = dadd(head, fold_queue(w.q, s_->G.pq_c + static_cast<size_t>(c) * s_->C.qcap, 0.0));
       *exact = true;
       return;
     }
@@ -902,9 +942,9 @@ class Engine {
   // candidates in parallel; a candidate whose bracket starts above the
   // smallest upper bound cannot win, and exact folds run only when two or
   // more candidates remain in contention.
-  PDG_HD void argmin_route(int d, int32_t ctx, int32_t incr, RouteOut* r) {
+  PDG_COLD void argmin_route(int d, int32_t ctx, int32_t incr, RouteOut* r) {
     constexpr int kPer = (kMaxSlots + PDG_NL - 1) / PDG_NL;
-    const int n = PL.P;
+    const int n = s_->PL.P;
     const int lane = lane_id();
     double llo, lhi;
     bool lex;
@@ -933,7 +973,7 @@ class Engine {
     bool est_exact;
     if (count >= 2) {
       if (lcan && !lex) {
-        ++folds_;
+        ++s_->folds_;
         estimate(d, ctx, incr, -1, true, &llo, &lhi, &lex);
       }
       double v = lcan ? llo : kInf;
@@ -976,7 +1016,7 @@ class Engine {
       est = shfl_d(lo, owner);
       est_exact = shfl_i(ex, owner) != 0;
     }
-    if (!est_exact && REC.decisions) {
+    if (!est_exact && s_->REC.decisions) {
       double a, b;
       bool e;
       estimate(d, ctx, incr, winner, true, &a, &b, &e);
@@ -992,7 +1032,7 @@ class Engine {
   // Drops entries with time <= now - window from the head (times are
   // non-decreasing, so expired entries form a prefix): one ballot per 32.
   PDG_HD void window_trim(WinState& w, const double* times, uint32_t mask) {
-    const double cutoff = dsub(now_, PR.stat_window);
+    const double cutoff = dsub(s_->now_, s_->PR.stat_window);
     uint32_t head = w.head;
     const uint32_t end = w.end;
     while (head != end) {
@@ -1020,19 +1060,19 @@ class Engine {
   }
 
   PDG_HD void ttft_add(int p, double v) {
-    PrefillW& w = SM.pw[p];
-    const size_t base = static_cast<size_t>(p) * C.twcap;
-    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
-    if (!window_room(w.tw, G.tw_t + base, static_cast<uint32_t>(C.twcap))) return;
+    PrefillW& w = s_->SM.pw[p];
+    const size_t base = static_cast<size_t>(p) * s_->C.twcap;
+    const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
+    if (!window_room(w.tw, s_->G.tw_t + base, static_cast<uint32_t>(s_->C.twcap))) return;
     const uint32_t k = w.tw.end & mask;
     const Pfx cur = w.tw.tail;
     Pfx next = cur;
     next.add(v, 1);
     warp_sync();
     if (lane_id() == 0) {
-      G.tw_t[base + k] = now_;
-      G.tw_v[base + k] = v;
-      G.tw_p[base + k] = cur;
+      s_->G.tw_t[base + k] = s_->now_;
+      s_->G.tw_v[base + k] = v;
+      s_->G.tw_p[base + k] = cur;
       w.tw.tail = next;
       ++w.tw.end;
     }
@@ -1041,36 +1081,36 @@ class Engine {
 
   // query(now) <= thr with the sequential windowed mean's semantics.
   PDG_HD bool ttft_has_slack(int p, double thr) {
-    PrefillW& w = SM.pw[p];
-    const size_t base = static_cast<size_t>(p) * C.twcap;
-    const uint32_t mask = static_cast<uint32_t>(C.twcap - 1);
-    window_trim(w.tw, G.tw_t + base, mask);
+    PrefillW& w = s_->SM.pw[p];
+    const size_t base = static_cast<size_t>(p) * s_->C.twcap;
+    const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
+    window_trim(w.tw, s_->G.tw_t + base, mask);
     const uint32_t head = w.tw.head, end = w.tw.end;
     if (head == end) return 0.0 <= thr;  // an empty window reads 0
-    const Pfx hp = G.tw_p[base + (head & mask)];
+    const Pfx hp = s_->G.tw_p[base + (head & mask)];
     const int dec = window_mean_le(w.tw.tail, hp, thr);
     if (dec >= 0) return dec == 1;
-    ++folds_;
+    ++s_->folds_;
     double sum = 0.0;
-    for (uint32_t k = head; k != end; ++k) sum = dadd(sum, G.tw_v[base + (k & mask)]);
+    for (uint32_t k = head; k != end; ++k) sum = dadd(sum, s_->G.tw_v[base + (k & mask)]);
     return ddiv(sum, static_cast<double>(end - head)) <= thr;
   }
 
   PDG_HD void itl_add(int d, double gap, uint32_t count) {
-    DecodeW& w = SM.dw[d];
-    const size_t base = static_cast<size_t>(d) * C.iwcap;
-    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
-    if (!window_room(w.iw, G.iw_t + base, static_cast<uint32_t>(C.iwcap))) return;
+    DecodeW& w = s_->SM.dw[d];
+    const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
+    const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
+    if (!window_room(w.iw, s_->G.iw_t + base, static_cast<uint32_t>(s_->C.iwcap))) return;
     const uint32_t k = w.iw.end & mask;
     const Pfx cur = w.iw.tail;
     Pfx next = cur;
     next.add(gap, count);
     warp_sync();
     if (lane_id() == 0) {
-      G.iw_t[base + k] = now_;
-      G.iw_g[base + k] = gap;
-      G.iw_c[base + k] = count;
-      G.iw_p[base + k] = cur;
+      s_->G.iw_t[base + k] = s_->now_;
+      s_->G.iw_g[base + k] = gap;
+      s_->G.iw_c[base + k] = count;
+      s_->G.iw_p[base + k] = cur;
       w.iw.tail = next;
       ++w.iw.end;
     }
@@ -1078,29 +1118,29 @@ class Engine {
   }
 
   PDG_HD bool itl_has_slack(int d, double thr) {
-    DecodeW& w = SM.dw[d];
-    const size_t base = static_cast<size_t>(d) * C.iwcap;
-    const uint32_t mask = static_cast<uint32_t>(C.iwcap - 1);
-    window_trim(w.iw, G.iw_t + base, mask);
+    DecodeW& w = s_->SM.dw[d];
+    const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
+    const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
+    window_trim(w.iw, s_->G.iw_t + base, mask);
     const uint32_t head = w.iw.head, end = w.iw.end;
     if (head == end) return 0.0 <= thr;
-    const Pfx hp = G.iw_p[base + (head & mask)];
+    const Pfx hp = s_->G.iw_p[base + (head & mask)];
     const int dec = window_mean_le(w.iw.tail, hp, thr);
     if (dec >= 0) return dec == 1;
-    ++folds_;
+    ++s_->folds_;
     double sum = 0.0;
-    for (uint32_t k = head; k != end; ++k) sum = fold_repeat(sum, G.iw_g[base + (k & mask)], G.iw_c[base + (k & mask)]);
+    for (uint32_t k = head; k != end; ++k) sum = fold_repeat(sum, s_->G.iw_g[base + (k & mask)], s_->G.iw_c[base + (k & mask)]);
     return ddiv(sum, static_cast<double>(w.iw.tail.terms - hp.terms)) <= thr;
   }
 
   // ---- queues + reorder (reorder.cpp:76-146; select_next sim_engine.cpp:335-350) ----
   PDG_HD bool queue_push(TaskQueue& q, int32_t* qs, double* qc, int32_t i, double cost) {
     const uint32_t qh = q.qh, qt = q.qt;
-    if (qt - qh >= static_cast<uint32_t>(C.qcap)) {
+    if (qt - qh >= static_cast<uint32_t>(s_->C.qcap)) {
       fail();
       return false;
     }
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     ExactSum ns = q.sum;
     ns.add(cost);
     warp_sync();
@@ -1116,25 +1156,25 @@ class Engine {
 
   // Dequeues the next task (after reordering the head window).
   PDG_HD int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     const uint32_t qh = q.qh;
-    if (PR.reorder) {
+    if (s_->PR.reorder) {
       const uint32_t len = q.qt - qh;
-      const int m = static_cast<int>(len < static_cast<uint32_t>(PR.window) ? len : static_cast<uint32_t>(PR.window));
+      const int m = static_cast<int>(len < static_cast<uint32_t>(s_->PR.window) ? len : static_cast<uint32_t>(s_->PR.window));
       if (m > 1) reorder_head(qs, qc, qh, m);
     }
     const int32_t i = qs[qh & mask];
     *cost = qc[qh & mask];
     ExactSum ns = q.sum;
     ns.remove(*cost);
-    const int32_t pc = G.sess[i].postpone;
+    const int32_t pc = s_->G.sess[i].postpone;
     warp_sync();
     if (lane_id() == 0) {
       q.sum = ns;
       q.qh = qh + 1;
     }
     warp_sync();
-    if (pc > ctr_.max_postpone_observed) ctr_.max_postpone_observed = pc;
+    if (pc > s_->ctr_.max_postpone_observed) s_->ctr_.max_postpone_observed = pc;
     return i;
   }
 
@@ -1143,19 +1183,19 @@ class Engine {
   // lexicographically first permutation with the maximum count among the
   // allowed ones (the identity is always allowed); capped tasks cannot be
   // pushed back (reorder.cpp:93-138). Lanes evaluate permutations in parallel.
-  PDG_HD void reorder_head(int32_t* qs, double* qc, uint32_t qh, int m) {
-    const uint32_t mask = static_cast<uint32_t>(C.qcap - 1);
+  PDG_COLD void reorder_head(int32_t* qs, double* qc, uint32_t qh, int m) {
+    const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     int32_t hs[8];
     double hc[8], wait[8];
     int pc[8];
     for (int k = 0; k < m; ++k) {
       hs[k] = qs[(qh + k) & mask];
       hc[k] = qc[(qh + k) & mask];
-      const SessRt& s = G.sess[hs[k]];
-      wait[k] = dsub(now_, s.t_enq);
+      const SessRt& s = s_->G.sess[hs[k]];
+      wait[k] = dsub(s_->now_, s.t_enq);
       pc[k] = s.postpone;
     }
-    const double thres = T.ttft_thres;
+    const double thres = s_->T.ttft_thres;
     int perm[8];
     for (int k = 0; k < m; ++k) perm[k] = k;
     const int id_sat = count_satisfied(perm, m, hc, wait, thres);
@@ -1168,7 +1208,7 @@ class Engine {
       unrank_perm(r, m, perm);
       bool allowed = true;
       for (int k = 0; k < m; ++k) {
-        if (k > perm[k] && pc[perm[k]] >= PR.window) {
+        if (k > perm[k] && pc[perm[k]] >= s_->PR.window) {
           allowed = false;
           break;
         }
@@ -1194,7 +1234,7 @@ class Engine {
     if (lane_id() == 0) {
       for (int k = 0; k < m; ++k) {
         const int p = perm[k];
-        if (k > p) ++G.sess[hs[p]].postpone;
+        if (k > p) ++s_->G.sess[hs[p]].postpone;
         qs[(qh + k) & mask] = hs[p];
         qc[(qh + k) & mask] = hc[p];
       }
@@ -1213,27 +1253,27 @@ class Engine {
   }
 
   // ---- prefill workers (sim_engine.cpp:354-453) ----
-  PDG_HD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
-    PrefillW& w = SM.pw[p];
+  PDG_COLD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
+    PrefillW& w = s_->SM.pw[p];
     const double cost = t_prefill(ctx, incr, w.deg);
-    if (!queue_push(w.q, G.pq_s + static_cast<size_t>(p) * C.qcap, G.pq_c + static_cast<size_t>(p) * C.qcap, i, cost))
+    if (!queue_push(w.q, s_->G.pq_s + static_cast<size_t>(p) * s_->C.qcap, s_->G.pq_c + static_cast<size_t>(p) * s_->C.qcap, i, cost))
       return;
     try_stage(p);
     try_start_compute(p);
   }
 
-  PDG_HD void try_stage(int p) {
-    PrefillW& w = SM.pw[p];
+  PDG_COLD void try_stage(int p) {
+    PrefillW& w = s_->SM.pw[p];
     if (w.staged || w.q.qh == w.q.qt) return;
     double cost;
-    const int32_t stg = select_next(w.q, G.pq_s + static_cast<size_t>(p) * C.qcap,
-                                    G.pq_c + static_cast<size_t>(p) * C.qcap, &cost);
-    const int32_t hist = G.sess[stg].ctx;
-    double ready = now_;
+    const int32_t stg = select_next(w.q, s_->G.pq_s + static_cast<size_t>(p) * s_->C.qcap,
+                                    s_->G.pq_c + static_cast<size_t>(p) * s_->C.qcap, &cost);
+    const int32_t hist = s_->G.sess[stg].ctx;
+    double ready = s_->now_;
     if (hist > 0) {
       // Lazy history read from the bound decode worker (sim_engine.cpp:368-383).
-      const int dd = SM.dw[G.sess[stg].bound].deg;
-      ready = dadd(now_, t_kv(hist, dd, w.deg));
+      const int dd = s_->SM.dw[s_->G.sess[stg].bound].deg;
+      ready = dadd(s_->now_, t_kv(hist, dd, w.deg));
     }
     warp_sync();
     if (lane_id() == 0) {
@@ -1248,9 +1288,9 @@ class Engine {
   }
 
   PDG_HD void try_start_compute(int p) {
-    PrefillW& w = SM.pw[p];
-    if (w.computing || !w.staged || w.pending || w.staged_ready > now_) return;
-    const double done = dadd(now_, w.stg_cost);
+    PrefillW& w = s_->SM.pw[p];
+    if (w.computing || !w.staged || w.pending || w.staged_ready > s_->now_) return;
+    const double done = dadd(s_->now_, w.stg_cost);
     warp_sync();
     if (lane_id() == 0) {
       w.cur = w.stg;
@@ -1263,14 +1303,14 @@ class Engine {
     try_stage(p);  // the next task's history read overlaps this compute
   }
 
-  PDG_HD void on_prefill_done(int p) {
-    PrefillW& w = SM.pw[p];
+  PDG_COLD void on_prefill_done(int p) {
+    PrefillW& w = s_->SM.pw[p];
     const int32_t i = w.cur;
     warp_sync();
     if (lane_id() == 0) w.computing = 0;
     warp_sync();
-    const int dd = SM.dw[G.sess[i].bound].deg;
-    heap_push(dadd(now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
+    const int dd = s_->SM.dw[s_->G.sess[i].bound].deg;
+    heap_push(dadd(s_->now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
               static_cast<uint32_t>(p));
     try_stage(p);
     try_start_compute(p);
@@ -1278,74 +1318,74 @@ class Engine {
 
   PDG_HD void on_history_read(int p) {
     warp_sync();
-    if (lane_id() == 0) SM.pw[p].pending = 0;
+    if (lane_id() == 0) s_->SM.pw[p].pending = 0;
     warp_sync();
     try_start_compute(p);
   }
 
   PDG_HD void on_writeback(int32_t i, int p) {
-    const int d = G.sess[i].bound;
+    const int d = s_->G.sess[i].bound;
     complete_task(i, false, p, d);
     advance_decode(d);
   }
 
   // complete_task (sim_engine.cpp:458-484).
-  PDG_HD void complete_task(int32_t i, bool local, int p, int d) {
-    SessRt& s = G.sess[i];
+  PDG_COLD void complete_task(int32_t i, bool local, int p, int d) {
+    SessRt& s = s_->G.sess[i];
     const int round = s.round;
-    const double created = round == 1 ? T.arrival[i] : s.t_enq;
-    const double value = dsub(now_, created);
+    const double created = round == 1 ? s_->T.arrival[i] : s.t_enq;
+    const double value = dsub(s_->now_, created);
     if (!local) ttft_add(p, value);  // decode workers' TTFT windows are never queried
-    if (REC.ttft && lane_id() == 0) {
-      pdsim_ttft_sample& o = REC.ttft[n_ttft_];
-      o.session_id = T.sid[i];
+    if (s_->REC.ttft && lane_id() == 0) {
+      pdsim_ttft_sample& o = s_->REC.ttft[s_->n_ttft_];
+      o.session_id = s_->T.sid[i];
       o.round = round;
       o.kind = round == 1 ? 0 : 1;
       o.local = local ? 1 : 0;
       o.reserved[0] = o.reserved[1] = 0;
       o.created_time = created;
-      o.completion_time = now_;
+      o.completion_time = s_->now_;
       o.value = value;
     }
-    ++n_ttft_;
-    const int32_t ridx = T.round_off[i] + round - 1;
-    const int32_t incr = T.incr[ridx];
-    const int32_t dec = T.dec[ridx];
-    DecodeW& w = SM.dw[d];
+    ++s_->n_ttft_;
+    const int32_t ridx = s_->T.round_off[i] + round - 1;
+    const int32_t incr = s_->T.incr[ridx];
+    const int32_t dec = s_->T.dec[ridx];
+    DecodeW& w = s_->SM.dw[d];
     const int32_t join = w.steps;  // first token in the next step started
     const uint64_t key =
-        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(T.rank[i]);
+        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(s_->T.rank[i]);
     warp_sync();
     if (lane_id() == 0) {
-      if (value > T.ttft_thres) s.ttft_bad = 1;
+      if (value > s_->T.ttft_thres) s.ttft_bad = 1;
       s.ctx += incr;
       s.join = join;
-      w.kv_used += static_cast<int64_t>(incr) * PF.kv_bytes_per_token;
+      w.kv_used += static_cast<int64_t>(incr) * PDG_PROF.kv_bytes_per_token;
       ++w.batch_n;
       ++w.n_new;
     }
     warp_sync();
     fh_push(d, key);
-    ++ctr_.tasks_completed;
+    ++s_->ctr_.tasks_completed;
   }
 
   // ---- decode workers (sim_engine.cpp:488-583) ----
   PDG_HD void enqueue_local(int d, int32_t i, int32_t ctx, int32_t incr) {
-    DecodeW& w = SM.dw[d];
+    DecodeW& w = s_->SM.dw[d];
     const double cost = t_prefill(ctx, incr, w.deg);
-    if (!queue_push(w.q, G.dq_s + static_cast<size_t>(d) * C.qcap, G.dq_c + static_cast<size_t>(d) * C.qcap, i, cost))
+    if (!queue_push(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap, s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, i, cost))
       return;
     advance_decode(d);
   }
 
   PDG_HD void advance_decode(int d) {
-    DecodeW& w = SM.dw[d];
+    DecodeW& w = s_->SM.dw[d];
     if (w.stepping || w.prefilling) return;
     if (w.q.qh != w.q.qt) {
       // Local prefill preempts decoding until the queue drains.
       double cost;
-      const int32_t cur = select_next(w.q, G.dq_s + static_cast<size_t>(d) * C.qcap,
-                                      G.dq_c + static_cast<size_t>(d) * C.qcap, &cost);
+      const int32_t cur = select_next(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap,
+                                      s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, &cost);
       warp_sync();
       if (lane_id() == 0) {
         w.cur = cur;
@@ -1353,13 +1393,13 @@ class Engine {
         w.prefilling = 1;
       }
       warp_sync();
-      set_slot(d, dadd(now_, cost), kPrefillDone);
+      set_slot(d, dadd(s_->now_, cost), kPrefillDone);
       return;
     }
     const int32_t batch = w.batch_n;
     if (batch > 0) {
       double dur = w.dur;
-      if (w.dur_cohort != batch) dur = curve_eval(PF.decode[w.deg], static_cast<double>(batch));
+      if (w.dur_cohort != batch) dur = curve_eval(PDG_PROF.decode[w.deg], static_cast<double>(batch));
       const int32_t first = w.n_new;
       warp_sync();
       if (lane_id() == 0) {
@@ -1372,12 +1412,12 @@ class Engine {
         w.stepping = 1;
       }
       warp_sync();
-      set_slot(d, dadd(now_, dur), kDecodeStep);
+      set_slot(d, dadd(s_->now_, dur), kDecodeStep);
     }
   }
 
   PDG_HD void on_local_prefill_done(int d) {
-    DecodeW& w = SM.dw[d];
+    DecodeW& w = s_->SM.dw[d];
     const int32_t i = w.cur;
     warp_sync();
     if (lane_id() == 0) w.prefilling = 0;
@@ -1387,42 +1427,42 @@ class Engine {
   }
 
   PDG_HD void on_decode_step(int d) {
-    DecodeW& w = SM.dw[d];
+    DecodeW& w = s_->SM.dw[d];
     const int32_t k = w.steps - 1;  // index of the step that just ended
     const int32_t cohort = w.cohort_n;
     const int32_t n_itl = cohort - w.first_n;
     const double prev = w.last_step_t;
-    const uint32_t lmask = static_cast<uint32_t>(C.lcap - 1);
-    double* slog = G.slog + static_cast<size_t>(d) * C.lcap;
+    const uint32_t lmask = static_cast<uint32_t>(s_->C.lcap - 1);
+    double* slog = s_->G.slog + static_cast<size_t>(d) * s_->C.lcap;
     warp_sync();
     if (lane_id() == 0) {
-      slog[static_cast<uint32_t>(k) & lmask] = now_;
+      slog[static_cast<uint32_t>(k) & lmask] = s_->now_;
       w.stepping = 0;
-      w.last_step_t = now_;
-      w.kv_used += static_cast<int64_t>(cohort) * PF.kv_bytes_per_token;
+      w.last_step_t = s_->now_;
+      w.kv_used += static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
     }
     warp_sync();
-    if (n_itl > 0) itl_add(d, dsub(now_, prev), static_cast<uint32_t>(n_itl));
-    ctr_.tokens_decoded += cohort;
+    if (n_itl > 0) itl_add(d, dsub(s_->now_, prev), static_cast<uint32_t>(n_itl));
+    s_->ctr_.tokens_decoded += cohort;
 
     bool any_terminated = false;
-    while (!failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
+    while (!s_->failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
       if (static_cast<int32_t>(w.fh_top >> 32) < k) {  // a round end was missed
         fail();
         return;
       }
       const uint32_t rank = static_cast<uint32_t>(w.fh_top);
       fh_pop(d);
-      const int32_t i = T.by_rank[rank];
-      SessRt& s = G.sess[i];
-      const int32_t ridx = T.round_off[i] + s.round - 1;
-      const int32_t dec = T.dec[ridx];
+      const int32_t i = s_->T.by_rank[rank];
+      SessRt& s = s_->G.sess[i];
+      const int32_t ridx = s_->T.round_off[i] + s.round - 1;
+      const int32_t dec = s_->T.dec[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
       for (int32_t j = s.join + 1; j <= k; ++j) {
         sum = dadd(sum, dsub(slog[static_cast<uint32_t>(j) & lmask], slog[static_cast<uint32_t>(j - 1) & lmask]));
       }
-      const bool last = s.round == T.round_off[i + 1] - T.round_off[i];
+      const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
       warp_sync();
       if (lane_id() == 0) {
         s.itl_sum = sum;
@@ -1435,7 +1475,7 @@ class Engine {
         terminate_session(i, d);
         any_terminated = true;
       } else {
-        heap_push(dadd(now_, T.delay[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
+        heap_push(dadd(s_->now_, s_->T.delay[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
       }
     }
     if (any_terminated) admit_waiting();
@@ -1443,7 +1483,7 @@ class Engine {
   }
 
   PDG_HD void on_interaction_done(int32_t i) {
-    SessRt& s = G.sess[i];
+    SessRt& s = s_->G.sess[i];
     const int round = s.round + 1;
     const int bound = s.bound;
     const int32_t ctx = s.ctx;
@@ -1454,25 +1494,25 @@ class Engine {
   }
 
   // terminate_session + slo_verdict (sim_engine.cpp:591-607, 668-674).
-  PDG_HD void terminate_session(int32_t i, int d) {
-    SessRt& s = G.sess[i];
+  PDG_COLD void terminate_session(int32_t i, int d) {
+    SessRt& s = s_->G.sess[i];
     const int32_t ctx = s.ctx;
     const int32_t cnt = s.itl_cnt;
     const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
     const bool ttft_ok = !s.ttft_bad;
-    const bool itl_ok = cnt == 0 || mean_itl <= T.itl_thres;
+    const bool itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
     const bool slo_ok = ttft_ok && itl_ok;
     warp_sync();
     if (lane_id() == 0) {
-      SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PF.kv_bytes_per_token;
-      if (REC.sessions) {
-        pdsim_session_outcome& o = REC.sessions[att_.sessions_completed];
-        o.session_id = T.sid[i];
-        o.arrival_time = T.arrival[i];
-        o.completion_time = now_;
-        o.admission_wait = dsub(s.bind_time, T.arrival[i]);
+      s_->SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
+      if (s_->REC.sessions) {
+        pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
+        o.session_id = s_->T.sid[i];
+        o.arrival_time = s_->T.arrival[i];
+        o.completion_time = s_->now_;
+        o.admission_wait = dsub(s.bind_time, s_->T.arrival[i]);
         o.mean_itl = mean_itl;
-        o.rounds = T.round_off[i + 1] - T.round_off[i];
+        o.rounds = s_->T.round_off[i + 1] - s_->T.round_off[i];
         o.ttft_ok = ttft_ok;
         o.itl_ok = itl_ok;
         o.slo_ok = slo_ok;
@@ -1480,21 +1520,21 @@ class Engine {
       }
     }
     warp_sync();
-    ++att_.sessions_completed;
-    att_.slo_ok += slo_ok;
-    att_.ttft_ok += ttft_ok;
-    att_.itl_ok += itl_ok;
+    ++s_->att_.sessions_completed;
+    s_->att_.slo_ok += slo_ok;
+    s_->att_.ttft_ok += ttft_ok;
+    s_->att_.itl_ok += itl_ok;
   }
 
   // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
-  PDG_HD void fh_push(int d, uint64_t key) {
-    DecodeW& w = SM.dw[d];
+  PDG_COLD void fh_push(int d, uint64_t key) {
+    DecodeW& w = s_->SM.dw[d];
     const int32_t n = w.fh_n;
-    if (n >= C.fcap) {
+    if (n >= s_->C.fcap) {
       fail();
       return;
     }
-    uint64_t* h = G.fh + static_cast<size_t>(d) * C.fcap;
+    uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
     const uint64_t top = w.fh_top;
     warp_sync();
     if (lane_id() == 0) {
@@ -1513,9 +1553,9 @@ class Engine {
     warp_sync();
   }
 
-  PDG_HD void fh_pop(int d) {
-    DecodeW& w = SM.dw[d];
-    uint64_t* h = G.fh + static_cast<size_t>(d) * C.fcap;
+  PDG_COLD void fh_pop(int d) {
+    DecodeW& w = s_->SM.dw[d];
+    uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
     warp_sync();
     if (lane_id() == 0) {
       const int32_t n = w.fh_n - 1;

@@ -71,7 +71,8 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   dt.by_rank = t.by_rank.data();
   const pdg::DevParams dprm = pdg::to_dev_params(*params);
   pdg::Records rec{out->decisions, out->ttft_samples, out->sessions};
-  pdg::Engine eng(dt, dp, *prof, dprm, caps, sslot, gslot, rec, seed);
+  pdg::host_profile() = prof;
+  pdg::Engine eng(sslot.es, dt, dp, dprm, caps, sslot, gslot, rec, seed);
   pdg::PairResult res;
   std::memset(&res, 0, sizeof(res));
   eng.run(&res);
