@@ -242,6 +242,11 @@ struct DecodeW {  // shared memory
   int32_t steps;  // steps started
   int32_t fh_n;   // finisher-heap size
   int8_t stepping, prefilling, reserved[2];
+  // cached fixed-point image of the last ITL run (gap, count)
+  ufx_t c_prod;
+  double c_gap;
+  uint32_t c_cnt;
+  int32_t c_inex;
 };
 
 // Capacities (host-computed provable upper bounds, see pack.hpp).
@@ -456,25 +461,11 @@ class Engine {
     const int D = s_->PL.D, P = s_->PL.P;
     const int nslots = s_->nslots_;
     while (!s_->failed_) {
+      warp_sync();  // re-converge once per event (handlers store uniform values)
       // Next worker event: min over the slot table (lanes split the slots).
-      double bt = kInf;
-      uint64_t bk = ~0ull;
-      for (int j = lane_id(); j < nslots; j += PDG_NL) {
-        const double t = s_->st_[j];
-        const uint64_t k = s_->sk_[j];
-        if (before(t, k, bt, bk)) {
-          bt = t;
-          bk = k;
-        }
-      }
-      for (int m = PDG_NL / 2; m > 0; m >>= 1) {
-        const double ot = bitsd(shfl_xor_u64(dbits(bt), m));
-        const uint64_t ok = shfl_xor_u64(bk, m);
-        if (before(ot, ok, bt, bk)) {
-          bt = ot;
-          bk = ok;
-        }
-      }
+      double bt;
+      uint64_t bk;
+      next_slot_event(nslots, &bt, &bk);
       int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
       if (s_->hn_ > 0) {
         const HEv* h = heap_base();
@@ -605,6 +596,10 @@ class Engine {
         w.steps = 0;
         w.fh_n = 0;
         w.stepping = w.prefilling = 0;
+        w.c_prod = 0;
+        w.c_gap = 0.0;
+        w.c_cnt = 0;
+        w.c_inex = 0;
       }
     }
     s_->mt_idx_ = Mt64::kN;
@@ -673,6 +668,57 @@ class Engine {
   }
 
   // ---- worker-event slots (registers) ----
+  // Minimum (time, key) over the slot table. Times are >= 0 (or +inf), so
+  // their bit patterns order like unsigned integers: two warp REDUX.MIN on
+  // the 32-bit halves find the earliest time; equal times (rare) are broken
+  // by the key the same way.
+  PDG_HD void next_slot_event(int nslots, double* bt_out, uint64_t* bk_out) const {
+#if defined(__CUDA_ARCH__)
+    const int lane = lane_id();
+    uint64_t tb = 0x7ff0000000000000ull;  // +inf
+    uint64_t kb = ~0ull;
+    if (lane < nslots) {
+      tb = dbits(s_->st_[lane]);
+      kb = s_->sk_[lane];
+    }
+    if (lane + 32 < nslots) {
+      const uint64_t t2 = dbits(s_->st_[lane + 32]);
+      const uint64_t k2 = s_->sk_[lane + 32];
+      if (t2 < tb || (t2 == tb && k2 < kb)) {
+        tb = t2;
+        kb = k2;
+      }
+    }
+    const uint32_t hi = static_cast<uint32_t>(tb >> 32);
+    const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t lo = hi == mhi ? static_cast<uint32_t>(tb) : 0xffffffffu;
+    const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
+    const bool at = hi == mhi && static_cast<uint32_t>(tb) == mlo;
+    uint32_t b = __ballot_sync(0xffffffffu, at);
+    if (__popc(b) > 1) {  // several slots share the earliest time: smallest key
+      const uint32_t khi = at ? static_cast<uint32_t>(kb >> 32) : 0xffffffffu;
+      const uint32_t mkhi = __reduce_min_sync(0xffffffffu, khi);
+      const uint32_t klo = (at && khi == mkhi) ? static_cast<uint32_t>(kb) : 0xffffffffu;
+      const uint32_t mklo = __reduce_min_sync(0xffffffffu, klo);
+      b = __ballot_sync(0xffffffffu, at && khi == mkhi && static_cast<uint32_t>(kb) == mklo);
+    }
+    const int src = __ffs(b) - 1;
+    *bt_out = bitsd((static_cast<uint64_t>(mhi) << 32) | mlo);
+    *bk_out = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(kb), src);
+#else
+    double bt = kInf;
+    uint64_t bk = ~0ull;
+    for (int j = 0; j < nslots; ++j) {
+      if (before(s_->st_[j], s_->sk_[j], bt, bk)) {
+        bt = s_->st_[j];
+        bk = s_->sk_[j];
+      }
+    }
+    *bt_out = bt;
+    *bk_out = bk;
+#endif
+  }
+
   PDG_HD void set_slot(int s, double t, uint32_t kind) {
     const uint64_t seq = s_->seq_;
     const uint64_t key = mk_key(kind, seq, static_cast<uint32_t>(s));
@@ -1103,18 +1149,32 @@ class Engine {
     if (!window_room(w.iw, s_->G.iw_t + base, static_cast<uint32_t>(s_->C.iwcap))) return;
     const uint32_t k = w.iw.end & mask;
     const Pfx cur = w.iw.tail;
-    Pfx next = cur;
-    next.add(gap, count);
-    warp_sync();
-    if (lane_id() == 0) {
-      s_->G.iw_t[base + k] = s_->now_;
-      s_->G.iw_g[base + k] = gap;
-      s_->G.iw_c[base + k] = count;
-      s_->G.iw_p[base + k] = cur;
-      w.iw.tail = next;
-      ++w.iw.end;
+    // Consecutive steps of a stable batch repeat (gap, count): reuse the
+    // fixed-point product.
+    ufx_t prod;
+    int32_t inex;
+    if (gap == w.c_gap && count == w.c_cnt) {
+      prod = w.c_prod;
+      inex = w.c_inex;
+    } else {
+      fx_t f;
+      inex = to_fx(gap, &f) ? 0 : 1;
+      prod = static_cast<ufx_t>(f) * static_cast<ufx_t>(count);
+      w.c_gap = gap;
+      w.c_cnt = count;
+      w.c_prod = prod;
+      w.c_inex = inex;
     }
-    warp_sync();
+    // Warp-uniform values: every lane stores the same bytes.
+    s_->G.iw_t[base + k] = s_->now_;
+    s_->G.iw_g[base + k] = gap;
+    s_->G.iw_c[base + k] = count;
+    s_->G.iw_p[base + k] = cur;
+    const uint32_t end = w.iw.end;
+    w.iw.tail.sum = cur.sum + prod;
+    w.iw.tail.terms = cur.terms + count;
+    w.iw.tail.inexact = cur.inexact + inex;
+    w.iw.end = end + 1;
   }
 
   PDG_HD bool itl_has_slack(int d, double thr) {
@@ -1401,17 +1461,15 @@ class Engine {
       double dur = w.dur;
       if (w.dur_cohort != batch) dur = curve_eval(PDG_PROF.decode[w.deg], static_cast<double>(batch));
       const int32_t first = w.n_new;
-      warp_sync();
-      if (lane_id() == 0) {
-        w.dur = dur;
-        w.dur_cohort = batch;
-        w.cohort_n = batch;
-        w.first_n = first;
-        w.n_new = 0;
-        ++w.steps;
-        w.stepping = 1;
-      }
-      warp_sync();
+      const int32_t steps = w.steps;
+      // warp-uniform stores (every lane writes the same values)
+      w.dur = dur;
+      w.dur_cohort = batch;
+      w.cohort_n = batch;
+      w.first_n = first;
+      w.n_new = 0;
+      w.steps = steps + 1;
+      w.stepping = 1;
       set_slot(d, dadd(s_->now_, dur), kDecodeStep);
     }
   }
@@ -1434,16 +1492,16 @@ class Engine {
     const double prev = w.last_step_t;
     const uint32_t lmask = static_cast<uint32_t>(s_->C.lcap - 1);
     double* slog = s_->G.slog + static_cast<size_t>(d) * s_->C.lcap;
-    warp_sync();
-    if (lane_id() == 0) {
-      slog[static_cast<uint32_t>(k) & lmask] = s_->now_;
-      w.stepping = 0;
-      w.last_step_t = s_->now_;
-      w.kv_used += static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
-    }
-    warp_sync();
-    if (n_itl > 0) itl_add(d, dsub(s_->now_, prev), static_cast<uint32_t>(n_itl));
-    s_->ctr_.tokens_decoded += cohort;
+    const double now = s_->now_;
+    const int64_t kv = w.kv_used;
+    const int64_t tokens = s_->ctr_.tokens_decoded;
+    // warp-uniform stores
+    slog[static_cast<uint32_t>(k) & lmask] = now;
+    w.stepping = 0;
+    w.last_step_t = now;
+    w.kv_used = kv + static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
+    s_->ctr_.tokens_decoded = tokens + cohort;
+    if (n_itl > 0) itl_add(d, dsub(now, prev), static_cast<uint32_t>(n_itl));
 
     bool any_terminated = false;
     while (!s_->failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
