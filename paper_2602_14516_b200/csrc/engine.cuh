@@ -234,6 +234,9 @@ struct DecodeW {  // shared memory
   uint64_t fh_top;     // cached finisher-heap minimum (valid when fh_n > 0)
   double cur_cost;
   double last_step_t;  // end time of the previous step
+  double cur_end;      // end time of the step in flight (valid while stepping)
+  int32_t run_b;       // lazy mode: the in-flight run's next explicit step index
+  int32_t run_pad;
   double dur;          // cached t_decode(dur_cohort)
   int32_t dur_cohort;
   int32_t deg;
@@ -414,6 +417,8 @@ struct EngState {
   uint32_t mt_idx_;
   int32_t failed_;
   int32_t nslots_;
+  int32_t lazy_;   // lazy decode stepping enabled for this attempt
+  int32_t abort_;  // lazy attempt hit an ambiguous tie: replay exactly
   pdsim_attainment att_;
   pdsim_counters ctr_;
   int64_t n_dec_;
@@ -457,15 +462,28 @@ class Engine {
   }
 
   PDG_HD void run(PairResult* out) {
-    init();
+    // Lazy decode stepping first; an ambiguous equal-time ordering between a
+    // lazily advanced decode step and another decode step aborts the attempt,
+    // and the pair is replayed with every step as an explicit event.
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      init();
+      s_->lazy_ = attempt == 0 ? 1 : 0;
+      event_loop();
+      if (!s_->abort_) break;
+    }
+    finish_result(out);
+  }
+
+  PDG_HD void event_loop() {
     const int D = s_->PL.D, P = s_->PL.P;
     const int nslots = s_->nslots_;
-    while (!s_->failed_) {
+    while (!s_->failed_ && !s_->abort_) {
       warp_sync();  // re-converge once per event (handlers store uniform values)
       // Next worker event: min over the slot table (lanes split the slots).
       double bt;
       uint64_t bk;
-      next_slot_event(nslots, &bt, &bk);
+      bool slot_tie;
+      next_slot_event(nslots, &bt, &bk, &slot_tie);
       int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
       if (s_->hn_ > 0) {
         const HEv* h = heap_base();
@@ -480,18 +498,32 @@ class Engine {
       // Arrivals carry kind 0 and seq = index: they precede every dynamic
       // event at an equal time (sim_engine.cpp:137-143).
       if (s_->next_arr_ < s_->T.S && (src < 0 || s_->next_arr_t_ <= bt)) src = 2;
-      if (src < 0) break;
+      if (src < 0) {
+        if (s_->lazy_) catch_up(kInf, 0);  // drain silent steps (none remain)
+        break;
+      }
       if (src == 2) {
         const int32_t i = s_->next_arr_++;
         const double t = s_->next_arr_t_;
         if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = s_->T.arrival[s_->next_arr_];
+        if (s_->lazy_) catch_up(t, kArrival);
         advance_to(t);
         on_arrival(i);
         continue;
       }
+      const uint32_t kind = static_cast<uint32_t>(bk >> 58);
+      if (s_->lazy_) {
+        // Two decode-step events at the same time: their order is the
+        // scheduling order, which lazily materialised steps do not carry.
+        if (src == 0 && kind == kDecodeStep && slot_tie) {
+          s_->abort_ = 1;
+          return;
+        }
+        catch_up(bt, kind);
+        if (s_->abort_) return;
+      }
       ++s_->events_;
       advance_to(bt);
-      const uint32_t kind = static_cast<uint32_t>(bk >> 58);
       if (src == 1) {
         const HEv e = heap_pop();
         if (kind == kInteractionDone) {
@@ -515,6 +547,9 @@ class Engine {
         on_history_read(s - D - P);
       }
     }
+  }
+
+  PDG_HD void finish_result(PairResult* out) {
     for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += s_->SM.dw[d].kv_used;
     out->att = s_->att_;
     out->att.sessions_total = s_->T.S;
@@ -548,6 +583,7 @@ class Engine {
     s_->ctr_.events_in_order = 1;
     s_->nslots_ = s_->PL.D + 2 * s_->PL.P;
     s_->failed_ = 0;
+    s_->abort_ = 0;
     s_->heap_spilled_ = 0;
     s_->mt_idx_ = 0;
     s_->att_ = pdsim_attainment{};
@@ -596,6 +632,9 @@ class Engine {
         w.steps = 0;
         w.fh_n = 0;
         w.stepping = w.prefilling = 0;
+        w.cur_end = 0.0;
+        w.run_b = 0;
+        w.run_pad = 0;
         w.c_prod = 0;
         w.c_gap = 0.0;
         w.c_cnt = 0;
@@ -672,7 +711,7 @@ class Engine {
   // their bit patterns order like unsigned integers: two warp REDUX.MIN on
   // the 32-bit halves find the earliest time; equal times (rare) are broken
   // by the key the same way.
-  PDG_HD void next_slot_event(int nslots, double* bt_out, uint64_t* bk_out) const {
+  PDG_HD void next_slot_event(int nslots, double* bt_out, uint64_t* bk_out, bool* tie_out) const {
 #if defined(__CUDA_ARCH__)
     const int lane = lane_id();
     uint64_t tb = 0x7ff0000000000000ull;  // +inf
@@ -695,6 +734,7 @@ class Engine {
     const uint32_t mlo = __reduce_min_sync(0xffffffffu, lo);
     const bool at = hi == mhi && static_cast<uint32_t>(tb) == mlo;
     uint32_t b = __ballot_sync(0xffffffffu, at);
+    *tie_out = __popc(b) > 1 && mhi != 0x7ff00000u;
     if (__popc(b) > 1) {  // several slots share the earliest time: smallest key
       const uint32_t khi = at ? static_cast<uint32_t>(kb >> 32) : 0xffffffffu;
       const uint32_t mkhi = __reduce_min_sync(0xffffffffu, khi);
@@ -708,14 +748,18 @@ class Engine {
 #else
     double bt = kInf;
     uint64_t bk = ~0ull;
+    int ties = 0;
     for (int j = 0; j < nslots; ++j) {
+      if (s_->st_[j] == bt) ++ties;
       if (before(s_->st_[j], s_->sk_[j], bt, bk)) {
+        if (s_->st_[j] < bt) ties = 1;
         bt = s_->st_[j];
         bk = s_->sk_[j];
       }
     }
     *bt_out = bt;
     *bk_out = bk;
+    *tie_out = ties > 1 && bt != kInf;
 #endif
   }
 
@@ -1077,8 +1121,8 @@ class Engine {
   // ---- windowed statistics (coordinator.cpp:27-47) ----
   // Drops entries with time <= now - window from the head (times are
   // non-decreasing, so expired entries form a prefix): one ballot per 32.
-  PDG_HD void window_trim(WinState& w, const double* times, uint32_t mask) {
-    const double cutoff = dsub(s_->now_, s_->PR.stat_window);
+  PDG_HD void window_trim(WinState& w, const double* times, uint32_t mask, double now) {
+    const double cutoff = dsub(now, s_->PR.stat_window);
     uint32_t head = w.head;
     const uint32_t end = w.end;
     while (head != end) {
@@ -1094,9 +1138,9 @@ class Engine {
     warp_sync();
   }
 
-  PDG_HD bool window_room(WinState& w, const double* times, uint32_t cap) {
+  PDG_HD bool window_room(WinState& w, const double* times, uint32_t cap, double now) {
     if (w.end - w.head >= cap - 1) {
-      window_trim(w, times, cap - 1);
+      window_trim(w, times, cap - 1, now);
       if (w.end - w.head >= cap - 1) {
         fail();
         return false;
@@ -1109,7 +1153,7 @@ class Engine {
     PrefillW& w = s_->SM.pw[p];
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
-    if (!window_room(w.tw, s_->G.tw_t + base, static_cast<uint32_t>(s_->C.twcap))) return;
+    if (!window_room(w.tw, s_->G.tw_t + base, static_cast<uint32_t>(s_->C.twcap), s_->now_)) return;
     const uint32_t k = w.tw.end & mask;
     const Pfx cur = w.tw.tail;
     Pfx next = cur;
@@ -1130,7 +1174,7 @@ class Engine {
     PrefillW& w = s_->SM.pw[p];
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
-    window_trim(w.tw, s_->G.tw_t + base, mask);
+    window_trim(w.tw, s_->G.tw_t + base, mask, s_->now_);
     const uint32_t head = w.tw.head, end = w.tw.end;
     if (head == end) return 0.0 <= thr;  // an empty window reads 0
     const Pfx hp = s_->G.tw_p[base + (head & mask)];
@@ -1142,11 +1186,11 @@ class Engine {
     return ddiv(sum, static_cast<double>(end - head)) <= thr;
   }
 
-  PDG_HD void itl_add(int d, double gap, uint32_t count) {
+  PDG_HD void itl_add(int d, double t, double gap, uint32_t count) {
     DecodeW& w = s_->SM.dw[d];
     const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
-    if (!window_room(w.iw, s_->G.iw_t + base, static_cast<uint32_t>(s_->C.iwcap))) return;
+    if (!window_room(w.iw, s_->G.iw_t + base, static_cast<uint32_t>(s_->C.iwcap), t)) return;
     const uint32_t k = w.iw.end & mask;
     const Pfx cur = w.iw.tail;
     // Consecutive steps of a stable batch repeat (gap, count): reuse the
@@ -1166,7 +1210,7 @@ class Engine {
       w.c_inex = inex;
     }
     // Warp-uniform values: every lane stores the same bytes.
-    s_->G.iw_t[base + k] = s_->now_;
+    s_->G.iw_t[base + k] = t;
     s_->G.iw_g[base + k] = gap;
     s_->G.iw_c[base + k] = count;
     s_->G.iw_p[base + k] = cur;
@@ -1181,7 +1225,7 @@ class Engine {
     DecodeW& w = s_->SM.dw[d];
     const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
-    window_trim(w.iw, s_->G.iw_t + base, mask);
+    window_trim(w.iw, s_->G.iw_t + base, mask, s_->now_);
     const uint32_t head = w.iw.head, end = w.iw.end;
     if (head == end) return 0.0 <= thr;
     const Pfx hp = s_->G.iw_p[base + (head & mask)];
@@ -1412,6 +1456,7 @@ class Engine {
     const int32_t incr = s_->T.incr[ridx];
     const int32_t dec = s_->T.dec[ridx];
     DecodeW& w = s_->SM.dw[d];
+    interrupt_run(d);
     const int32_t join = w.steps;  // first token in the next step started
     const uint64_t key =
         (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(s_->T.rank[i]);
@@ -1435,6 +1480,7 @@ class Engine {
     const double cost = t_prefill(ctx, incr, w.deg);
     if (!queue_push(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap, s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, i, cost))
       return;
+    interrupt_run(d);
     advance_decode(d);
   }
 
@@ -1461,7 +1507,20 @@ class Engine {
       double dur = w.dur;
       if (w.dur_cohort != batch) dur = curve_eval(PDG_PROF.decode[w.deg], static_cast<double>(batch));
       const int32_t first = w.n_new;
-      const int32_t steps = w.steps;
+      const int32_t steps = w.steps;  // index of the step starting now
+      const double end = dadd(s_->now_, dur);
+      // Lazy mode: steps before the next round end of a batch member are
+      // "silent" (no state outside this worker changes) and are advanced by
+      // catch_up(); only the step where a member finishes is an event.
+      int32_t b = steps;
+      double b_end = end;
+      if (s_->lazy_ && w.fh_n > 0) {
+        const int32_t fin = static_cast<int32_t>(w.fh_top >> 32);
+        if (fin > steps) {
+          b = fin;
+          b_end = fold_repeat(end, dur, static_cast<uint64_t>(fin - steps));
+        }
+      }
       // warp-uniform stores (every lane writes the same values)
       w.dur = dur;
       w.dur_cohort = batch;
@@ -1470,8 +1529,91 @@ class Engine {
       w.n_new = 0;
       w.steps = steps + 1;
       w.stepping = 1;
-      set_slot(d, dadd(s_->now_, dur), kDecodeStep);
+      w.cur_end = end;
+      w.run_b = b;
+      set_slot(d, b_end, kDecodeStep);
     }
+  }
+
+  // ---- lazy decode stepping ----
+  // Advances every decode worker's silent steps that end strictly before the
+  // event about to run at time t. A silent step ending exactly at t comes
+  // after an event of kind < 4 (kinds order equal-time events), so it stays
+  // pending; against another decode step (kind 4) the order is the
+  // scheduling order, which lazy steps do not carry: abort to exact mode.
+  PDG_HD void catch_up(double t, uint32_t kind) {
+    const int D = s_->PL.D;
+    for (int base = 0; base < D; base += PDG_NL) {
+      // lanes test their workers in parallel; only flagged workers advance
+      const int mine = base + lane_id();
+      bool need = false;
+      if (mine < D) {
+        const DecodeW& w = s_->SM.dw[mine];
+        need = w.stepping && w.steps - 1 < w.run_b && w.cur_end <= t;
+      }
+      uint32_t m = ballot(need);
+      while (m) {
+        const int d = base + first_zero(~m);
+        m &= m - 1;
+        catch_up_worker(d, t, kind);
+        if (s_->failed_ || s_->abort_) return;
+      }
+    }
+  }
+
+  PDG_HD void catch_up_worker(int d, double t, uint32_t kind) {
+    {
+      DecodeW& w = s_->SM.dw[d];
+      while (w.stepping && w.steps - 1 < w.run_b) {
+        const double e = w.cur_end;
+        if (e > t) break;
+        if (e == t) {
+          if (kind == kDecodeStep) s_->abort_ = 1;
+          break;
+        }
+        silent_step(d, e);
+        if (s_->failed_ || s_->abort_) return;
+      }
+    }
+  }
+
+  // End of a silent step (no member finishes its round in it) at time e: the
+  // effects of on_decode_step without finishers, then the next step of the
+  // same cohort starts at once (sim_engine.cpp:530-583, 513-527).
+  PDG_HD void silent_step(int d, double e) {
+    DecodeW& w = s_->SM.dw[d];
+    const int32_t k = w.steps - 1;
+    const int32_t cohort = w.cohort_n;
+    const int32_t n_itl = cohort - w.first_n;
+    const double prev = w.last_step_t;
+    const int64_t kv = w.kv_used;
+    const int64_t tokens = s_->ctr_.tokens_decoded;
+    const double next = dadd(e, w.dur);
+    const uint32_t lmask = static_cast<uint32_t>(s_->C.lcap - 1);
+    s_->G.slog[static_cast<size_t>(d) * s_->C.lcap + (static_cast<uint32_t>(k) & lmask)] = e;
+    w.last_step_t = e;
+    w.kv_used = kv + static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
+    s_->ctr_.tokens_decoded = tokens + cohort;
+    if (n_itl > 0) itl_add(d, e, dsub(e, prev), static_cast<uint32_t>(n_itl));
+    if (!(next > e)) {  // a zero-length step cannot be advanced lazily
+      s_->abort_ = 1;
+      return;
+    }
+    w.first_n = 0;  // no joins inside a run (a join ends the run)
+    w.steps = k + 2;
+    w.cur_end = next;
+  }
+
+  // A join or a local prefill on a worker whose in-flight step is silent:
+  // that step's end becomes an explicit event (its successor differs).
+  PDG_HD void interrupt_run(int d) {
+    DecodeW& w = s_->SM.dw[d];
+    if (!s_->lazy_ || !w.stepping) return;
+    const int32_t k = w.steps - 1;
+    if (w.run_b <= k) return;
+    const double end = w.cur_end;
+    w.run_b = k;
+    set_slot(d, end, kDecodeStep);
   }
 
   PDG_HD void on_local_prefill_done(int d) {
@@ -1501,7 +1643,7 @@ class Engine {
     w.last_step_t = now;
     w.kv_used = kv + static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
     s_->ctr_.tokens_decoded = tokens + cohort;
-    if (n_itl > 0) itl_add(d, dsub(now, prev), static_cast<uint32_t>(n_itl));
+    if (n_itl > 0) itl_add(d, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
 
     bool any_terminated = false;
     while (!s_->failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
