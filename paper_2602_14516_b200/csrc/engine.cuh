@@ -36,6 +36,8 @@
 // the reference without a device.
 #pragma once
 
+#include <math.h>
+
 #include "common.cuh"
 #include "exactsum.cuh"
 #include "fold.cuh"
@@ -226,9 +228,23 @@ struct PrefillW {  // shared memory
   double staged_ready;
 };
 
+// A run of consecutive decode steps of one worker with the same ITL gap and
+// the same ITL sample count per step: step j (first <= j < first + n) ends
+// at t0 + (j - first) * gap exactly (each step adds exactly `gap`).
+struct Seg {
+  Pfx pfx;       // window prefix before this segment
+  double t0;     // end time of step `first`
+  double gap;    // every step's ITL gap (end - previous end)
+  int32_t first; // first step index
+  int32_t n;     // steps
+  uint32_t cnt;  // ITL samples per step (cohort members past their first token)
+  int32_t inex;  // gap has no exact fixed-point image (and cnt > 0)
+};
+
 struct DecodeW {  // shared memory
   TaskQueue q;  // local prefill queue
-  WinState iw;  // ITL window (runs)
+  Seg sg;       // the open (newest) segment of the step log
+  ufx_t sg_prod;       // fx(sg.gap) * sg.cnt
   int64_t kv_used;
   int64_t kv_cap;
   uint64_t fh_top;     // cached finisher-heap minimum (valid when fh_n > 0)
@@ -245,11 +261,13 @@ struct DecodeW {  // shared memory
   int32_t steps;  // steps started
   int32_t fh_n;   // finisher-heap size
   int8_t stepping, prefilling, reserved[2];
-  // cached fixed-point image of the last ITL run (gap, count)
-  ufx_t c_prod;
-  double c_gap;
-  uint32_t c_cnt;
-  int32_t c_inex;
+  // closed segments live in the global ring [seg_keep, seg_end); the open
+  // segment has index seg_end. ITL window head: segment seg_head with its
+  // first seg_off steps expired.
+  int32_t seg_end;
+  int32_t seg_keep;
+  int32_t seg_head;
+  int32_t seg_off;
 };
 
 // Capacities (host-computed provable upper bounds, see pack.hpp).
@@ -260,8 +278,8 @@ struct Caps {
   int32_t qcap;   // per-worker task queue (power of 2)
   int32_t fcap;   // per-decode-worker finisher heap
   int32_t twcap;  // TTFT window ring (power of 2)
-  int32_t iwcap;  // ITL-run ring (power of 2)
-  int32_t lcap;   // step-log ring (power of 2)
+  int32_t segcap;  // per-decode-worker step-segment ring (power of 2)
+  int32_t maxdec;  // longest decode round (steps a per-session fold may reach back)
   int32_t pmax;
   int32_t dmax;
 };
@@ -289,12 +307,8 @@ struct GlobalSlot {
   double* tw_t;
   double* tw_v;
   Pfx* tw_p;
-  double* iw_t;
-  double* iw_g;
-  uint32_t* iw_c;
-  Pfx* iw_p;
+  Seg* seg;  // [dmax][segcap]
   uint64_t* fh;
-  double* slog;
 };
 
 PDG_HD size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -338,12 +352,8 @@ PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
   t.tw_t = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
   t.tw_v = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
   t.tw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * P * static_cast<size_t>(c.twcap)));
-  t.iw_t = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.iwcap)));
-  t.iw_g = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.iwcap)));
-  t.iw_c = reinterpret_cast<uint32_t*>(take(4 * D * static_cast<size_t>(c.iwcap)));
-  t.iw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * D * static_cast<size_t>(c.iwcap)));
+  t.seg = reinterpret_cast<Seg*>(take(sizeof(Seg) * D * static_cast<size_t>(c.segcap)));
   t.fh = reinterpret_cast<uint64_t*>(take(8 * D * static_cast<size_t>(c.fcap)));
-  t.slog = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.lcap)));
   if (s) *s = t;
   return off;
 }
@@ -617,8 +627,15 @@ class Engine {
         DecodeW& w = s_->SM.dw[d];
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
-        w.iw.tail.clear();
-        w.iw.head = w.iw.end = 0;
+        w.sg.pfx.clear();
+        w.sg.t0 = 0.0;
+        w.sg.gap = 0.0;
+        w.sg.first = 0;
+        w.sg.n = 0;
+        w.sg.cnt = 0;
+        w.sg.inex = 0;
+        w.sg_prod = 0;
+        w.seg_end = w.seg_keep = w.seg_head = w.seg_off = 0;
         w.kv_used = 0;
         w.kv_cap = static_cast<int64_t>(PDG_PROF.degrees[s_->PL.ddeg[d]]) * PDG_PROF.gpu_memory_capacity;
         w.fh_top = 0;
@@ -635,10 +652,6 @@ class Engine {
         w.cur_end = 0.0;
         w.run_b = 0;
         w.run_pad = 0;
-        w.c_prod = 0;
-        w.c_gap = 0.0;
-        w.c_cnt = 0;
-        w.c_inex = 0;
       }
     }
     s_->mt_idx_ = Mt64::kN;
@@ -1186,55 +1199,171 @@ class Engine {
     return ddiv(sum, static_cast<double>(end - head)) <= thr;
   }
 
-  PDG_HD void itl_add(int d, double t, double gap, uint32_t count) {
-    DecodeW& w = s_->SM.dw[d];
-    const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
-    const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
-    if (!window_room(w.iw, s_->G.iw_t + base, static_cast<uint32_t>(s_->C.iwcap), t)) return;
-    const uint32_t k = w.iw.end & mask;
-    const Pfx cur = w.iw.tail;
-    // Consecutive steps of a stable batch repeat (gap, count): reuse the
-    // fixed-point product.
-    ufx_t prod;
-    int32_t inex;
-    if (gap == w.c_gap && count == w.c_cnt) {
-      prod = w.c_prod;
-      inex = w.c_inex;
-    } else {
-      fx_t f;
-      inex = to_fx(gap, &f) ? 0 : 1;
-      prod = static_cast<ufx_t>(f) * static_cast<ufx_t>(count);
-      w.c_gap = gap;
-      w.c_cnt = count;
-      w.c_prod = prod;
-      w.c_inex = inex;
-    }
-    // Warp-uniform values: every lane stores the same bytes.
-    s_->G.iw_t[base + k] = t;
-    s_->G.iw_g[base + k] = gap;
-    s_->G.iw_c[base + k] = count;
-    s_->G.iw_p[base + k] = cur;
-    const uint32_t end = w.iw.end;
-    w.iw.tail.sum = cur.sum + prod;
-    w.iw.tail.terms = cur.terms + count;
-    w.iw.tail.inexact = cur.inexact + inex;
-    w.iw.end = end + 1;
+  // ---- step-segment log: ITL window + per-session ITL folds ----
+  PDG_HD Seg* seg_ring(int d) const { return s_->G.seg + static_cast<size_t>(d) * s_->C.segcap; }
+  // Segment i of worker d (i == seg_end is the open one, in shared memory).
+  PDG_HD Seg seg_at(int d, int32_t i) const {
+    const DecodeW& w = s_->SM.dw[d];
+    if (i == w.seg_end) return w.sg;
+    return seg_ring(d)[static_cast<uint32_t>(i) & static_cast<uint32_t>(s_->C.segcap - 1)];
+  }
+  // Exact end time of step j of segment g (the progression is exact).
+  PDG_HD static double seg_time(const Seg& g, int32_t j) {
+    return dadd(g.t0, dmul(static_cast<double>(j - g.first), g.gap));
+  }
+  // Prefix after the open segment (the window's running total).
+  PDG_HD Pfx tail_pfx(const DecodeW& w) const {
+    Pfx t = w.sg.pfx;
+    t.sum += w.sg_prod * static_cast<ufx_t>(static_cast<uint32_t>(w.sg.n));
+    t.terms += static_cast<int64_t>(w.sg.cnt) * w.sg.n;
+    t.inexact += w.sg.n > 0 ? w.sg.inex : 0;
+    return t;
   }
 
-  PDG_HD bool itl_has_slack(int d, double thr) {
+  // Appends n consecutive steps (first index `first`, first end time t0,
+  // each with ITL gap `gap` and `cnt` ITL samples) to worker d's log.
+  PDG_HD void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
     DecodeW& w = s_->SM.dw[d];
-    const size_t base = static_cast<size_t>(d) * s_->C.iwcap;
-    const uint32_t mask = static_cast<uint32_t>(s_->C.iwcap - 1);
-    window_trim(w.iw, s_->G.iw_t + base, mask, s_->now_);
-    const uint32_t head = w.iw.head, end = w.iw.end;
-    if (head == end) return 0.0 <= thr;
-    const Pfx hp = s_->G.iw_p[base + (head & mask)];
-    const int dec = window_mean_le(w.iw.tail, hp, thr);
+    if (w.sg.n > 0 && gap == w.sg.gap && cnt == w.sg.cnt && first == w.sg.first + w.sg.n) {
+      w.sg.n = w.sg.n + n;  // extends the open segment (t0 continues the progression)
+      return;
+    }
+    if (w.sg.n > 0) {
+      // close the open segment into the ring
+      const int32_t end = w.seg_end;
+      if (end - w.seg_keep >= s_->C.segcap) {
+        seg_trim(d, t0);  // later queries are at >= t0
+        seg_reclaim(d, first);
+        if (end - w.seg_keep >= s_->C.segcap) {
+          fail();
+          return;
+        }
+      }
+      const Seg closed = w.sg;
+      const Pfx next_pfx = tail_pfx(w);
+      seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = closed;
+      w.seg_end = end + 1;
+      w.sg.pfx = next_pfx;
+    }
+    fx_t f;
+    const bool exact = to_fx(gap, &f);
+    w.sg.t0 = t0;
+    w.sg.gap = gap;
+    w.sg.first = first;
+    w.sg.n = n;
+    w.sg.cnt = cnt;
+    w.sg.inex = (cnt > 0 && !exact) ? 1 : 0;
+    w.sg_prod = cnt > 0 ? static_cast<ufx_t>(f) * static_cast<ufx_t>(cnt) : static_cast<ufx_t>(0);
+  }
+
+  // Frees ring slots no longer needed: behind the ITL window head and before
+  // any step an active round can still fold (rounds span <= maxdec steps).
+  PDG_HD void seg_reclaim(int d, int32_t cur_step) {
+    DecodeW& w = s_->SM.dw[d];
+    const int32_t oldest_needed = cur_step - s_->C.maxdec - 1;
+    int32_t keep = w.seg_keep;
+    while (keep < w.seg_head && keep < w.seg_end) {
+      const Seg g = seg_ring(d)[static_cast<uint32_t>(keep) & static_cast<uint32_t>(s_->C.segcap - 1)];
+      if (g.first + g.n - 1 >= oldest_needed) break;
+      ++keep;
+    }
+    w.seg_keep = keep;
+  }
+
+  // Advances the ITL window head past steps that ended at or before
+  // now - window (coordinator.cpp:32-40: the interval is (now - w, now]).
+  PDG_HD void seg_trim(int d, double now) {
+    DecodeW& w = s_->SM.dw[d];
+    const double cutoff = dsub(now, s_->PR.stat_window);
+    int32_t h = w.seg_head, off = w.seg_off;
+    for (;;) {
+      const Seg g = seg_at(d, h);
+      if (g.n == 0 || off >= g.n) {  // empty open segment, or fully expired
+        if (h == w.seg_end) break;
+        ++h;
+        off = 0;
+        continue;
+      }
+      if (seg_time(g, g.first + g.n - 1) <= cutoff) {  // the whole segment expired
+        if (h == w.seg_end) {
+          off = g.n;
+          break;
+        }
+        ++h;
+        off = 0;
+        continue;
+      }
+      // partially expired: steps first .. first+q-1 end at or before cutoff
+      int32_t q = 0;
+      if (g.t0 <= cutoff) {
+        const double est = floor(ddiv(dsub(cutoff, g.t0), g.gap));
+        q = static_cast<int32_t>(est < 0.0 ? 0.0 : (est > g.n ? g.n : est)) + 1;
+        while (q > 1 && seg_time(g, g.first + q - 1) > cutoff) --q;
+        while (q < g.n && seg_time(g, g.first + q) <= cutoff) ++q;
+      }
+      if (q > off) off = q;
+      break;
+    }
+    w.seg_head = h;
+    w.seg_off = off;
+  }
+
+  // Windowed ITL mean <= thr (coordinator.cpp:32-47 over run-length steps).
+  PDG_HD bool itl_has_slack(int d, double thr) {
+    seg_trim(d, s_->now_);
+    const DecodeW& w = s_->SM.dw[d];
+    const Pfx tail = tail_pfx(w);
+    const Seg h = seg_at(d, w.seg_head);
+    Pfx head = h.pfx;
+    if (w.seg_head <= w.seg_end && w.seg_off > 0) {
+      const ufx_t prod = w.seg_head == w.seg_end ? w.sg_prod : head_prod(h);
+      head.sum += prod * static_cast<ufx_t>(static_cast<uint32_t>(w.seg_off));
+      head.terms += static_cast<int64_t>(h.cnt) * w.seg_off;
+      if (w.seg_off >= h.n) head.inexact += h.n > 0 ? h.inex : 0;
+    }
+    const int64_t terms = tail.terms - head.terms;
+    if (terms == 0) return 0.0 <= thr;  // an empty window reads 0
+    const int dec = window_mean_le(tail, head, thr);
     if (dec >= 0) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
-    for (uint32_t k = head; k != end; ++k) sum = fold_repeat(sum, s_->G.iw_g[base + (k & mask)], s_->G.iw_c[base + (k & mask)]);
-    return ddiv(sum, static_cast<double>(w.iw.tail.terms - hp.terms)) <= thr;
+    for (int32_t i = w.seg_head; i <= w.seg_end; ++i) {
+      const Seg g = seg_at(d, i);
+      const int32_t skip = i == w.seg_head ? w.seg_off : 0;
+      if (g.n > skip) {
+        sum = fold_repeat(sum, g.gap, static_cast<uint64_t>(g.cnt) * static_cast<uint64_t>(g.n - skip));
+      }
+    }
+    return ddiv(sum, static_cast<double>(terms)) <= thr;
+  }
+  PDG_HD static ufx_t head_prod(const Seg& g) {
+    fx_t f;
+    to_fx(g.gap, &f);
+    return g.cnt > 0 ? static_cast<ufx_t>(f) * static_cast<ufx_t>(g.cnt) : static_cast<ufx_t>(0);
+  }
+
+  // Sequential fold of the ITL gaps of steps [a, k] of worker d onto s
+  // (one sample per step: a session's own tokens, sim_engine.cpp:544-555).
+  PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s) {
+    const DecodeW& w = s_->SM.dw[d];
+    if (a > k) return s;
+    int32_t i = w.seg_end;
+    for (;;) {
+      const Seg g = seg_at(d, i);
+      if (g.first <= a) break;
+      if (i <= w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
+        fail();
+        return s;
+      }
+      --i;
+    }
+    for (; i <= w.seg_end; ++i) {
+      const Seg g = seg_at(d, i);
+      const int32_t lo = a > g.first ? a : g.first;
+      const int32_t hi = k < g.first + g.n - 1 ? k : g.first + g.n - 1;
+      if (hi >= lo) s = fold_repeat(s, g.gap, static_cast<uint64_t>(hi - lo + 1));
+    }
+    return s;
   }
 
   // ---- queues + reorder (reorder.cpp:76-146; select_next sim_engine.cpp:335-350) ----
@@ -1562,46 +1691,114 @@ class Engine {
   }
 
   PDG_HD void catch_up_worker(int d, double t, uint32_t kind) {
-    {
-      DecodeW& w = s_->SM.dw[d];
-      while (w.stepping && w.steps - 1 < w.run_b) {
-        const double e = w.cur_end;
-        if (e > t) break;
-        if (e == t) {
-          if (kind == kDecodeStep) s_->abort_ = 1;
-          break;
-        }
-        silent_step(d, e);
-        if (s_->failed_ || s_->abort_) return;
+    DecodeW& w = s_->SM.dw[d];
+    const int64_t kvb = PDG_PROF.kv_bytes_per_token;
+    while (w.stepping && w.steps - 1 < w.run_b) {
+      const double e = w.cur_end;
+      if (e > t) break;
+      if (e == t) {
+        if (kind == kDecodeStep) s_->abort_ = 1;
+        break;
       }
+      // The in-flight step k ends at e (a silent step: no member finishes).
+      const int32_t k = w.steps - 1;
+      const int32_t cohort = w.cohort_n;
+      const double dur = w.dur;
+      const double last = w.last_step_t;
+      const int64_t kv = w.kv_used;
+      const int64_t tokens = s_->ctr_.tokens_decoded;
+      seg_append(d, k, 1, e, dsub(e, last), static_cast<uint32_t>(cohort - w.first_n));
+      double end = e;
+      int32_t done = 1;
+      double next = dadd(e, dur);
+      if (!(next > e)) {  // a zero-length step cannot be advanced lazily
+        s_->abort_ = 1;
+        return;
+      }
+      // Bulk: the following steps add exactly the same gap while the end
+      // time stays in one binade; complete all of them that end before t.
+      const int32_t room = w.run_b - (k + 1);
+      if (room > 0 && next < t) {
+        const double g = dsub(next, e);
+        const int64_t m = stable_run(e, dur, g, t, room);
+        if (m > 0) {
+          seg_append(d, k + 1, static_cast<int32_t>(m), next, g, static_cast<uint32_t>(cohort));
+          end = dadd(next, dmul(static_cast<double>(m - 1), g));
+          done += static_cast<int32_t>(m);
+          next = dadd(end, dur);
+          if (!(next > end)) {
+            s_->abort_ = 1;
+            return;
+          }
+        }
+      }
+      // warp-uniform stores
+      w.last_step_t = end;
+      w.kv_used = kv + static_cast<int64_t>(cohort) * done * kvb;
+      s_->ctr_.tokens_decoded = tokens + static_cast<int64_t>(cohort) * done;
+      w.first_n = 0;  // no joins inside a run (a join ends the run)
+      w.steps = k + 1 + done;
+      w.cur_end = next;
+      if (s_->failed_) return;
     }
   }
 
-  // End of a silent step (no member finishes its round in it) at time e: the
-  // effects of on_decode_step without finishers, then the next step of the
-  // same cohort starts at once (sim_engine.cpp:530-583, 513-527).
-  PDG_HD void silent_step(int d, double e) {
-    DecodeW& w = s_->SM.dw[d];
-    const int32_t k = w.steps - 1;
-    const int32_t cohort = w.cohort_n;
-    const int32_t n_itl = cohort - w.first_n;
-    const double prev = w.last_step_t;
-    const int64_t kv = w.kv_used;
-    const int64_t tokens = s_->ctr_.tokens_decoded;
-    const double next = dadd(e, w.dur);
-    const uint32_t lmask = static_cast<uint32_t>(s_->C.lcap - 1);
-    s_->G.slog[static_cast<size_t>(d) * s_->C.lcap + (static_cast<uint32_t>(k) & lmask)] = e;
-    w.last_step_t = e;
-    w.kv_used = kv + static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
-    s_->ctr_.tokens_decoded = tokens + cohort;
-    if (n_itl > 0) itl_add(d, e, dsub(e, prev), static_cast<uint32_t>(n_itl));
-    if (!(next > e)) {  // a zero-length step cannot be advanced lazily
-      s_->abort_ = 1;
-      return;
+  // Number m >= 0 of consecutive steps after a step ending at e0 whose ends
+  // E_1 = e0 + g (given, = fl(e0 + dur)), E_2 = fl(E_1 + dur), ... all add
+  // exactly g, stay below t, and number at most max_m. Within one binade of
+  // the end time the rounded increment of fl(E + dur) is the same integer
+  // number of ulps unless dur/ulp is an exact half (then it is constant once
+  // the significand is even) — the same argument as fold_repeat (fold.cuh).
+  PDG_HD static int64_t stable_run(double e0, double dur, double g, double t, int64_t max_m) {
+    const double e1 = dadd(e0, g);
+    if (!(e1 < t) || max_m <= 0) return 0;
+    const uint64_t eb = dbits(e1), db = dbits(dur);
+    const int es = static_cast<int>((eb >> 52) & 0x7ff);
+    const int ed = static_cast<int>((db >> 52) & 0x7ff);
+    if (es == 0 || ed == 0 || es >= 0x7fe || ed > es || es < 53 + 1) return 1;
+    const uint64_t kMant = (1ull << 52) - 1;
+    const uint64_t kTop = (1ull << 53) - 2;
+    const uint64_t S1 = (eb & kMant) | (1ull << 52);
+    const uint64_t G = (db & kMant) | (1ull << 52);
+    const int sh = es - ed;
+    uint64_t k, rem, half;
+    if (sh == 0) {
+      k = G;
+      rem = 0;
+      half = 1;
+    } else if (sh < 64) {
+      k = G >> sh;
+      rem = G & ((1ull << sh) - 1);
+      half = 1ull << (sh - 1);
+    } else {
+      k = 0;
+      rem = 1;
+      half = 2;
     }
-    w.first_n = 0;  // no joins inside a run (a join ends the run)
-    w.steps = k + 2;
-    w.cur_end = next;
+    uint64_t dstep;
+    if (rem == 0 || rem < half) {
+      dstep = k;
+    } else if (rem > half) {
+      dstep = k + 1;
+    } else {
+      if (S1 & 1ull) return 1;  // tie with an odd significand: one step at a time
+      dstep = k + (k & 1ull);
+    }
+    if (dstep == 0) return 1;
+    // the stable increment must be the gap we were given
+    const double ulp = bitsd(static_cast<uint64_t>(es - 52) << 52);
+    if (dmul(static_cast<double>(dstep), ulp) != g) return 1;
+    if (S1 > kTop) return 1;
+    int64_t m = 1 + static_cast<int64_t>((kTop - S1) / dstep);
+    const uint64_t tb = dbits(t);
+    const int et = static_cast<int>((tb >> 52) & 0x7ff);
+    if (et == es) {  // t in the same binade: S1 + (j-1) d < T
+      const uint64_t T = (tb & kMant) | (1ull << 52);
+      const int64_t mt = 1 + static_cast<int64_t>((T - S1 - 1) / dstep);
+      if (mt < m) m = mt;
+    }
+    if (max_m < m) m = max_m;
+    return m;
   }
 
   // A join or a local prefill on a worker whose in-flight step is silent:
@@ -1632,18 +1829,15 @@ class Engine {
     const int32_t cohort = w.cohort_n;
     const int32_t n_itl = cohort - w.first_n;
     const double prev = w.last_step_t;
-    const uint32_t lmask = static_cast<uint32_t>(s_->C.lcap - 1);
-    double* slog = s_->G.slog + static_cast<size_t>(d) * s_->C.lcap;
     const double now = s_->now_;
     const int64_t kv = w.kv_used;
     const int64_t tokens = s_->ctr_.tokens_decoded;
+    seg_append(d, k, 1, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
     // warp-uniform stores
-    slog[static_cast<uint32_t>(k) & lmask] = now;
     w.stepping = 0;
     w.last_step_t = now;
     w.kv_used = kv + static_cast<int64_t>(cohort) * PDG_PROF.kv_bytes_per_token;
     s_->ctr_.tokens_decoded = tokens + cohort;
-    if (n_itl > 0) itl_add(d, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
 
     bool any_terminated = false;
     while (!s_->failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
@@ -1658,10 +1852,7 @@ class Engine {
       const int32_t ridx = s_->T.round_off[i] + s.round - 1;
       const int32_t dec = s_->T.dec[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
-      double sum = s.itl_sum;
-      for (int32_t j = s.join + 1; j <= k; ++j) {
-        sum = dadd(sum, dsub(slog[static_cast<uint32_t>(j) & lmask], slog[static_cast<uint32_t>(j - 1) & lmask]));
-      }
+      const double sum = seg_fold(d, s.join + 1, k, s.itl_sum);
       const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
       warp_sync();
       if (lane_id() == 0) {

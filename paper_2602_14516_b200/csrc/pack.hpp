@@ -370,8 +370,10 @@ inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax
   // Windows are trimmed lazily (at queries, or when full): twice the
   // in-window bound keeps forced trims rare.
   c.twcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(2 * tw + 2, 4)));
-  c.iwcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(2 * iw + 2, 4)));
-  c.lcap = static_cast<int32_t>(pow2_at_least(maxdec + 2));
+  // Step segments retained: those in the ITL window (<= one per step in it)
+  // plus those a running round may still fold (rounds span <= maxdec steps).
+  c.segcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(iw + maxdec + 16, 16)));
+  c.maxdec = static_cast<int32_t>(maxdec);
   return c;
 }
 
