@@ -201,7 +201,9 @@ struct SessRt {
   int8_t bound;      // decode worker index
   int8_t postpone;   // PrefillTask::postpone_count
   int8_t ttft_bad;   // some TTFT > threshold
-  int8_t reserved[7];
+  int8_t reserved0;
+  int32_t seg_hint;  // bound worker's open-segment index when the round joined
+  int8_t reserved1[2];
 };
 
 // A worker's task queue (global ring) + exact sum of the queued costs.
@@ -1344,24 +1346,34 @@ class Engine {
 
   // Sequential fold of the ITL gaps of steps [a, k] of worker d onto s
   // (one sample per step: a session's own tokens, sim_engine.cpp:544-555).
-  PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s) {
+  // `hint` is the open-segment index when the round joined: the segment
+  // holding step a is at or after it.
+  PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s, int32_t hint) {
     const DecodeW& w = s_->SM.dw[d];
     if (a > k) return s;
-    int32_t i = w.seg_end;
-    for (;;) {
-      const Seg g = seg_at(d, i);
-      if (g.first <= a) break;
-      if (i <= w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
-        fail();
-        return s;
-      }
-      --i;
+    if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
+      fail();
+      return s;
     }
-    for (; i <= w.seg_end; ++i) {
-      const Seg g = seg_at(d, i);
-      const int32_t lo = a > g.first ? a : g.first;
-      const int32_t hi = k < g.first + g.n - 1 ? k : g.first + g.n - 1;
-      if (hi >= lo) s = fold_repeat(s, g.gap, static_cast<uint64_t>(hi - lo + 1));
+    const Seg* ring = seg_ring(d);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
+    for (int32_t i = hint; i <= w.seg_end; ++i) {
+      const Seg& g = i == w.seg_end ? w.sg : ring[static_cast<uint32_t>(i) & mask];
+      const int32_t gfirst = g.first, gn = g.n;
+      const int32_t lo = a > gfirst ? a : gfirst;
+      const int32_t hi = k < gfirst + gn - 1 ? k : gfirst + gn - 1;
+      if (hi < lo) {
+        if (gfirst > k) break;
+        continue;
+      }
+      const double gap = g.gap;
+      const int32_t cnt = hi - lo + 1;
+      if (cnt <= 4) {
+        for (int32_t c = 0; c < cnt; ++c) s = dadd(s, gap);
+      } else {
+        s = fold_repeat(s, gap, static_cast<uint64_t>(cnt));
+      }
+      if (hi == k) break;
     }
     return s;
   }
@@ -1590,10 +1602,12 @@ class Engine {
     const uint64_t key =
         (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(s_->T.rank[i]);
     warp_sync();
+    const int32_t hint = w.seg_end;
     if (lane_id() == 0) {
       if (value > s_->T.ttft_thres) s.ttft_bad = 1;
       s.ctx += incr;
       s.join = join;
+      s.seg_hint = hint;
       w.kv_used += static_cast<int64_t>(incr) * PDG_PROF.kv_bytes_per_token;
       ++w.batch_n;
       ++w.n_new;
@@ -1852,7 +1866,7 @@ class Engine {
       const int32_t ridx = s_->T.round_off[i] + s.round - 1;
       const int32_t dec = s_->T.dec[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
-      const double sum = seg_fold(d, s.join + 1, k, s.itl_sum);
+      const double sum = seg_fold(d, s.join + 1, k, s.itl_sum, s.seg_hint);
       const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
       warp_sync();
       if (lane_id() == 0) {
