@@ -430,6 +430,7 @@ struct EngState {
   int32_t failed_;
   int32_t nslots_;
   int32_t lazy_;   // lazy decode stepping enabled for this attempt
+  uint32_t cur_kind_;  // kind of the event being processed (catch-up tie rule)
   int32_t abort_;  // lazy attempt hit an ambiguous tie: replay exactly
   pdsim_attainment att_;
   pdsim_counters ctr_;
@@ -518,22 +519,19 @@ class Engine {
         const int32_t i = s_->next_arr_++;
         const double t = s_->next_arr_t_;
         if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = s_->T.arrival[s_->next_arr_];
-        if (s_->lazy_) catch_up(t, kArrival);
+        s_->cur_kind_ = kArrival;
         advance_to(t);
         on_arrival(i);
         continue;
       }
       const uint32_t kind = static_cast<uint32_t>(bk >> 58);
-      if (s_->lazy_) {
-        // Two decode-step events at the same time: their order is the
-        // scheduling order, which lazily materialised steps do not carry.
-        if (src == 0 && kind == kDecodeStep && slot_tie) {
-          s_->abort_ = 1;
-          return;
-        }
-        catch_up(bt, kind);
-        if (s_->abort_) return;
+      // Two decode-step events at the same time: their order is the
+      // scheduling order, which lazily materialised steps do not carry.
+      if (s_->lazy_ && src == 0 && kind == kDecodeStep && slot_tie) {
+        s_->abort_ = 1;
+        return;
       }
+      s_->cur_kind_ = kind;
       ++s_->events_;
       advance_to(bt);
       if (src == 1) {
@@ -860,7 +858,8 @@ class Engine {
     s_->adm_head_ = i + 1;
   }
 
-  PDG_HD int bind_session() const {  // least KV bytes, lowest index on ties
+  PDG_HD int bind_session() {  // least KV bytes, lowest index on ties
+    if (s_->lazy_) catch_up(s_->now_, s_->cur_kind_);
     int best = 0;
     int64_t bv = s_->SM.dw[0].kv_used;
     for (int d = 1; d < s_->PL.D; ++d) {
@@ -1312,6 +1311,7 @@ class Engine {
 
   // Windowed ITL mean <= thr (coordinator.cpp:32-47 over run-length steps).
   PDG_HD bool itl_has_slack(int d, double thr) {
+    if (s_->lazy_) catch_up_worker(d, s_->now_, s_->cur_kind_);
     seg_trim(d, s_->now_);
     const DecodeW& w = s_->SM.dw[d];
     const Pfx tail = tail_pfx(w);
@@ -1820,6 +1820,7 @@ class Engine {
   PDG_HD void interrupt_run(int d) {
     DecodeW& w = s_->SM.dw[d];
     if (!s_->lazy_ || !w.stepping) return;
+    catch_up_worker(d, s_->now_, s_->cur_kind_);
     const int32_t k = w.steps - 1;
     if (w.run_b <= k) return;
     const double end = w.cur_end;
@@ -1839,6 +1840,7 @@ class Engine {
 
   PDG_HD void on_decode_step(int d) {
     DecodeW& w = s_->SM.dw[d];
+    if (s_->lazy_) catch_up_worker(d, s_->now_, kDecodeStep);
     const int32_t k = w.steps - 1;  // index of the step that just ended
     const int32_t cohort = w.cohort_n;
     const int32_t n_itl = cohort - w.first_n;
