@@ -607,8 +607,7 @@ class Engine {
       s_->st_[j] = kInf;
       s_->sk_[j] = ~0ull;
     }
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       uint32_t idx;
       mt64_seed(s_->SM.mt, &idx, s_->seed_);
       for (int p = 0; p < s_->PL.P; ++p) {
@@ -814,13 +813,10 @@ class Engine {
       const int32_t par = (i - 1) >> 1;
       const HEv pe = h[par];
       if (!before(e.t, e.key, pe.t, pe.key)) break;
-      warp_sync();
-      if (lane_id() == 0) h[i] = pe;
+      h[i] = pe;  // warp-uniform store
       i = par;
     }
-    warp_sync();
-    if (lane_id() == 0) h[i] = e;
-    warp_sync();
+    h[i] = e;  // warp-uniform store
   }
 
   PDG_COLD HEv heap_pop() {
@@ -840,8 +836,7 @@ class Engine {
         }
       }
       if (!before(ce.t, ce.key, last.t, last.key)) break;
-      warp_sync();
-      if (lane_id() == 0) h[i] = ce;
+      h[i] = ce;  // warp-uniform store
       i = c;
     }
     warp_sync();
@@ -878,8 +873,7 @@ class Engine {
     const int64_t first = static_cast<int64_t>(s_->T.incr[s_->T.round_off[i]]) * PDG_PROF.kv_bytes_per_token;
     if (w.kv_used + first > w.kv_cap) return false;
     SessRt& s = s_->G.sess[i];
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       s.bound = static_cast<int8_t>(best);
       s.bind_time = s_->now_;
       s.round = 1;
@@ -890,7 +884,6 @@ class Engine {
       s.postpone = 0;
       s.ttft_bad = 0;
     }
-    warp_sync();
     start_round(i, 1, best, 0);
     return true;
   }
@@ -902,12 +895,10 @@ class Engine {
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
   PDG_COLD void start_round(int32_t i, int round, int bound, int32_t ctx) {
     SessRt& s = s_->G.sess[i];
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       s.t_enq = s_->now_;
       s.postpone = 0;
     }
-    warp_sync();
     ++s_->ctr_.tasks_created;
     const int32_t incr = s_->T.incr[s_->T.round_off[i] + round - 1];
     const RouteOut r = decide(i, bound, ctx, incr);
@@ -961,20 +952,16 @@ class Engine {
     const int n = s_->PL.P;
     if (n > 0) {
       int32_t* order = s_->SM.order;
-      warp_sync();
-      if (lane_id() == 0) {
+      {  // warp-uniform stores (every lane writes the same values)
         for (int k = 0; k < n; ++k) order[k] = k;
       }
-      warp_sync();
       for (int k = n - 1; k > 0; --k) {
         const int j = static_cast<int>(rng_next() % static_cast<uint64_t>(k + 1));
         const int a = order[k], b = order[j];
-        warp_sync();
-        if (lane_id() == 0) {
+        {  // warp-uniform stores (every lane writes the same values)
           order[k] = b;
           order[j] = a;
         }
-        warp_sync();
       }
       const double thr = dmul(s_->PR.alpha, s_->T.ttft_thres);
       for (int k = 0; k < n; ++k) {
@@ -1147,9 +1134,7 @@ class Engine {
       head += static_cast<uint32_t>(n);
       if (n < PDG_NL) break;
     }
-    warp_sync();
-    if (lane_id() == 0) w.head = head;
-    warp_sync();
+    w.head = head;  // warp-uniform store
   }
 
   PDG_HD bool window_room(WinState& w, const double* times, uint32_t cap, double now) {
@@ -1172,15 +1157,13 @@ class Engine {
     const Pfx cur = w.tw.tail;
     Pfx next = cur;
     next.add(v, 1);
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       s_->G.tw_t[base + k] = s_->now_;
       s_->G.tw_v[base + k] = v;
       s_->G.tw_p[base + k] = cur;
       w.tw.tail = next;
       ++w.tw.end;
     }
-    warp_sync();
   }
 
   // query(now) <= thr with the sequential windowed mean's semantics.
@@ -1388,14 +1371,12 @@ class Engine {
     const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     ExactSum ns = q.sum;
     ns.add(cost);
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       qs[qt & mask] = i;
       qc[qt & mask] = cost;
       q.sum = ns;
       q.qt = qt + 1;
     }
-    warp_sync();
     return true;
   }
 
@@ -1413,12 +1394,10 @@ class Engine {
     ExactSum ns = q.sum;
     ns.remove(*cost);
     const int32_t pc = s_->G.sess[i].postpone;
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       q.sum = ns;
       q.qh = qh + 1;
     }
-    warp_sync();
     if (pc > s_->ctr_.max_postpone_observed) s_->ctr_.max_postpone_observed = pc;
     return i;
   }
@@ -1475,8 +1454,7 @@ class Engine {
     }
     if (best_r == 0) return;
     unrank_perm(best_r, m, perm);
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       for (int k = 0; k < m; ++k) {
         const int p = perm[k];
         if (k > p) ++s_->G.sess[hs[p]].postpone;
@@ -1484,7 +1462,6 @@ class Engine {
         qc[(qh + k) & mask] = hc[p];
       }
     }
-    warp_sync();
   }
 
   PDG_HD static int count_satisfied(const int* perm, int m, const double* hc, const double* wait, double thres) {
@@ -1520,15 +1497,13 @@ class Engine {
       const int dd = s_->SM.dw[s_->G.sess[stg].bound].deg;
       ready = dadd(s_->now_, t_kv(hist, dd, w.deg));
     }
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       w.stg = stg;
       w.stg_cost = cost;
       w.staged = 1;
       w.staged_ready = ready;
       w.pending = hist > 0 ? 1 : 0;
     }
-    warp_sync();
     if (hist > 0) set_slot(slot_history(p), ready, kKvTransferDone);
   }
 
@@ -1536,14 +1511,12 @@ class Engine {
     PrefillW& w = s_->SM.pw[p];
     if (w.computing || !w.staged || w.pending || w.staged_ready > s_->now_) return;
     const double done = dadd(s_->now_, w.stg_cost);
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       w.cur = w.stg;
       w.cur_cost = w.stg_cost;
       w.staged = 0;
       w.computing = 1;
     }
-    warp_sync();
     set_slot(slot_compute(p), done, kPrefillDone);
     try_stage(p);  // the next task's history read overlaps this compute
   }
@@ -1551,9 +1524,7 @@ class Engine {
   PDG_COLD void on_prefill_done(int p) {
     PrefillW& w = s_->SM.pw[p];
     const int32_t i = w.cur;
-    warp_sync();
-    if (lane_id() == 0) w.computing = 0;
-    warp_sync();
+    w.computing = 0;  // warp-uniform store
     const int dd = s_->SM.dw[s_->G.sess[i].bound].deg;
     heap_push(dadd(s_->now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
               static_cast<uint32_t>(p));
@@ -1562,9 +1533,7 @@ class Engine {
   }
 
   PDG_HD void on_history_read(int p) {
-    warp_sync();
-    if (lane_id() == 0) s_->SM.pw[p].pending = 0;
-    warp_sync();
+    s_->SM.pw[p].pending = 0;  // warp-uniform store
     try_start_compute(p);
   }
 
@@ -1635,13 +1604,11 @@ class Engine {
       double cost;
       const int32_t cur = select_next(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap,
                                       s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, &cost);
-      warp_sync();
-      if (lane_id() == 0) {
+      {  // warp-uniform stores (every lane writes the same values)
         w.cur = cur;
         w.cur_cost = cost;
         w.prefilling = 1;
       }
-      warp_sync();
       set_slot(d, dadd(s_->now_, cost), kPrefillDone);
       return;
     }
@@ -1831,9 +1798,7 @@ class Engine {
   PDG_HD void on_local_prefill_done(int d) {
     DecodeW& w = s_->SM.dw[d];
     const int32_t i = w.cur;
-    warp_sync();
-    if (lane_id() == 0) w.prefilling = 0;
-    warp_sync();
+    w.prefilling = 0;  // warp-uniform store
     complete_task(i, true, -1, d);
     advance_decode(d);
   }
@@ -1870,14 +1835,12 @@ class Engine {
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       const double sum = seg_fold(d, s.join + 1, k, s.itl_sum, s.seg_hint);
       const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
-      warp_sync();
-      if (lane_id() == 0) {
+      {  // warp-uniform stores (every lane writes the same values)
         s.itl_sum = sum;
         s.itl_cnt += dec - 1;
         s.ctx += dec;
         --w.batch_n;
       }
-      warp_sync();
       if (last) {
         terminate_session(i, d);
         any_terminated = true;
@@ -1894,9 +1857,7 @@ class Engine {
     const int round = s.round + 1;
     const int bound = s.bound;
     const int32_t ctx = s.ctx;
-    warp_sync();
-    if (lane_id() == 0) s.round = static_cast<int16_t>(round);
-    warp_sync();
+    s.round = static_cast<int16_t>(round);  // warp-uniform store
     start_round(i, round, bound, ctx);
   }
 
@@ -1909,8 +1870,7 @@ class Engine {
     const bool ttft_ok = !s.ttft_bad;
     const bool itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
     const bool slo_ok = ttft_ok && itl_ok;
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       s_->SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
       if (s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
@@ -1926,7 +1886,6 @@ class Engine {
         o.reserved = 0;
       }
     }
-    warp_sync();
     ++s_->att_.sessions_completed;
     s_->att_.slo_ok += slo_ok;
     s_->att_.ttft_ok += ttft_ok;
@@ -1943,8 +1902,7 @@ class Engine {
     }
     uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
     const uint64_t top = w.fh_top;
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       int32_t i = n;
       while (i > 0) {
         const int32_t par = (i - 1) >> 1;
@@ -1957,14 +1915,12 @@ class Engine {
       w.fh_n = n + 1;
       if (n == 0 || key < top) w.fh_top = key;
     }
-    warp_sync();
   }
 
   PDG_COLD void fh_pop(int d) {
     DecodeW& w = s_->SM.dw[d];
     uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
-    warp_sync();
-    if (lane_id() == 0) {
+    {  // warp-uniform stores (every lane writes the same values)
       const int32_t n = w.fh_n - 1;
       const uint64_t last = h[n];
       int32_t i = 0;
@@ -1987,7 +1943,6 @@ class Engine {
       w.fh_n = n;
       w.fh_top = n > 0 ? h[0] : 0;
     }
-    warp_sync();
   }
 };
 
