@@ -792,7 +792,7 @@ class Engine {
   // ---- session-event heap (shared memory, global spill) ----
   PDG_HD HEv* heap_base() const { return s_->heap_spilled_ ? s_->G.heap : s_->SM.heap; }
 
-  PDG_COLD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
+  PDG_HD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
     HEv e;
     e.t = t;
     e.key = mk_key(kind, s_->seq_++, 0);
@@ -819,7 +819,7 @@ class Engine {
     h[i] = e;  // warp-uniform store
   }
 
-  PDG_COLD HEv heap_pop() {
+  PDG_HD HEv heap_pop() {
     HEv* h = heap_base();
     const HEv top = h[0];
     const HEv last = h[--s_->hn_];
@@ -1475,7 +1475,7 @@ class Engine {
   }
 
   // ---- prefill workers (sim_engine.cpp:354-453) ----
-  PDG_COLD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
+  PDG_HD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
     PrefillW& w = s_->SM.pw[p];
     const double cost = t_prefill(ctx, incr, w.deg);
     if (!queue_push(w.q, s_->G.pq_s + static_cast<size_t>(p) * s_->C.qcap, s_->G.pq_c + static_cast<size_t>(p) * s_->C.qcap, i, cost))
@@ -1484,7 +1484,7 @@ class Engine {
     try_start_compute(p);
   }
 
-  PDG_COLD void try_stage(int p) {
+  PDG_HD void try_stage(int p) {
     PrefillW& w = s_->SM.pw[p];
     if (w.staged || w.q.qh == w.q.qt) return;
     double cost;
@@ -1521,7 +1521,7 @@ class Engine {
     try_stage(p);  // the next task's history read overlaps this compute
   }
 
-  PDG_COLD void on_prefill_done(int p) {
+  PDG_HD void on_prefill_done(int p) {
     PrefillW& w = s_->SM.pw[p];
     const int32_t i = w.cur;
     w.computing = 0;  // warp-uniform store
@@ -1544,7 +1544,7 @@ class Engine {
   }
 
   // complete_task (sim_engine.cpp:458-484).
-  PDG_COLD void complete_task(int32_t i, bool local, int p, int d) {
+  PDG_HD void complete_task(int32_t i, bool local, int p, int d) {
     SessRt& s = s_->G.sess[i];
     const int round = s.round;
     const double created = round == 1 ? s_->T.arrival[i] : s.t_enq;
@@ -1893,7 +1893,7 @@ class Engine {
   }
 
   // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
-  PDG_COLD void fh_push(int d, uint64_t key) {
+  PDG_HD void fh_push(int d, uint64_t key) {
     DecodeW& w = s_->SM.dw[d];
     const int32_t n = w.fh_n;
     if (n >= s_->C.fcap) {
@@ -1917,7 +1917,7 @@ class Engine {
     }
   }
 
-  PDG_COLD void fh_pop(int d) {
+  PDG_HD void fh_pop(int d) {
     DecodeW& w = s_->SM.dw[d];
     uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
     {  // warp-uniform stores (every lane writes the same values)
