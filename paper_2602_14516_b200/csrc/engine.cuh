@@ -191,19 +191,20 @@ struct DevParams {
 
 // Per-session runtime state (SessionRt + the one PrefillTask in flight).
 struct SessRt {
+  ufx_t itl_fx;      // search mode: exact fixed-point sum of this session's ITL samples
   double t_enq;      // enqueue time of the current task (== created for r >= 2)
-  double itl_sum;    // sequential fold of this session's ITL samples
+  double itl_sum;    // exact mode: sequential fold of this session's ITL samples
   double bind_time;  // admission time
   int32_t itl_cnt;
+  int32_t itl_inex;  // ITL samples without an exact fixed-point image
   int32_t join;      // step index at which the current round joined the batch
   int32_t ctx;       // context_len
+  int32_t seg_hint;  // bound worker's open-segment index when the round joined
   int16_t round;     // 1-based current round
   int8_t bound;      // decode worker index
   int8_t postpone;   // PrefillTask::postpone_count
   int8_t ttft_bad;   // some TTFT > threshold
-  int8_t reserved0;
-  int32_t seg_hint;  // bound worker's open-segment index when the round joined
-  int8_t reserved1[2];
+  int8_t reserved[7];
 };
 
 // A worker's task queue (global ring) + exact sum of the queued costs.
@@ -235,18 +236,22 @@ struct PrefillW {  // shared memory
 // at t0 + (j - first) * gap exactly (each step adds exactly `gap`).
 struct Seg {
   Pfx pfx;       // window prefix before this segment
+  ufx_t p1;      // sum of fx(gap) over every step before this segment (one per step)
   double t0;     // end time of step `first`
   double gap;    // every step's ITL gap (end - previous end)
   int32_t first; // first step index
   int32_t n;     // steps
   uint32_t cnt;  // ITL samples per step (cohort members past their first token)
   int32_t inex;  // gap has no exact fixed-point image (and cnt > 0)
+  int32_t inex1; // steps before this segment whose gap has no exact image
+  int32_t gx;    // gap has an exact fixed-point image
 };
 
 struct DecodeW {  // shared memory
   TaskQueue q;  // local prefill queue
   Seg sg;       // the open (newest) segment of the step log
   ufx_t sg_prod;       // fx(sg.gap) * sg.cnt
+  ufx_t sg_fx;         // fx(sg.gap)
   int64_t kv_used;
   int64_t kv_cap;
   uint64_t fh_top;     // cached finisher-heap minimum (valid when fh_n > 0)
@@ -430,6 +435,7 @@ struct EngState {
   int32_t failed_;
   int32_t nslots_;
   int32_t lazy_;   // lazy decode stepping enabled for this attempt
+  int32_t exact_itl_;  // per-session ITL means by sequential fold (records / retry)
   uint32_t cur_kind_;  // kind of the event being processed (catch-up tie rule)
   int32_t abort_;  // lazy attempt hit an ambiguous tie: replay exactly
   pdsim_attainment att_;
@@ -481,6 +487,7 @@ class Engine {
     for (int attempt = 0; attempt < 2; ++attempt) {
       init();
       s_->lazy_ = attempt == 0 ? 1 : 0;
+      s_->exact_itl_ = (attempt > 0 || s_->REC.sessions) ? 1 : 0;
       event_loop();
       if (!s_->abort_) break;
     }
@@ -627,6 +634,10 @@ class Engine {
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.sg.pfx.clear();
+        w.sg.p1 = 0;
+        w.sg.inex1 = 0;
+        w.sg.gx = 1;
+        w.sg_fx = 0;
         w.sg.t0 = 0.0;
         w.sg.gap = 0.0;
         w.sg.first = 0;
@@ -879,6 +890,8 @@ class Engine {
       s.round = 1;
       s.ctx = 0;
       s.itl_sum = 0.0;
+      s.itl_fx = 0;
+      s.itl_inex = 0;
       s.itl_cnt = 0;
       s.join = 0;
       s.postpone = 0;
@@ -1225,12 +1238,18 @@ class Engine {
       }
       const Seg closed = w.sg;
       const Pfx next_pfx = tail_pfx(w);
+      const ufx_t next_p1 = closed.p1 + w.sg_fx * static_cast<ufx_t>(static_cast<uint32_t>(closed.n));
+      const int32_t next_inex1 = closed.inex1 + (closed.gx ? 0 : closed.n);
       seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = closed;
       w.seg_end = end + 1;
       w.sg.pfx = next_pfx;
+      w.sg.p1 = next_p1;
+      w.sg.inex1 = next_inex1;
     }
     fx_t f;
     const bool exact = to_fx(gap, &f);
+    w.sg.gx = exact ? 1 : 0;
+    w.sg_fx = static_cast<ufx_t>(f);
     w.sg.t0 = t0;
     w.sg.gap = gap;
     w.sg.first = first;
@@ -1325,6 +1344,41 @@ class Engine {
     fx_t f;
     to_fx(g.gap, &f);
     return g.cnt > 0 ? static_cast<ufx_t>(f) * static_cast<ufx_t>(g.cnt) : static_cast<ufx_t>(0);
+  }
+
+  // Exact fixed-point sum of the ITL gaps of steps (j0, k] of worker d (one
+  // sample per step) and the number of those gaps without an exact image.
+  // Step k is in the open segment; the segment holding j0 is at or after
+  // `hint` (the open-segment index when the round joined).
+  PDG_HD ufx_t seg_sum(int d, int32_t j0, int32_t k, int32_t hint, int32_t* inex) {
+    const DecodeW& w = s_->SM.dw[d];
+    if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
+      fail();
+      *inex = 0;
+      return 0;
+    }
+    // prefix through step k (open segment)
+    const int32_t nk = k - w.sg.first + 1;
+    const ufx_t pk = w.sg.p1 + w.sg_fx * static_cast<ufx_t>(static_cast<uint32_t>(nk));
+    const int32_t ik = w.sg.inex1 + (w.sg.gx ? 0 : nk);
+    // prefix through step j0
+    const Seg* ring = seg_ring(d);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
+    ufx_t pj = 0;
+    int32_t ij = 0;
+    for (int32_t i = hint; i <= w.seg_end; ++i) {
+      const Seg& g = i == w.seg_end ? w.sg : ring[static_cast<uint32_t>(i) & mask];
+      if (j0 < g.first + g.n) {
+        const int32_t nj = j0 - g.first + 1;  // >= 0 (j0 >= g.first - 1)
+        fx_t f;
+        to_fx(g.gap, &f);
+        pj = g.p1 + static_cast<ufx_t>(f) * static_cast<ufx_t>(static_cast<uint32_t>(nj < 0 ? 0 : nj));
+        ij = g.inex1 + (g.gx ? 0 : (nj < 0 ? 0 : nj));
+        break;
+      }
+    }
+    *inex = ik - ij;
+    return pk - pj;
   }
 
   // Sequential fold of the ITL gaps of steps [a, k] of worker d onto s
@@ -1833,10 +1887,21 @@ class Engine {
       const int32_t ridx = s_->T.round_off[i] + s.round - 1;
       const int32_t dec = s_->T.dec[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
-      const double sum = seg_fold(d, s.join + 1, k, s.itl_sum, s.seg_hint);
+      double sum = s.itl_sum;
+      ufx_t fxs = s.itl_fx;
+      int32_t inex = s.itl_inex;
+      if (s_->exact_itl_) {
+        sum = seg_fold(d, s.join + 1, k, sum, s.seg_hint);
+      } else if (dec > 1) {
+        int32_t ri;
+        fxs += seg_sum(d, s.join, k, s.seg_hint, &ri);
+        inex += ri;
+      }
       const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
       {  // warp-uniform stores (every lane writes the same values)
         s.itl_sum = sum;
+        s.itl_fx = fxs;
+        s.itl_inex = inex;
         s.itl_cnt += dec - 1;
         s.ctx += dec;
         --w.batch_n;
@@ -1868,7 +1933,23 @@ class Engine {
     const int32_t cnt = s.itl_cnt;
     const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
     const bool ttft_ok = !s.ttft_bad;
-    const bool itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
+    bool itl_ok;
+    if (s_->exact_itl_ || cnt == 0) {
+      itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
+    } else {
+      // search mode: certified decision of fl(fold / cnt) <= itl_thres
+      ExactSum es;
+      es.sum = static_cast<fx_t>(s.itl_fx);
+      es.terms = cnt;
+      es.inexact = s.itl_inex;
+      es.reserved = 0;
+      const int dec = mean_le_certified(es, s_->T.itl_thres);
+      if (dec < 0) {  // inside the error band: replay this pair with exact folds
+        s_->abort_ = 1;
+        return;
+      }
+      itl_ok = dec == 1;
+    }
     const bool slo_ok = ttft_ok && itl_ok;
     {  // warp-uniform stores (every lane writes the same values)
       s_->SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;

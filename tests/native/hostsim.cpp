@@ -96,3 +96,20 @@ extern "C" void hostsim_set_smem_budget(size_t bytes) { g_smem_budget = bytes; }
 extern "C" double hostsim_fold_repeat(double s, double g, uint64_t count) {
   return pdg::fold_repeat(s, g, count);
 }
+
+// Counts only (no record arrays): exercises the search-mode paths (certified
+// per-session ITL verdicts) exactly as the batched GPU search runs them.
+extern "C" int hostsim_run_counts(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_profile* prof,
+                                  const pdsim_sched_params* params, uint64_t seed, pdsim_run_output* out) {
+  pdsim_run_output o = *out;
+  o.decisions = nullptr;
+  o.ttft_samples = nullptr;
+  o.sessions = nullptr;
+  const int rc = hostsim_run(trace, plan, prof, params, seed, &o);
+  out->n_decisions = o.n_decisions;
+  out->n_ttft = o.n_ttft;
+  out->n_sessions = o.n_sessions;
+  out->counters = o.counters;
+  out->attainment = o.attainment;
+  return rc;
+}

@@ -24,6 +24,7 @@ def hostsim():
         L.hostsim_run.argtypes = [P(abi.Trace), P(abi.Plan), P(abi.Profile), P(abi.SchedParams), C.c_uint64,
                                   P(abi.RunOutput)]
         L.hostsim_last_error.restype = C.c_char_p
+        L.hostsim_run_counts.argtypes = L.hostsim_run.argtypes
         L.hostsim_fold_repeat.argtypes = [C.c_double, C.c_double, C.c_uint64]
         L.hostsim_fold_repeat.restype = C.c_double
         _hostsim = L
@@ -65,6 +66,27 @@ def host_run(trace, plan, profile, params, seed):
     if rc:
         raise EngineError(rc, hostsim().hostsim_last_error().decode())
     return Run(out, dec, ttft, sess)
+
+
+def host_run_counts(trace, plan, profile, params, seed):
+    """Counts-only host replay (search mode: no records)."""
+    out = abi.RunOutput()
+    rc = hostsim().hostsim_run_counts(C.byref(trace), C.byref(plan), C.byref(profile), C.byref(params), seed,
+                                      C.byref(out))
+    if rc:
+        raise EngineError(rc, hostsim().hostsim_last_error().decode())
+    return Run(out, None, None, None)
+
+
+def diff_counts(got, want):
+    errs = []
+    for f in CTR_FIELDS:
+        if getattr(got.counters, f) != getattr(want.counters, f):
+            errs.append(f"counter {f}: {getattr(got.counters, f)} != {getattr(want.counters, f)}")
+    for f in ATT_FIELDS:
+        if getattr(got.attainment, f) != getattr(want.attainment, f):
+            errs.append(f"attainment {f}: {getattr(got.attainment, f)} != {getattr(want.attainment, f)}")
+    return errs
 
 
 def oracle_kind():

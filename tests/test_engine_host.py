@@ -44,6 +44,8 @@ def test_engine_matches_oracle_random_configs(seed):
         a = parity.host_run(tr.view, plan, prof, prm, es)
         b = parity.oracle_run(tr.view, plan, prof, prm, es)
         parity.assert_same_run(a, b)
+        c = parity.host_run_counts(tr.view, plan, prof, prm, es)
+        assert not parity.diff_counts(c, b)
 
 
 def naive_fold(s, g, n):
@@ -132,3 +134,15 @@ def test_engine_heap_spill_to_global_matches_golden():
             assert parity.digest(got) == entry["expect"], c["name"]
     finally:
         H.hostsim_set_smem_budget(0)
+
+
+@pytest.mark.parametrize("entry", CASES, ids=golden_cases.ids())
+def test_engine_search_mode_counts_match_golden(entry):
+    """Without record arrays the engine runs its search-mode paths (exact
+    fixed-point per-session ITL sums with certified verdicts); counters and
+    attainment must still equal the reference's."""
+    c = entry["case"]
+    trace, plan, prof, params = parity.build_case(c)
+    got = parity.host_run_counts(trace.view, plan, prof, params, c["engine_seed"])
+    assert parity.digest(got)["counters"] == entry["expect"]["counters"]
+    assert parity.digest(got)["attainment"] == entry["expect"]["attainment"]
