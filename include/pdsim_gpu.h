@@ -285,6 +285,15 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
                             int64_t pair_end, uint64_t seed,
                             pdsim_search_output* out);
 
+/* Diagnostics: per-phase SM-cycle instrumentation of the replay kernel
+ * (buckets: 0 event selection, 1 arrival, 2 interaction done, 3 write-back,
+ * 4 decode step, 5 local prefill done, 6 prefill compute done, 7 history
+ * read), summed over the pairs of the last search; `replayed` counts pairs
+ * whose fast attempt was replayed in exact mode. */
+int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
+int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles8, int64_t* counts8,
+                               int64_t* replayed);
+
 /* ---- host-side helpers (reference generators; host C++, libm) ------------ */
 
 /* SynthProfileSpec (perf_model.hpp:110-139). */

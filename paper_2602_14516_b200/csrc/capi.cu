@@ -81,6 +81,11 @@ struct pdsim_gpu_ctx {
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
   DevBuf d_dec, d_ttft, d_sess;
+  // diagnostics
+  int profiling = 0;
+  int64_t prof_cycles[8] = {0};
+  int64_t prof_count[8] = {0};
+  int64_t attempts2 = 0;
 };
 
 namespace {
@@ -123,6 +128,8 @@ struct KernelArgs {
   int* cand_bad;                       // [n_candidates]
   pdg::Records rec;                    // single-run records (one pair only)
   uint64_t seed;
+  int32_t profile;                     // per-phase clock64 instrumentation
+  int32_t reserved2;
 };
 
 // One warp per block; the warp replays pairs pulled from an atomic queue.
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed);
+      pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, a.profile);
       eng.run(&res);
       res.cycles = clock64() - t0;
     }
@@ -362,6 +369,7 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.cand_bad = ctx->d_cand_bad.as<int>();
   a.rec = rec;
   a.seed = seed;
+  a.profile = ctx->profiling;
   int64_t launches = 0;
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
@@ -398,7 +406,16 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   CU(ctx, cudaEventElapsedTime(&d_ms, ctx->ev[0], ctx->ev[3]));
 
   bool engine_error = false;
-  for (const auto& r : res) engine_error |= r.status == PDSIM_PAIR_ERROR;
+  for (int j = 0; j < 8; ++j) ctx->prof_cycles[j] = ctx->prof_count[j] = 0;
+  ctx->attempts2 = 0;
+  for (const auto& r : res) {
+    engine_error |= r.status == PDSIM_PAIR_ERROR;
+    ctx->attempts2 += r.attempts > 1 ? 1 : 0;
+    for (int j = 0; j < 8; ++j) {
+      ctx->prof_cycles[j] += r.prof_cycles[j];
+      ctx->prof_count[j] += r.prof_count[j];
+    }
+  }
   if (out) {
     for (int64_t k = 0; k < n; ++k) {
       if (out->pair_attainment) out->pair_attainment[k] = res[static_cast<size_t>(k)].att;
@@ -477,6 +494,22 @@ const char* pdsim_gpu_last_error(const pdsim_gpu_ctx* ctx) { return ctx ? ctx->e
 int pdsim_gpu_set_stream(pdsim_gpu_ctx* ctx, void* stream) {
   if (int rc = check_ctx(ctx)) return rc;
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable) {
+  if (int rc = check_ctx(ctx)) return rc;
+  ctx->profiling = enable ? 1 : 0;
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles8, int64_t* counts8, int64_t* replayed) {
+  if (!ctx) return set_err(nullptr, PDSIM_ERR_CONFIG, "null context");
+  for (int j = 0; j < 8; ++j) {
+    if (cycles8) cycles8[j] = ctx->prof_cycles[j];
+    if (counts8) counts8[j] = ctx->prof_count[j];
+  }
+  if (replayed) *replayed = ctx->attempts2;
   return PDSIM_OK;
 }
 

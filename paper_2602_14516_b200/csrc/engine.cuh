@@ -381,8 +381,22 @@ struct PairResult {
   int64_t cycles;       // device clock64() ticks for this pair (0 on host)
   int64_t exact_folds;  // certified comparisons that fell back to a fold
   int32_t status;       // PDSIM_PAIR_*
-  int32_t reserved;
+  int32_t attempts;     // 1, or 2 when the lazy/search-mode attempt was replayed exactly
+  int64_t prof_cycles[8];  // optional per-phase SM cycles (kProf*), 0 unless profiling
+  int64_t prof_count[8];
 };
+
+// Per-phase instrumentation buckets (enabled by KernelArgs::profile).
+enum ProfBucket { kProfSelect = 0, kProfArrival, kProfInteraction, kProfWriteback, kProfDecodeStep,
+                  kProfLocalPrefill, kProfPrefillDone, kProfHistory };
+
+PDG_HD int64_t pdg_clock() {
+#if defined(__CUDA_ARCH__)
+  return clock64();
+#else
+  return 0;
+#endif
+}
 
 struct RouteOut {
   int32_t local;
@@ -435,6 +449,10 @@ struct EngState {
   int32_t failed_;
   int32_t nslots_;
   int32_t lazy_;   // lazy decode stepping enabled for this attempt
+  int32_t profile_;
+  int32_t attempts_;
+  int64_t prof_c_[8];
+  int64_t prof_n_[8];
   int32_t exact_itl_;  // per-session ITL means by sequential fold (records / retry)
   uint32_t cur_kind_;  // kind of the event being processed (catch-up tie rule)
   int32_t abort_;  // lazy attempt hit an ambiguous tie: replay exactly
@@ -467,8 +485,9 @@ class Engine {
  public:
   // `es` must point at this warp's EngState (shared memory on the device).
   PDG_HD Engine(EngState* es, const DevTrace& tr, const DevPlan& plan, const DevParams& prm, const Caps& caps,
-                const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed)
+                const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed, int profile = 0)
       : s_(es) {
+    s_->profile_ = profile;
     s_->T = tr;
     s_->PL = plan;
     s_->PR = prm;
@@ -486,6 +505,7 @@ class Engine {
     // and the pair is replayed with every step as an explicit event.
     for (int attempt = 0; attempt < 2; ++attempt) {
       init();
+      s_->attempts_ = attempt + 1;
       s_->lazy_ = attempt == 0 ? 1 : 0;
       s_->exact_itl_ = (attempt > 0 || s_->REC.sessions) ? 1 : 0;
       event_loop();
@@ -497,8 +517,20 @@ class Engine {
   PDG_HD void event_loop() {
     const int D = s_->PL.D, P = s_->PL.P;
     const int nslots = s_->nslots_;
+    const bool prof = s_->profile_ != 0;
+    int64_t tp = prof ? pdg_clock() : 0;
+    int bucket = -1;
     while (!s_->failed_ && !s_->abort_) {
       warp_sync();  // re-converge once per event (handlers store uniform values)
+      if (prof) {
+        const int64_t now_c = pdg_clock();
+        if (bucket >= 0) {
+          s_->prof_c_[bucket] += now_c - tp;
+          s_->prof_n_[bucket] += 1;
+        }
+        tp = now_c;
+        bucket = kProfSelect;
+      }
       // Next worker event: min over the slot table (lanes split the slots).
       double bt;
       uint64_t bk;
@@ -527,6 +559,7 @@ class Engine {
         const double t = s_->next_arr_t_;
         if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = s_->T.arrival[s_->next_arr_];
         s_->cur_kind_ = kArrival;
+        if (prof) prof_switch(&tp, &bucket, kProfArrival);
         advance_to(t);
         on_arrival(i);
         continue;
@@ -541,6 +574,9 @@ class Engine {
       s_->cur_kind_ = kind;
       ++s_->events_;
       advance_to(bt);
+      if (prof) prof_switch(&tp, &bucket, src == 1 ? (kind == kInteractionDone ? kProfInteraction : kProfWriteback)
+                                           : (static_cast<int>(bk & 63u) < D ? (kind == kDecodeStep ? kProfDecodeStep : kProfLocalPrefill)
+                                              : (static_cast<int>(bk & 63u) < D + P ? kProfPrefillDone : kProfHistory)));
       if (src == 1) {
         const HEv e = heap_pop();
         if (kind == kInteractionDone) {
@@ -566,6 +602,14 @@ class Engine {
     }
   }
 
+  PDG_HD void prof_switch(int64_t* tp, int* bucket, int next) {
+    const int64_t c = pdg_clock();
+    s_->prof_c_[*bucket] += c - *tp;
+    s_->prof_n_[*bucket] += 1;
+    *tp = c;
+    *bucket = next;
+  }
+
   PDG_HD void finish_result(PairResult* out) {
     for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += s_->SM.dw[d].kv_used;
     out->att = s_->att_;
@@ -576,6 +620,11 @@ class Engine {
     out->events = s_->events_;
     out->exact_folds = s_->folds_;
     out->status = s_->failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
+    out->attempts = s_->attempts_;
+    for (int j = 0; j < 8; ++j) {
+      out->prof_cycles[j] = s_->prof_c_[j];
+      out->prof_count[j] = s_->prof_n_[j];
+    }
   }
 
  private:
@@ -610,6 +659,10 @@ class Engine {
     s_->events_ = 0;
     s_->folds_ = 0;
     s_->ctr_.events_in_order = 1;
+    for (int j = 0; j < 8; ++j) {
+      s_->prof_c_[j] = 0;
+      s_->prof_n_[j] = 0;
+    }
     for (int j = lane_id(); j < kMaxSlots; j += PDG_NL) {
       s_->st_[j] = kInf;
       s_->sk_[j] = ~0ull;

@@ -56,6 +56,8 @@ def lib():
         L.pdsim_gpu_plan_search.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams),
                                             C.c_uint64, P(abi.SearchOutput)]
         L.pdsim_gpu_stage.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams)]
+        L.pdsim_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.pdsim_gpu_profile_counters.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.pdsim_gpu_search_staged.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, P(abi.SearchOutput)]
         L.pdsim_synth_spec_default.argtypes = [P(abi.SynthSpec)]
         L.pdsim_synth_profile.argtypes = [P(abi.SynthSpec), C.c_uint64, P(abi.Profile)]
@@ -252,6 +254,17 @@ class Context:
         self._check(lib().pdsim_gpu_plan_search(self._h, C.byref(inp), C.byref(profile), C.byref(params), seed,
                                                 C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
+
+    def set_profiling(self, enable):
+        self._check(lib().pdsim_gpu_set_profiling(self._h, 1 if enable else 0))
+
+    def profile_counters(self):
+        """(cycles[8], counts[8], replayed_pairs) of the last search."""
+        cy = (C.c_int64 * 8)()
+        n = (C.c_int64 * 8)()
+        rp = C.c_int64(0)
+        self._check(lib().pdsim_gpu_profile_counters(self._h, cy, n, C.byref(rp)))
+        return list(cy), list(n), rp.value
 
     def stage(self, traces, plans, profile, params):
         inp = search_input(traces, plans)

@@ -13,6 +13,10 @@ def main(cfg="C2"):
     with native.Context(0) as ctx:
         ctx.stage(wl.traces, wl.plans, wl.profile, wl.params)
         ctx.search_staged(wl.seed)
+        ctx.set_profiling(True)
+        ctx.search_staged(wl.seed)
+        prof = ctx.profile_counters()
+        ctx.set_profiling(False)
         t0 = time.time()
         res = ctx.search_staged(wl.seed)
         wall = time.time() - t0
@@ -23,7 +27,12 @@ def main(cfg="C2"):
     out = {"config": cfg, "kernel_ms": res.kernel_ms, "wall_s": wall, "pairs": res.n_pairs,
            "top": [{"cycles": c, "events": e, "ns_per_event_at_1.965GHz": c / 1.965 / max(e, 1), "pair": p,
                     "plan": s} for c, e, p, s in rows[:10]],
-           "total_events": sum(r[1] for r in rows), "total_cycles": sum(r[0] for r in rows)}
+           "total_events": sum(r[1] for r in rows), "total_cycles": sum(r[0] for r in rows),
+           "phases": {name: {"cycles": prof[0][k], "count": prof[1][k],
+                             "cycles_per": prof[0][k] / max(prof[1][k], 1)}
+                      for k, name in enumerate(["select", "arrival", "interaction", "writeback", "decode_step",
+                                                "local_prefill_done", "prefill_done", "history_read"])},
+           "replayed_pairs": prof[2]}
     print(json.dumps(out, indent=1))
 
 
