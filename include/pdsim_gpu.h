@@ -285,13 +285,18 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
                             int64_t pair_end, uint64_t seed,
                             pdsim_search_output* out);
 
-/* Diagnostics: per-phase SM-cycle instrumentation of the replay kernel
- * (buckets: 0 event selection, 1 arrival, 2 interaction done, 3 write-back,
- * 4 decode step, 5 local prefill done, 6 prefill compute done, 7 history
- * read), summed over the pairs of the last search; `replayed` counts pairs
- * whose fast attempt was replayed in exact mode. */
+/* Diagnostics: per-phase SM-cycle instrumentation of the replay kernel,
+ * PDSIM_PROF_BUCKETS buckets summed over the pairs of the last search.
+ * Exclusive handler phases: 0 event selection, 1 arrival, 2 interaction done,
+ * 3 write-back, 4 decode step, 5 local prefill done, 6 prefill compute done,
+ * 7 history read. Inclusive sub-scopes (nested inside the phases): 8 routing
+ * decision, 9 task enqueue, 10 lazy decode catch-up, 11 finishing-member
+ * fold, 12 advance_decode, 13 complete_task, 14 session-event heap,
+ * 15 queue dequeue (reorder). `replayed` counts pairs whose fast attempt was
+ * replayed in exact mode. */
+#define PDSIM_PROF_BUCKETS 16
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
-int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles8, int64_t* counts8,
+int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts,
                                int64_t* replayed);
 
 /* ---- host-side helpers (reference generators; host C++, libm) ------------ */

@@ -83,8 +83,8 @@ struct pdsim_gpu_ctx {
   DevBuf d_dec, d_ttft, d_sess;
   // diagnostics
   int profiling = 0;
-  int64_t prof_cycles[8] = {0};
-  int64_t prof_count[8] = {0};
+  int64_t prof_cycles[PDSIM_PROF_BUCKETS] = {0};
+  int64_t prof_count[PDSIM_PROF_BUCKETS] = {0};
   int64_t attempts2 = 0;
 };
 
@@ -133,13 +133,13 @@ struct KernelArgs {
 };
 
 // One warp per block; the warp replays pairs pulled from an atomic queue.
+template <bool kProf>
 __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
-  extern __shared__ __align__(16) char smem[];
   const int slot_id = blockIdx.x;
   pdg::GlobalSlot gslot;
   pdg::global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
   pdg::SmemSlot sslot;
-  pdg::smem_slot_bytes(a.caps, &sslot, smem);
+  pdg::smem_slot_bytes(a.caps, &sslot, pdg::pdg_smem);  // EngState first (engine.cuh)
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long ticket = 0;
@@ -158,8 +158,13 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, a.profile);
-      eng.run(&res);
+      if (kProf) {
+        pdg::EngineT<true> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, 1);
+        eng.run(&res);
+      } else {
+        pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, 0);
+        eng.run(&res);
+      }
       res.cycles = clock64() - t0;
     }
     if (lane == 0) {
@@ -373,9 +378,11 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   int64_t launches = 0;
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
-    CU(ctx, cudaFuncSetAttribute(replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(ctx->smem_bytes)));
-    replay_kernel<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
+    // The diagnostics build (per-phase clock64 counters) is a separate
+    // instantiation so the product kernel carries no instrumentation.
+    void (*kern)(KernelArgs) = ctx->profiling ? replay_kernel<true> : replay_kernel<false>;
+    CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
+    kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;
     CU(ctx, cudaGetLastError());
   }
@@ -406,12 +413,12 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   CU(ctx, cudaEventElapsedTime(&d_ms, ctx->ev[0], ctx->ev[3]));
 
   bool engine_error = false;
-  for (int j = 0; j < 8; ++j) ctx->prof_cycles[j] = ctx->prof_count[j] = 0;
+  for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) ctx->prof_cycles[j] = ctx->prof_count[j] = 0;
   ctx->attempts2 = 0;
   for (const auto& r : res) {
     engine_error |= r.status == PDSIM_PAIR_ERROR;
     ctx->attempts2 += r.attempts > 1 ? 1 : 0;
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
       ctx->prof_cycles[j] += r.prof_cycles[j];
       ctx->prof_count[j] += r.prof_count[j];
     }
@@ -503,11 +510,11 @@ int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable) {
   return PDSIM_OK;
 }
 
-int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles8, int64_t* counts8, int64_t* replayed) {
+int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts, int64_t* replayed) {
   if (!ctx) return set_err(nullptr, PDSIM_ERR_CONFIG, "null context");
-  for (int j = 0; j < 8; ++j) {
-    if (cycles8) cycles8[j] = ctx->prof_cycles[j];
-    if (counts8) counts8[j] = ctx->prof_count[j];
+  for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
+    if (cycles) cycles[j] = ctx->prof_cycles[j];
+    if (counts) counts[j] = ctx->prof_count[j];
   }
   if (replayed) *replayed = ctx->attempts2;
   return PDSIM_OK;

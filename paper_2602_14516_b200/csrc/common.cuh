@@ -67,6 +67,31 @@ PDG_HD double bitsd(uint64_t u) {
 #endif
 }
 
+// ---- exact integer helpers without the u64 division subroutine ----
+// floor(a / d) for a < 2^53, 1 <= d < 2^53: the correctly rounded fp64
+// quotient is n or n + 1 (rounding is monotonic and n is representable);
+// one exact integer check fixes it.
+PDG_HD uint64_t udiv53(uint64_t a, uint64_t d) {
+#if defined(__CUDA_ARCH__)
+  uint64_t q = static_cast<uint64_t>(__ddiv_rz(static_cast<double>(a), static_cast<double>(d)));
+  if (q * d > a) --q;
+  return q;
+#else
+  return a / d;
+#endif
+}
+// x mod m for 2 <= m < 2^16 (the routing scan's `rng() % (i + 1)`,
+// coordinator.cpp:124-130), from three 32-bit remainders.
+PDG_HD uint32_t umod64_small(uint64_t x, uint32_t m) {
+#if defined(__CUDA_ARCH__)
+  const uint32_t hi = static_cast<uint32_t>(x >> 32), lo = static_cast<uint32_t>(x);
+  const uint32_t c = (0xffffffffu % m + 1u) % m;  // 2^32 mod m
+  return ((hi % m) * c + lo % m) % m;
+#else
+  return static_cast<uint32_t>(x % m);
+#endif
+}
+
 // ---- std::mt19937_64 (the reference's engine for routing scan order,
 // coordinator.hpp:84, coordinator.cpp:124-130, and for trace/profile
 // generation, workload.cpp:32-74, perf_model.cpp:36-39). Parameters are the

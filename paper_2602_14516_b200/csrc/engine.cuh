@@ -50,6 +50,36 @@ namespace pdg {
 #define PDG_NL 1
 #endif
 
+// Address-space hints. Engine state lives in shared memory and the workspace
+// in global memory, but the pointers to them are stored in (shared) engine
+// state, which makes them generic; generic loads are tracked on the long
+// scoreboard and pay an extra address-space check. The hints let ptxas emit
+// LDS/LDG instead.
+#if defined(__CUDACC__)
+extern __shared__ __align__(16) char pdg_smem[];
+#endif
+#if defined(__CUDA_ARCH__)
+template <class T>
+__device__ __forceinline__ T* SHP(T* p) {
+  __builtin_assume(__isShared(p));
+  return p;
+}
+template <class T>
+__device__ __forceinline__ T* GLP(T* p) {
+  __builtin_assume(__isGlobal(p));
+  return p;
+}
+#else
+template <class T>
+inline T* SHP(T* p) {
+  return p;
+}
+template <class T>
+inline T* GLP(T* p) {
+  return p;
+}
+#endif
+
 constexpr int kMaxSlots = 64;
 constexpr int kSlotsPerLane = kMaxSlots / PDG_NL;
 constexpr double kInf = __builtin_huge_val();
@@ -382,13 +412,16 @@ struct PairResult {
   int64_t exact_folds;  // certified comparisons that fell back to a fold
   int32_t status;       // PDSIM_PAIR_*
   int32_t attempts;     // 1, or 2 when the lazy/search-mode attempt was replayed exactly
-  int64_t prof_cycles[8];  // optional per-phase SM cycles (kProf*), 0 unless profiling
-  int64_t prof_count[8];
+  int64_t prof_cycles[PDSIM_PROF_BUCKETS];  // optional per-phase SM cycles (kProf*), 0 unless profiling
+  int64_t prof_count[PDSIM_PROF_BUCKETS];
 };
 
 // Per-phase instrumentation buckets (enabled by KernelArgs::profile).
 enum ProfBucket { kProfSelect = 0, kProfArrival, kProfInteraction, kProfWriteback, kProfDecodeStep,
-                  kProfLocalPrefill, kProfPrefillDone, kProfHistory };
+                  kProfLocalPrefill, kProfPrefillDone, kProfHistory,
+                  // inclusive sub-scopes
+                  kProfRoute, kProfEnqueue, kProfCatchUp, kProfFinisher, kProfAdvance, kProfComplete,
+                  kProfHeap, kProfDequeue };
 
 PDG_HD int64_t pdg_clock() {
 #if defined(__CUDA_ARCH__)
@@ -451,8 +484,8 @@ struct EngState {
   int32_t lazy_;   // lazy decode stepping enabled for this attempt
   int32_t profile_;
   int32_t attempts_;
-  int64_t prof_c_[8];
-  int64_t prof_n_[8];
+  int64_t prof_c_[PDSIM_PROF_BUCKETS];
+  int64_t prof_n_[PDSIM_PROF_BUCKETS];
   int32_t exact_itl_;  // per-session ITL means by sequential fold (records / retry)
   uint32_t cur_kind_;  // kind of the event being processed (catch-up tie rule)
   int32_t abort_;  // lazy attempt hit an ambiguous tie: replay exactly
@@ -481,12 +514,26 @@ inline const pdsim_profile*& host_profile() {  // host (test) builds only
 
 static_assert(sizeof(EngState) <= kEngStateBytes, "EngState outgrew its shared-memory reservation");
 
-class Engine {
+#if defined(__CUDA_ARCH__)
+#define s_ (reinterpret_cast<EngState*>(pdg_smem))
+#endif
+
+// kProf compiles in the per-phase clock64 instrumentation (diagnostics
+// kernel only); the product kernel is EngineT<false>.
+template <bool kProf>
+class EngineT {
  public:
   // `es` must point at this warp's EngState (shared memory on the device).
-  PDG_HD Engine(EngState* es, const DevTrace& tr, const DevPlan& plan, const DevParams& prm, const Caps& caps,
+  // On the device `es` must be the EngState at the start of the block's
+  // dynamic shared memory (one warp per block): the engine addresses it
+  // directly from the shared-memory base, so `this` carries no state.
+  PDG_HD EngineT(EngState* es, const DevTrace& tr, const DevPlan& plan, const DevParams& prm, const Caps& caps,
                 const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed, int profile = 0)
-      : s_(es) {
+#if !defined(__CUDA_ARCH__)
+      : s_(es)
+#endif
+  {
+    (void)es;
     s_->profile_ = profile;
     s_->T = tr;
     s_->PL = plan;
@@ -517,7 +564,7 @@ class Engine {
   PDG_HD void event_loop() {
     const int D = s_->PL.D, P = s_->PL.P;
     const int nslots = s_->nslots_;
-    const bool prof = s_->profile_ != 0;
+    constexpr bool prof = kProf;
     int64_t tp = prof ? pdg_clock() : 0;
     int bucket = -1;
     while (!s_->failed_ && !s_->abort_) {
@@ -538,9 +585,9 @@ class Engine {
       next_slot_event(nslots, &bt, &bk, &slot_tie);
       int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
       if (s_->hn_ > 0) {
-        const HEv* h = heap_base();
-        const double ht = h[0].t;
-        const uint64_t hk = h[0].key;
+        double ht;
+        uint64_t hk;
+        heap_top(&ht, &hk);
         if (src < 0 || before(ht, hk, bt, bk)) {
           bt = ht;
           bk = hk;
@@ -557,7 +604,7 @@ class Engine {
       if (src == 2) {
         const int32_t i = s_->next_arr_++;
         const double t = s_->next_arr_t_;
-        if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = s_->T.arrival[s_->next_arr_];
+        if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = GLP(s_->T.arrival)[s_->next_arr_];
         s_->cur_kind_ = kArrival;
         if (prof) prof_switch(&tp, &bucket, kProfArrival);
         advance_to(t);
@@ -602,6 +649,15 @@ class Engine {
     }
   }
 
+  // Inclusive sub-scope timers (no code unless kProf).
+  PDG_HD int64_t pb() const { return kProf ? pdg_clock() : 0; }
+  PDG_HD void pe(int k, int64_t t0) {
+    if (kProf) {
+      s_->prof_c_[k] += pdg_clock() - t0;
+      s_->prof_n_[k] += 1;
+    }
+  }
+
   PDG_HD void prof_switch(int64_t* tp, int* bucket, int next) {
     const int64_t c = pdg_clock();
     s_->prof_c_[*bucket] += c - *tp;
@@ -611,7 +667,7 @@ class Engine {
   }
 
   PDG_HD void finish_result(PairResult* out) {
-    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += s_->SM.dw[d].kv_used;
+    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += SHP(s_->SM.dw)[d].kv_used;
     out->att = s_->att_;
     out->att.sessions_total = s_->T.S;
     out->ctr = s_->ctr_;
@@ -621,14 +677,16 @@ class Engine {
     out->exact_folds = s_->folds_;
     out->status = s_->failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
     out->attempts = s_->attempts_;
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
       out->prof_cycles[j] = s_->prof_c_[j];
       out->prof_count[j] = s_->prof_n_[j];
     }
   }
 
  private:
+#if !defined(__CUDA_ARCH__)
   EngState* s_;
+#endif
 
   PDG_HD void fail() { s_->failed_ = 1; }
 
@@ -643,7 +701,7 @@ class Engine {
     s_->hn_ = 0;
     s_->heap_spilled_ = false;
     s_->next_arr_ = 0;
-    s_->next_arr_t_ = s_->T.S > 0 ? s_->T.arrival[0] : 0.0;
+    s_->next_arr_t_ = s_->T.S > 0 ? GLP(s_->T.arrival)[0] : 0.0;
     s_->adm_head_ = 0;
     s_->rr_next_ = 0;
     s_->ctr_.events_in_order = 1;
@@ -659,7 +717,7 @@ class Engine {
     s_->events_ = 0;
     s_->folds_ = 0;
     s_->ctr_.events_in_order = 1;
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
       s_->prof_c_[j] = 0;
       s_->prof_n_[j] = 0;
     }
@@ -669,9 +727,9 @@ class Engine {
     }
     {  // warp-uniform stores (every lane writes the same values)
       uint32_t idx;
-      mt64_seed(s_->SM.mt, &idx, s_->seed_);
+      mt64_seed(SHP(s_->SM.mt), &idx, s_->seed_);
       for (int p = 0; p < s_->PL.P; ++p) {
-        PrefillW& w = s_->SM.pw[p];
+        PrefillW& w = SHP(s_->SM.pw)[p];
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.tw.tail.clear();
@@ -683,7 +741,7 @@ class Engine {
         w.staged_ready = 0.0;
       }
       for (int d = 0; d < s_->PL.D; ++d) {
-        DecodeW& w = s_->SM.dw[d];
+        DecodeW& w = SHP(s_->SM.dw)[d];
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.sg.pfx.clear();
@@ -731,9 +789,9 @@ class Engine {
     return curve_eval(PDG_PROF.kv[src][dst], static_cast<double>(l));
   }
 
-  PDG_HD int32_t l_incr_of(int32_t i) const { return s_->T.incr[s_->T.round_off[i] + s_->G.sess[i].round - 1]; }
+  PDG_HD int32_t l_incr_of(int32_t i) const { return GLP(s_->T.incr)[GLP(s_->T.round_off)[i] + GLP(s_->G.sess)[i].round - 1]; }
   PDG_HD double created_of(int32_t i) const {
-    return s_->G.sess[i].round == 1 ? s_->T.arrival[i] : s_->G.sess[i].t_enq;  // sim_engine.cpp:258, 283, 588
+    return GLP(s_->G.sess)[i].round == 1 ? GLP(s_->T.arrival)[i] : GLP(s_->G.sess)[i].t_enq;  // sim_engine.cpp:258, 283, 588
   }
 
   // ---- RNG (coordinator.cpp:124-130): std::mt19937_64 in shared memory ----
@@ -743,7 +801,7 @@ class Engine {
       // Warp-parallel twist in three dependency phases: elements below 156
       // read only old words; 156..310 read updated words i-156; 311 reads
       // updated words 0 and 155.
-      uint64_t* mt = s_->SM.mt;
+      uint64_t* mt = SHP(s_->SM.mt);
       const int lane = lane_id();
       for (int base = 0; base < 156; base += 32) {
         const int i = base + lane;
@@ -775,11 +833,11 @@ class Engine {
         __syncwarp();
       }
 #else
-      mt64_twist(s_->SM.mt);
+      mt64_twist(SHP(s_->SM.mt));
 #endif
       s_->mt_idx_ = 0;
     }
-    return mt64_temper(s_->SM.mt[s_->mt_idx_++]);
+    return mt64_temper(SHP(s_->SM.mt)[s_->mt_idx_++]);
   }
 
   // ---- worker-event slots (registers) ----
@@ -855,15 +913,34 @@ class Engine {
 
   // ---- session-event heap (shared memory, global spill) ----
   PDG_HD HEv* heap_base() const { return s_->heap_spilled_ ? s_->G.heap : s_->SM.heap; }
+  // Earliest session event (requires hn_ > 0).
+  PDG_HD void heap_top(double* t, uint64_t* key) const {
+    if (s_->heap_spilled_) {
+      const HEv* h = GLP(s_->G.heap);
+      *t = h[0].t;
+      *key = h[0].key;
+    } else {
+      const HEv* h = SHP(s_->SM.heap);
+      *t = h[0].t;
+      *key = h[0].key;
+    }
+  }
 
   PDG_HD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
+    const int64_t t0 = pb();
+    heap_push_(t, kind, a, b);
+    pe(kProfHeap, t0);
+  }
+  PDG_HD void heap_push_(double t, uint32_t kind, uint32_t a, uint32_t b) {
     HEv e;
     e.t = t;
     e.key = mk_key(kind, s_->seq_++, 0);
     e.a = a;
     e.b = b;
     if (!s_->heap_spilled_ && s_->hn_ >= s_->C.hs) {
-      for (int k = lane_id(); k < s_->hn_; k += PDG_NL) s_->G.heap[k] = s_->SM.heap[k];
+      HEv* gh = GLP(s_->G.heap);
+      const HEv* sh = SHP(s_->SM.heap);
+      for (int k = lane_id(); k < s_->hn_; k += PDG_NL) gh[k] = sh[k];
       warp_sync();
       s_->heap_spilled_ = true;
     }
@@ -871,8 +948,14 @@ class Engine {
       fail();
       return;
     }
-    HEv* h = heap_base();
-    int32_t i = s_->hn_++;
+    const int32_t n = s_->hn_++;
+    if (s_->heap_spilled_) {
+      heap_sift_up(GLP(s_->G.heap), n, e);
+    } else {
+      heap_sift_up(SHP(s_->SM.heap), n, e);
+    }
+  }
+  PDG_HD static void heap_sift_up(HEv* h, int32_t i, const HEv& e) {
     while (i > 0) {
       const int32_t par = (i - 1) >> 1;
       const HEv pe = h[par];
@@ -884,15 +967,27 @@ class Engine {
   }
 
   PDG_HD HEv heap_pop() {
-    HEv* h = heap_base();
+    const int64_t t0 = pb();
+    const HEv top = heap_pop_();
+    pe(kProfHeap, t0);
+    return top;
+  }
+  PDG_HD HEv heap_pop_() {
+    const int32_t n = --s_->hn_;
+    const HEv top = s_->heap_spilled_ ? heap_sift_down(GLP(s_->G.heap), n) : heap_sift_down(SHP(s_->SM.heap), n);
+    if (n == 0) s_->heap_spilled_ = false;
+    return top;
+  }
+  // Removes h[0] from a heap that now holds n entries (h[n] is the last).
+  PDG_HD static HEv heap_sift_down(HEv* h, int32_t n) {
     const HEv top = h[0];
-    const HEv last = h[--s_->hn_];
+    const HEv last = h[n];
     int32_t i = 0;
     for (;;) {
       int32_t c = 2 * i + 1;
-      if (c >= s_->hn_) break;
+      if (c >= n) break;
       HEv ce = h[c];
-      if (c + 1 < s_->hn_) {
+      if (c + 1 < n) {
         const HEv c2 = h[c + 1];
         if (before(c2.t, c2.key, ce.t, ce.key)) {
           ++c;
@@ -904,9 +999,8 @@ class Engine {
       i = c;
     }
     warp_sync();
-    if (s_->hn_ > 0 && lane_id() == 0) h[i] = last;
+    if (n > 0 && lane_id() == 0) h[i] = last;
     warp_sync();
-    if (s_->hn_ == 0) s_->heap_spilled_ = false;
     return top;
   }
 
@@ -920,9 +1014,9 @@ class Engine {
   PDG_HD int bind_session() {  // least KV bytes, lowest index on ties
     if (s_->lazy_) catch_up(s_->now_, s_->cur_kind_);
     int best = 0;
-    int64_t bv = s_->SM.dw[0].kv_used;
+    int64_t bv = SHP(s_->SM.dw)[0].kv_used;
     for (int d = 1; d < s_->PL.D; ++d) {
-      const int64_t v = s_->SM.dw[d].kv_used;
+      const int64_t v = SHP(s_->SM.dw)[d].kv_used;
       if (v < bv) {
         bv = v;
         best = d;
@@ -933,10 +1027,10 @@ class Engine {
 
   PDG_COLD bool try_admit(int32_t i) {
     const int best = bind_session();
-    const DecodeW& w = s_->SM.dw[best];
-    const int64_t first = static_cast<int64_t>(s_->T.incr[s_->T.round_off[i]]) * PDG_PROF.kv_bytes_per_token;
+    const DecodeW& w = SHP(s_->SM.dw)[best];
+    const int64_t first = static_cast<int64_t>(GLP(s_->T.incr)[GLP(s_->T.round_off)[i]]) * PDG_PROF.kv_bytes_per_token;
     if (w.kv_used + first > w.kv_cap) return false;
-    SessRt& s = s_->G.sess[i];
+    SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.bound = static_cast<int8_t>(best);
       s.bind_time = s_->now_;
@@ -960,18 +1054,20 @@ class Engine {
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
   PDG_COLD void start_round(int32_t i, int round, int bound, int32_t ctx) {
-    SessRt& s = s_->G.sess[i];
+    SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.t_enq = s_->now_;
       s.postpone = 0;
     }
     ++s_->ctr_.tasks_created;
-    const int32_t incr = s_->T.incr[s_->T.round_off[i] + round - 1];
+    const int32_t incr = GLP(s_->T.incr)[GLP(s_->T.round_off)[i] + round - 1];
+    const int64_t tr0 = pb();
     const RouteOut r = decide(i, bound, ctx, incr);
+    pe(kProfRoute, tr0);
     if (s_->REC.decisions && lane_id() == 0) {
       pdsim_decision& d = s_->REC.decisions[s_->n_dec_];
       d.time = s_->now_;
-      d.session_id = s_->T.sid[i];
+      d.session_id = GLP(s_->T.sid)[i];
       d.round = round;
       d.worker = r.local ? s_->PL.P + bound : r.p;
       d.local = static_cast<int8_t>(r.local);
@@ -981,11 +1077,13 @@ class Engine {
       d.estimated_cost = r.has_est ? r.est : 0.0;
     }
     ++s_->n_dec_;
+    const int64_t te0 = pb();
     if (r.local) {
       enqueue_local(bound, i, ctx, incr);
     } else {
       enqueue_remote(r.p, i, ctx, incr);
     }
+    pe(kProfEnqueue, te0);
   }
 
   PDG_HD RouteOut decide(int32_t i, int bound, int32_t ctx, int32_t incr) {
@@ -1017,12 +1115,12 @@ class Engine {
   PDG_COLD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
     const int n = s_->PL.P;
     if (n > 0) {
-      int32_t* order = s_->SM.order;
+      int32_t* order = SHP(s_->SM.order);
       {  // warp-uniform stores (every lane writes the same values)
         for (int k = 0; k < n; ++k) order[k] = k;
       }
       for (int k = n - 1; k > 0; --k) {
-        const int j = static_cast<int>(rng_next() % static_cast<uint64_t>(k + 1));
+        const int j = static_cast<int>(umod64_small(rng_next(), static_cast<uint32_t>(k + 1)));
         const int a = order[k], b = order[j];
         {  // warp-uniform stores (every lane writes the same values)
           order[k] = b;
@@ -1062,11 +1160,11 @@ class Engine {
   PDG_HD void estimate(int d, int32_t ctx, int32_t incr, int c, bool force_exact, double* lo, double* hi,
                        bool* exact) const {
     if (c < 0) {
-      const DecodeW& w = s_->SM.dw[d];
+      const DecodeW& w = SHP(s_->SM.dw)[d];
       const uint32_t len = w.q.qt - w.q.qh;
       const double own = t_prefill(ctx, incr, w.deg);
       if (force_exact || len <= 2 || !w.q.sum.exact()) {
-        *lo = *hi = fold_queue(w.q, s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, own);
+        *lo = *hi = fold_queue(w.q, GLP(s_->G.dq_c) + static_cast<size_t>(d) * s_->C.qcap, own);
         *exact = true;
         return;
       }
@@ -1077,12 +1175,12 @@ class Engine {
       *exact = false;
       return;
     }
-    const PrefillW& w = s_->SM.pw[c];
-    const int pd = w.deg, dd = s_->SM.dw[d].deg;
+    const PrefillW& w = SHP(s_->SM.pw)[c];
+    const int pd = w.deg, dd = SHP(s_->SM.dw)[d].deg;
     const uint32_t len = w.q.qt - w.q.qh;
     const double head = dadd(t_prefill(ctx, incr, pd), dadd(t_kv(ctx, dd, pd), t_kv(incr, pd, dd)));
     if (force_exact || len <= 2 || !w.q.sum.exact()) {
-      *lo = *hi = dadd(head, fold_queue(w.q, s_->G.pq_c + static_cast<size_t>(c) * s_->C.qcap, 0.0));
+      *lo = *hi = dadd(head, fold_queue(w.q, GLP(s_->G.pq_c) + static_cast<size_t>(c) * s_->C.qcap, 0.0));
       *exact = true;
       return;
     }
@@ -1215,18 +1313,18 @@ class Engine {
   }
 
   PDG_HD void ttft_add(int p, double v) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
-    if (!window_room(w.tw, s_->G.tw_t + base, static_cast<uint32_t>(s_->C.twcap), s_->now_)) return;
+    if (!window_room(w.tw, GLP(s_->G.tw_t) + base, static_cast<uint32_t>(s_->C.twcap), s_->now_)) return;
     const uint32_t k = w.tw.end & mask;
     const Pfx cur = w.tw.tail;
     Pfx next = cur;
     next.add(v, 1);
     {  // warp-uniform stores (every lane writes the same values)
-      s_->G.tw_t[base + k] = s_->now_;
-      s_->G.tw_v[base + k] = v;
-      s_->G.tw_p[base + k] = cur;
+      GLP(s_->G.tw_t)[base + k] = s_->now_;
+      GLP(s_->G.tw_v)[base + k] = v;
+      GLP(s_->G.tw_p)[base + k] = cur;
       w.tw.tail = next;
       ++w.tw.end;
     }
@@ -1234,26 +1332,26 @@ class Engine {
 
   // query(now) <= thr with the sequential windowed mean's semantics.
   PDG_HD bool ttft_has_slack(int p, double thr) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
-    window_trim(w.tw, s_->G.tw_t + base, mask, s_->now_);
+    window_trim(w.tw, GLP(s_->G.tw_t) + base, mask, s_->now_);
     const uint32_t head = w.tw.head, end = w.tw.end;
     if (head == end) return 0.0 <= thr;  // an empty window reads 0
-    const Pfx hp = s_->G.tw_p[base + (head & mask)];
+    const Pfx hp = GLP(s_->G.tw_p)[base + (head & mask)];
     const int dec = window_mean_le(w.tw.tail, hp, thr);
     if (dec >= 0) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
-    for (uint32_t k = head; k != end; ++k) sum = dadd(sum, s_->G.tw_v[base + (k & mask)]);
+    for (uint32_t k = head; k != end; ++k) sum = dadd(sum, GLP(s_->G.tw_v)[base + (k & mask)]);
     return ddiv(sum, static_cast<double>(end - head)) <= thr;
   }
 
   // ---- step-segment log: ITL window + per-session ITL folds ----
-  PDG_HD Seg* seg_ring(int d) const { return s_->G.seg + static_cast<size_t>(d) * s_->C.segcap; }
+  PDG_HD Seg* seg_ring(int d) const { return GLP(s_->G.seg) + static_cast<size_t>(d) * s_->C.segcap; }
   // Segment i of worker d (i == seg_end is the open one, in shared memory).
   PDG_HD Seg seg_at(int d, int32_t i) const {
-    const DecodeW& w = s_->SM.dw[d];
+    const DecodeW& w = SHP(s_->SM.dw)[d];
     if (i == w.seg_end) return w.sg;
     return seg_ring(d)[static_cast<uint32_t>(i) & static_cast<uint32_t>(s_->C.segcap - 1)];
   }
@@ -1273,7 +1371,7 @@ class Engine {
   // Appends n consecutive steps (first index `first`, first end time t0,
   // each with ITL gap `gap` and `cnt` ITL samples) to worker d's log.
   PDG_HD void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     if (w.sg.n > 0 && gap == w.sg.gap && cnt == w.sg.cnt && first == w.sg.first + w.sg.n) {
       w.sg.n = w.sg.n + n;  // extends the open segment (t0 continues the progression)
       return;
@@ -1315,7 +1413,7 @@ class Engine {
   // Frees ring slots no longer needed: behind the ITL window head and before
   // any step an active round can still fold (rounds span <= maxdec steps).
   PDG_HD void seg_reclaim(int d, int32_t cur_step) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const int32_t oldest_needed = cur_step - s_->C.maxdec - 1;
     int32_t keep = w.seg_keep;
     while (keep < w.seg_head && keep < w.seg_end) {
@@ -1329,7 +1427,7 @@ class Engine {
   // Advances the ITL window head past steps that ended at or before
   // now - window (coordinator.cpp:32-40: the interval is (now - w, now]).
   PDG_HD void seg_trim(int d, double now) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const double cutoff = dsub(now, s_->PR.stat_window);
     int32_t h = w.seg_head, off = w.seg_off;
     for (;;) {
@@ -1368,7 +1466,7 @@ class Engine {
   PDG_HD bool itl_has_slack(int d, double thr) {
     if (s_->lazy_) catch_up_worker(d, s_->now_, s_->cur_kind_);
     seg_trim(d, s_->now_);
-    const DecodeW& w = s_->SM.dw[d];
+    const DecodeW& w = SHP(s_->SM.dw)[d];
     const Pfx tail = tail_pfx(w);
     const Seg h = seg_at(d, w.seg_head);
     Pfx head = h.pfx;
@@ -1404,7 +1502,7 @@ class Engine {
   // Step k is in the open segment; the segment holding j0 is at or after
   // `hint` (the open-segment index when the round joined).
   PDG_HD ufx_t seg_sum(int d, int32_t j0, int32_t k, int32_t hint, int32_t* inex) {
-    const DecodeW& w = s_->SM.dw[d];
+    const DecodeW& w = SHP(s_->SM.dw)[d];
     if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
       fail();
       *inex = 0;
@@ -1419,19 +1517,48 @@ class Engine {
     const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
     ufx_t pj = 0;
     int32_t ij = 0;
-    for (int32_t i = hint; i <= w.seg_end; ++i) {
-      const Seg& g = i == w.seg_end ? w.sg : ring[static_cast<uint32_t>(i) & mask];
-      if (j0 < g.first + g.n) {
-        const int32_t nj = j0 - g.first + 1;  // >= 0 (j0 >= g.first - 1)
-        fx_t f;
-        to_fx(g.gap, &f);
-        pj = g.p1 + static_cast<ufx_t>(f) * static_cast<ufx_t>(static_cast<uint32_t>(nj < 0 ? 0 : nj));
-        ij = g.inex1 + (g.gx ? 0 : (nj < 0 ? 0 : nj));
-        break;
-      }
+    const int32_t gi = seg_find(d, j0, hint);
+    if (gi >= 0) {
+      const Seg& g = gi == w.seg_end ? w.sg : ring[static_cast<uint32_t>(gi) & mask];
+      const int32_t nj = j0 - g.first + 1;  // >= 0 (j0 >= g.first - 1)
+      fx_t f;
+      to_fx(g.gap, &f);
+      pj = g.p1 + static_cast<ufx_t>(f) * static_cast<ufx_t>(static_cast<uint32_t>(nj < 0 ? 0 : nj));
+      ij = g.inex1 + (g.gx ? 0 : (nj < 0 ? 0 : nj));
     }
     *inex = ik - ij;
     return pk - pj;
+  }
+
+  // Index of the first segment at or after `hint` that holds step j (i.e.
+  // j < first + n; the open segment has index seg_end), or -1. Segments are
+  // ordered by first step; lanes test 32 candidates per ballot.
+  PDG_HD int32_t seg_find(int d, int32_t j, int32_t hint) const {
+    const DecodeW& w = SHP(s_->SM.dw)[d];
+    const int32_t end = w.seg_end;
+    const Seg* ring = seg_ring(d);
+    const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
+#if defined(__CUDA_ARCH__)
+    for (int32_t base = hint; base <= end; base += 32) {
+      const int32_t i = base + lane_id();
+      bool hit = false;
+      if (i < end) {
+        const Seg& g = ring[static_cast<uint32_t>(i) & mask];
+        hit = j < g.first + g.n;
+      } else if (i == end) {
+        hit = j < w.sg.first + w.sg.n;
+      }
+      const uint32_t b = ballot(hit);
+      if (b) return base + __ffs(b) - 1;
+    }
+    return -1;
+#else
+    for (int32_t i = hint; i <= end; ++i) {
+      const Seg& g = i == end ? w.sg : ring[static_cast<uint32_t>(i) & mask];
+      if (j < g.first + g.n) return i;
+    }
+    return -1;
+#endif
   }
 
   // Sequential fold of the ITL gaps of steps [a, k] of worker d onto s
@@ -1439,7 +1566,7 @@ class Engine {
   // `hint` is the open-segment index when the round joined: the segment
   // holding step a is at or after it.
   PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s, int32_t hint) {
-    const DecodeW& w = s_->SM.dw[d];
+    const DecodeW& w = SHP(s_->SM.dw)[d];
     if (a > k) return s;
     if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
       fail();
@@ -1447,7 +1574,9 @@ class Engine {
     }
     const Seg* ring = seg_ring(d);
     const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
-    for (int32_t i = hint; i <= w.seg_end; ++i) {
+    const int32_t from = seg_find(d, a, hint);
+    if (from < 0) return s;
+    for (int32_t i = from; i <= w.seg_end; ++i) {
       const Seg& g = i == w.seg_end ? w.sg : ring[static_cast<uint32_t>(i) & mask];
       const int32_t gfirst = g.first, gn = g.n;
       const int32_t lo = a > gfirst ? a : gfirst;
@@ -1489,6 +1618,12 @@ class Engine {
 
   // Dequeues the next task (after reordering the head window).
   PDG_HD int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
+    const int64_t t0 = pb();
+    const int32_t i = select_next_(q, qs, qc, cost);
+    pe(kProfDequeue, t0);
+    return i;
+  }
+  PDG_HD int32_t select_next_(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
     const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     const uint32_t qh = q.qh;
     if (s_->PR.reorder) {
@@ -1500,7 +1635,7 @@ class Engine {
     *cost = qc[qh & mask];
     ExactSum ns = q.sum;
     ns.remove(*cost);
-    const int32_t pc = s_->G.sess[i].postpone;
+    const int32_t pc = GLP(s_->G.sess)[i].postpone;
     {  // warp-uniform stores (every lane writes the same values)
       q.sum = ns;
       q.qh = qh + 1;
@@ -1514,6 +1649,91 @@ class Engine {
   // lexicographically first permutation with the maximum count among the
   // allowed ones (the identity is always allowed); capped tasks cannot be
   // pushed back (reorder.cpp:93-138). Lanes evaluate permutations in parallel.
+#if defined(__CUDA_ARCH__)
+  // Device form: lane k holds queued task k (session, cost, wait, postpone
+  // count) in registers; permutations are packed 4 bits per position and
+  // read the task fields with shuffles, so nothing goes to local memory.
+  // Lanes scan ranks base+lane in warp-uniform rounds; one REDUX.MAX over
+  // (count << 16 | ~rank) picks the largest count, ties to the smallest rank
+  // (the identity, rank 0, wins every tie: strict improvements only).
+  PDG_COLD void reorder_head(int32_t* qs, double* qc, uint32_t qh, int m) {
+    const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
+    const int lane = lane_id();
+    int32_t ms = 0;
+    double mc = 0.0, mw = 0.0;
+    int mp = 0;
+    if (lane < m) {
+      ms = qs[(qh + lane) & mask];
+      mc = qc[(qh + lane) & mask];
+      const SessRt& s = GLP(s_->G.sess)[ms];
+      mw = dsub(s_->now_, s.t_enq);
+      mp = s.postpone;
+    }
+    const double thres = s_->T.ttft_thres;
+    int id_sat = 0;
+    {
+      double el = 0.0;
+      for (int k = 0; k < m; ++k) {
+        el = dadd(el, shfl_d(mc, k));
+        if (dadd(shfl_d(mw, k), el) <= thres) ++id_sat;
+      }
+    }
+    if (id_sat == m) return;  // the identity already satisfies every task
+    const uint32_t capped = ballot(lane < m && mp >= s_->PR.window);
+    uint32_t nperm = 1;
+    for (int k = 2; k <= m; ++k) nperm *= static_cast<uint32_t>(k);
+    uint32_t best = (static_cast<uint32_t>(id_sat) << 16) | 0xffffu;
+    for (uint32_t base = 0; base < nperm; base += 32) {
+      const uint32_t r = base + static_cast<uint32_t>(lane);
+      const bool valid = r >= 1 && r < nperm;
+      const uint32_t pk = unrank_packed(valid ? r : 0u, m);
+      bool allowed = valid;
+      double el = 0.0;
+      int sat = 0;
+      for (int k = 0; k < m; ++k) {
+        const int p = static_cast<int>((pk >> (4 * k)) & 15u);
+        if (k > p && ((capped >> p) & 1u)) allowed = false;
+        el = dadd(el, shfl_d(mc, p));
+        if (dadd(shfl_d(mw, p), el) <= thres) ++sat;
+      }
+      if (allowed) {
+        const uint32_t key = (static_cast<uint32_t>(sat) << 16) | (0xffffu - r);
+        if (key > best) best = key;
+      }
+    }
+    best = __reduce_max_sync(0xffffffffu, best);
+    const uint32_t best_r = 0xffffu - (best & 0xffffu);
+    if (best_r == 0) return;
+    const uint32_t pk = unrank_packed(best_r, m);
+    const int p = lane < m ? static_cast<int>((pk >> (4 * lane)) & 15u) : 0;
+    const int32_t ns = shfl_i(ms, p);
+    const double nc = shfl_d(mc, p);
+    if (lane < m) {
+      qs[(qh + lane) & mask] = ns;
+      qc[(qh + lane) & mask] = nc;
+      if (lane > p) ++GLP(s_->G.sess)[ns].postpone;
+    }
+    warp_sync();
+  }
+
+  // k-th (0-based) lexicographic permutation of 0..m-1, 4 bits per position.
+  PDG_HD static uint32_t unrank_packed(uint32_t k, int m) {
+    uint64_t avail = 0x76543210ull;
+    uint32_t out = 0;
+    uint32_t f = 1;
+    for (int i = 2; i < m; ++i) f *= static_cast<uint32_t>(i);  // (m-1)!
+    for (int i = 0; i < m; ++i) {
+      const uint32_t q = k / f;
+      k -= q * f;
+      const uint32_t sh = 4 * q;
+      out |= static_cast<uint32_t>((avail >> sh) & 15u) << (4 * i);
+      avail = (avail & ((1ull << sh) - 1ull)) | ((avail >> (sh + 4)) << sh);
+      const int rest = m - 1 - i;
+      if (rest > 0) f /= static_cast<uint32_t>(rest);
+    }
+    return out;
+  }
+#else
   PDG_COLD void reorder_head(int32_t* qs, double* qc, uint32_t qh, int m) {
     const uint32_t mask = static_cast<uint32_t>(s_->C.qcap - 1);
     int32_t hs[8];
@@ -1522,7 +1742,7 @@ class Engine {
     for (int k = 0; k < m; ++k) {
       hs[k] = qs[(qh + k) & mask];
       hc[k] = qc[(qh + k) & mask];
-      const SessRt& s = s_->G.sess[hs[k]];
+      const SessRt& s = GLP(s_->G.sess)[hs[k]];
       wait[k] = dsub(s_->now_, s.t_enq);
       pc[k] = s.postpone;
     }
@@ -1564,12 +1784,14 @@ class Engine {
     {  // warp-uniform stores (every lane writes the same values)
       for (int k = 0; k < m; ++k) {
         const int p = perm[k];
-        if (k > p) ++s_->G.sess[hs[p]].postpone;
+        if (k > p) ++GLP(s_->G.sess)[hs[p]].postpone;
         qs[(qh + k) & mask] = hs[p];
         qc[(qh + k) & mask] = hc[p];
       }
     }
   }
+
+#endif
 
   PDG_HD static int count_satisfied(const int* perm, int m, const double* hc, const double* wait, double thres) {
     double elapsed = 0.0;
@@ -1583,25 +1805,25 @@ class Engine {
 
   // ---- prefill workers (sim_engine.cpp:354-453) ----
   PDG_HD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     const double cost = t_prefill(ctx, incr, w.deg);
-    if (!queue_push(w.q, s_->G.pq_s + static_cast<size_t>(p) * s_->C.qcap, s_->G.pq_c + static_cast<size_t>(p) * s_->C.qcap, i, cost))
+    if (!queue_push(w.q, GLP(s_->G.pq_s) + static_cast<size_t>(p) * s_->C.qcap, GLP(s_->G.pq_c) + static_cast<size_t>(p) * s_->C.qcap, i, cost))
       return;
     try_stage(p);
     try_start_compute(p);
   }
 
   PDG_HD void try_stage(int p) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     if (w.staged || w.q.qh == w.q.qt) return;
     double cost;
-    const int32_t stg = select_next(w.q, s_->G.pq_s + static_cast<size_t>(p) * s_->C.qcap,
-                                    s_->G.pq_c + static_cast<size_t>(p) * s_->C.qcap, &cost);
-    const int32_t hist = s_->G.sess[stg].ctx;
+    const int32_t stg = select_next(w.q, GLP(s_->G.pq_s) + static_cast<size_t>(p) * s_->C.qcap,
+                                    GLP(s_->G.pq_c) + static_cast<size_t>(p) * s_->C.qcap, &cost);
+    const int32_t hist = GLP(s_->G.sess)[stg].ctx;
     double ready = s_->now_;
     if (hist > 0) {
       // Lazy history read from the bound decode worker (sim_engine.cpp:368-383).
-      const int dd = s_->SM.dw[s_->G.sess[stg].bound].deg;
+      const int dd = SHP(s_->SM.dw)[GLP(s_->G.sess)[stg].bound].deg;
       ready = dadd(s_->now_, t_kv(hist, dd, w.deg));
     }
     {  // warp-uniform stores (every lane writes the same values)
@@ -1615,7 +1837,7 @@ class Engine {
   }
 
   PDG_HD void try_start_compute(int p) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     if (w.computing || !w.staged || w.pending || w.staged_ready > s_->now_) return;
     const double done = dadd(s_->now_, w.stg_cost);
     {  // warp-uniform stores (every lane writes the same values)
@@ -1629,10 +1851,10 @@ class Engine {
   }
 
   PDG_HD void on_prefill_done(int p) {
-    PrefillW& w = s_->SM.pw[p];
+    PrefillW& w = SHP(s_->SM.pw)[p];
     const int32_t i = w.cur;
     w.computing = 0;  // warp-uniform store
-    const int dd = s_->SM.dw[s_->G.sess[i].bound].deg;
+    const int dd = SHP(s_->SM.dw)[GLP(s_->G.sess)[i].bound].deg;
     heap_push(dadd(s_->now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
               static_cast<uint32_t>(p));
     try_stage(p);
@@ -1640,26 +1862,31 @@ class Engine {
   }
 
   PDG_HD void on_history_read(int p) {
-    s_->SM.pw[p].pending = 0;  // warp-uniform store
+    SHP(s_->SM.pw)[p].pending = 0;  // warp-uniform store
     try_start_compute(p);
   }
 
   PDG_HD void on_writeback(int32_t i, int p) {
-    const int d = s_->G.sess[i].bound;
+    const int d = GLP(s_->G.sess)[i].bound;
     complete_task(i, false, p, d);
     advance_decode(d);
   }
 
   // complete_task (sim_engine.cpp:458-484).
   PDG_HD void complete_task(int32_t i, bool local, int p, int d) {
-    SessRt& s = s_->G.sess[i];
+    const int64_t t0 = pb();
+    complete_task_(i, local, p, d);
+    pe(kProfComplete, t0);
+  }
+  PDG_HD void complete_task_(int32_t i, bool local, int p, int d) {
+    SessRt& s = GLP(s_->G.sess)[i];
     const int round = s.round;
-    const double created = round == 1 ? s_->T.arrival[i] : s.t_enq;
+    const double created = round == 1 ? GLP(s_->T.arrival)[i] : s.t_enq;
     const double value = dsub(s_->now_, created);
     if (!local) ttft_add(p, value);  // decode workers' TTFT windows are never queried
     if (s_->REC.ttft && lane_id() == 0) {
       pdsim_ttft_sample& o = s_->REC.ttft[s_->n_ttft_];
-      o.session_id = s_->T.sid[i];
+      o.session_id = GLP(s_->T.sid)[i];
       o.round = round;
       o.kind = round == 1 ? 0 : 1;
       o.local = local ? 1 : 0;
@@ -1669,14 +1896,14 @@ class Engine {
       o.value = value;
     }
     ++s_->n_ttft_;
-    const int32_t ridx = s_->T.round_off[i] + round - 1;
-    const int32_t incr = s_->T.incr[ridx];
-    const int32_t dec = s_->T.dec[ridx];
-    DecodeW& w = s_->SM.dw[d];
+    const int32_t ridx = GLP(s_->T.round_off)[i] + round - 1;
+    const int32_t incr = GLP(s_->T.incr)[ridx];
+    const int32_t dec = GLP(s_->T.dec)[ridx];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     interrupt_run(d);
     const int32_t join = w.steps;  // first token in the next step started
     const uint64_t key =
-        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(s_->T.rank[i]);
+        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(GLP(s_->T.rank)[i]);
     warp_sync();
     const int32_t hint = w.seg_end;
     if (lane_id() == 0) {
@@ -1695,22 +1922,27 @@ class Engine {
 
   // ---- decode workers (sim_engine.cpp:488-583) ----
   PDG_HD void enqueue_local(int d, int32_t i, int32_t ctx, int32_t incr) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const double cost = t_prefill(ctx, incr, w.deg);
-    if (!queue_push(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap, s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, i, cost))
+    if (!queue_push(w.q, GLP(s_->G.dq_s) + static_cast<size_t>(d) * s_->C.qcap, GLP(s_->G.dq_c) + static_cast<size_t>(d) * s_->C.qcap, i, cost))
       return;
     interrupt_run(d);
     advance_decode(d);
   }
 
   PDG_HD void advance_decode(int d) {
-    DecodeW& w = s_->SM.dw[d];
+    const int64_t t0 = pb();
+    advance_decode_(d);
+    pe(kProfAdvance, t0);
+  }
+  PDG_HD void advance_decode_(int d) {
+    DecodeW& w = SHP(s_->SM.dw)[d];
     if (w.stepping || w.prefilling) return;
     if (w.q.qh != w.q.qt) {
       // Local prefill preempts decoding until the queue drains.
       double cost;
-      const int32_t cur = select_next(w.q, s_->G.dq_s + static_cast<size_t>(d) * s_->C.qcap,
-                                      s_->G.dq_c + static_cast<size_t>(d) * s_->C.qcap, &cost);
+      const int32_t cur = select_next(w.q, GLP(s_->G.dq_s) + static_cast<size_t>(d) * s_->C.qcap,
+                                      GLP(s_->G.dq_c) + static_cast<size_t>(d) * s_->C.qcap, &cost);
       {  // warp-uniform stores (every lane writes the same values)
         w.cur = cur;
         w.cur_cost = cost;
@@ -1765,7 +1997,7 @@ class Engine {
       const int mine = base + lane_id();
       bool need = false;
       if (mine < D) {
-        const DecodeW& w = s_->SM.dw[mine];
+        const DecodeW& w = SHP(s_->SM.dw)[mine];
         need = w.stepping && w.steps - 1 < w.run_b && w.cur_end <= t;
       }
       uint32_t m = ballot(need);
@@ -1779,7 +2011,12 @@ class Engine {
   }
 
   PDG_HD void catch_up_worker(int d, double t, uint32_t kind) {
-    DecodeW& w = s_->SM.dw[d];
+    const int64_t t0 = pb();
+    catch_up_worker_(d, t, kind);
+    pe(kProfCatchUp, t0);
+  }
+  PDG_HD void catch_up_worker_(int d, double t, uint32_t kind) {
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const int64_t kvb = PDG_PROF.kv_bytes_per_token;
     while (w.stepping && w.steps - 1 < w.run_b) {
       const double e = w.cur_end;
@@ -1877,12 +2114,12 @@ class Engine {
     const double ulp = bitsd(static_cast<uint64_t>(es - 52) << 52);
     if (dmul(static_cast<double>(dstep), ulp) != g) return 1;
     if (S1 > kTop) return 1;
-    int64_t m = 1 + static_cast<int64_t>((kTop - S1) / dstep);
+    int64_t m = 1 + static_cast<int64_t>(udiv53(kTop - S1, dstep));
     const uint64_t tb = dbits(t);
     const int et = static_cast<int>((tb >> 52) & 0x7ff);
     if (et == es) {  // t in the same binade: S1 + (j-1) d < T
       const uint64_t T = (tb & kMant) | (1ull << 52);
-      const int64_t mt = 1 + static_cast<int64_t>((T - S1 - 1) / dstep);
+      const int64_t mt = 1 + static_cast<int64_t>(udiv53(T - S1 - 1, dstep));
       if (mt < m) m = mt;
     }
     if (max_m < m) m = max_m;
@@ -1892,7 +2129,7 @@ class Engine {
   // A join or a local prefill on a worker whose in-flight step is silent:
   // that step's end becomes an explicit event (its successor differs).
   PDG_HD void interrupt_run(int d) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     if (!s_->lazy_ || !w.stepping) return;
     catch_up_worker(d, s_->now_, s_->cur_kind_);
     const int32_t k = w.steps - 1;
@@ -1903,7 +2140,7 @@ class Engine {
   }
 
   PDG_HD void on_local_prefill_done(int d) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const int32_t i = w.cur;
     w.prefilling = 0;  // warp-uniform store
     complete_task(i, true, -1, d);
@@ -1911,7 +2148,7 @@ class Engine {
   }
 
   PDG_HD void on_decode_step(int d) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     if (s_->lazy_) catch_up_worker(d, s_->now_, kDecodeStep);
     const int32_t k = w.steps - 1;  // index of the step that just ended
     const int32_t cohort = w.cohort_n;
@@ -1933,12 +2170,13 @@ class Engine {
         fail();
         return;
       }
+      const int64_t tf0 = pb();
       const uint32_t rank = static_cast<uint32_t>(w.fh_top);
       fh_pop(d);
-      const int32_t i = s_->T.by_rank[rank];
-      SessRt& s = s_->G.sess[i];
-      const int32_t ridx = s_->T.round_off[i] + s.round - 1;
-      const int32_t dec = s_->T.dec[ridx];
+      const int32_t i = GLP(s_->T.by_rank)[rank];
+      SessRt& s = GLP(s_->G.sess)[i];
+      const int32_t ridx = GLP(s_->T.round_off)[i] + s.round - 1;
+      const int32_t dec = GLP(s_->T.dec)[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
       ufx_t fxs = s.itl_fx;
@@ -1950,7 +2188,7 @@ class Engine {
         fxs += seg_sum(d, s.join, k, s.seg_hint, &ri);
         inex += ri;
       }
-      const bool last = s.round == s_->T.round_off[i + 1] - s_->T.round_off[i];
+      const bool last = s.round == GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
       {  // warp-uniform stores (every lane writes the same values)
         s.itl_sum = sum;
         s.itl_fx = fxs;
@@ -1963,15 +2201,16 @@ class Engine {
         terminate_session(i, d);
         any_terminated = true;
       } else {
-        heap_push(dadd(s_->now_, s_->T.delay[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
+        heap_push(dadd(s_->now_, GLP(s_->T.delay)[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
       }
+      pe(kProfFinisher, tf0);
     }
     if (any_terminated) admit_waiting();
     advance_decode(d);
   }
 
   PDG_HD void on_interaction_done(int32_t i) {
-    SessRt& s = s_->G.sess[i];
+    SessRt& s = GLP(s_->G.sess)[i];
     const int round = s.round + 1;
     const int bound = s.bound;
     const int32_t ctx = s.ctx;
@@ -1981,7 +2220,7 @@ class Engine {
 
   // terminate_session + slo_verdict (sim_engine.cpp:591-607, 668-674).
   PDG_COLD void terminate_session(int32_t i, int d) {
-    SessRt& s = s_->G.sess[i];
+    SessRt& s = GLP(s_->G.sess)[i];
     const int32_t ctx = s.ctx;
     const int32_t cnt = s.itl_cnt;
     const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
@@ -2005,15 +2244,15 @@ class Engine {
     }
     const bool slo_ok = ttft_ok && itl_ok;
     {  // warp-uniform stores (every lane writes the same values)
-      s_->SM.dw[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
+      SHP(s_->SM.dw)[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
       if (s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
-        o.session_id = s_->T.sid[i];
-        o.arrival_time = s_->T.arrival[i];
+        o.session_id = GLP(s_->T.sid)[i];
+        o.arrival_time = GLP(s_->T.arrival)[i];
         o.completion_time = s_->now_;
-        o.admission_wait = dsub(s.bind_time, s_->T.arrival[i]);
+        o.admission_wait = dsub(s.bind_time, GLP(s_->T.arrival)[i]);
         o.mean_itl = mean_itl;
-        o.rounds = s_->T.round_off[i + 1] - s_->T.round_off[i];
+        o.rounds = GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
         o.ttft_ok = ttft_ok;
         o.itl_ok = itl_ok;
         o.slo_ok = slo_ok;
@@ -2028,13 +2267,13 @@ class Engine {
 
   // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
   PDG_HD void fh_push(int d, uint64_t key) {
-    DecodeW& w = s_->SM.dw[d];
+    DecodeW& w = SHP(s_->SM.dw)[d];
     const int32_t n = w.fh_n;
     if (n >= s_->C.fcap) {
       fail();
       return;
     }
-    uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
+    uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
     const uint64_t top = w.fh_top;
     {  // warp-uniform stores (every lane writes the same values)
       int32_t i = n;
@@ -2052,8 +2291,8 @@ class Engine {
   }
 
   PDG_HD void fh_pop(int d) {
-    DecodeW& w = s_->SM.dw[d];
-    uint64_t* h = s_->G.fh + static_cast<size_t>(d) * s_->C.fcap;
+    DecodeW& w = SHP(s_->SM.dw)[d];
+    uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
     {  // warp-uniform stores (every lane writes the same values)
       const int32_t n = w.fh_n - 1;
       const uint64_t last = h[n];
@@ -2079,5 +2318,11 @@ class Engine {
     }
   }
 };
+
+using Engine = EngineT<false>;
+
+#if defined(__CUDA_ARCH__)
+#undef s_
+#endif
 
 }  // namespace pdg

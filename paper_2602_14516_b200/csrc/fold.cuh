@@ -80,7 +80,7 @@ PDG_HD double fold_repeat(double s, double g, uint64_t count) {
       --count;
       continue;
     }
-    uint64_t n = (kTop - S) / d;
+    uint64_t n = udiv53(kTop - S, d);
     if (n > count) n = count;
     S += n * d;
     count -= n;

@@ -31,7 +31,9 @@ def main(cfg="C2"):
            "phases": {name: {"cycles": prof[0][k], "count": prof[1][k],
                              "cycles_per": prof[0][k] / max(prof[1][k], 1)}
                       for k, name in enumerate(["select", "arrival", "interaction", "writeback", "decode_step",
-                                                "local_prefill_done", "prefill_done", "history_read"])},
+                                                "local_prefill_done", "prefill_done", "history_read",
+                                                "~route", "~enqueue", "~catch_up", "~finisher", "~advance_decode",
+                                                "~complete_task", "~heap", "~dequeue"])},
            "replayed_pairs": prof[2]}
     print(json.dumps(out, indent=1))
 
