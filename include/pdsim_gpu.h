@@ -292,9 +292,11 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
  * 7 history read. Inclusive sub-scopes (nested inside the phases): 8 routing
  * decision, 9 task enqueue, 10 lazy decode catch-up, 11 finishing-member
  * fold, 12 advance_decode, 13 complete_task, 14 session-event heap,
- * 15 queue dequeue (reorder). `replayed` counts pairs whose fast attempt was
- * replayed in exact mode. */
-#define PDSIM_PROF_BUCKETS 16
+ * 15 queue dequeue (reorder), 16 step-log append, 17 finisher heap,
+ * 18 TTFT window add, 19 ITL slack test, 20 TTFT slack test, 21 bulk silent
+ * steps, 22 per-round ITL sum, 23 prefill staging. `replayed` counts pairs
+ * whose fast attempt was replayed in exact mode. */
+#define PDSIM_PROF_BUCKETS 24
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
 int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts,
                                int64_t* replayed);

@@ -83,6 +83,7 @@ struct pdsim_gpu_ctx {
   DevBuf d_dec, d_ttft, d_sess;
   // diagnostics
   int profiling = 0;
+  int layout = 0;  // index of the compiled shared-memory layout (stage_impl)
   int64_t prof_cycles[PDSIM_PROF_BUCKETS] = {0};
   int64_t prof_count[PDSIM_PROF_BUCKETS] = {0};
   int64_t attempts2 = 0;
@@ -133,13 +134,22 @@ struct KernelArgs {
 };
 
 // One warp per block; the warp replays pairs pulled from an atomic queue.
-template <bool kProf>
+// kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
+// addresses slot state at compile-time offsets (engine.cuh smem_off).
+template <bool kProf, int kD, int kP>
 __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
   const int slot_id = blockIdx.x;
   pdg::GlobalSlot gslot;
   pdg::global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
   pdg::SmemSlot sslot;
   pdg::smem_slot_bytes(a.caps, &sslot, pdg::pdg_smem);  // EngState first (engine.cuh)
+  {
+    constexpr pdg::SmemOff off = pdg::smem_off(kD, kP);
+    if (a.caps.dres != kD || a.caps.pres != kP || reinterpret_cast<char*>(sslot.dw) != pdg::pdg_smem + off.dw ||
+        reinterpret_cast<char*>(sslot.pw) != pdg::pdg_smem + off.pw || reinterpret_cast<char*>(sslot.heap) != pdg::pdg_smem + off.heap) {
+      __trap();  // host/device slot layouts disagree: never replay on a wrong layout
+    }
+  }
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long ticket = 0;
@@ -158,13 +168,8 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      if (kProf) {
-        pdg::EngineT<true> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, 1);
-        eng.run(&res);
-      } else {
-        pdg::Engine eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, 0);
-        eng.run(&res);
-      }
+      pdg::EngineT<kProf, kD, kP> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
+      eng.run(&res);
       res.cycles = clock64() - t0;
     }
     if (lane == 0) {
@@ -261,7 +266,12 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   const size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
                              : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
                                                           : (size_t(12) << 10);
-  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params, smem_budget);
+  // Compiled shared-memory layouts (replay_kernel<.., kD, kP>): N <= 8 plans
+  // fit <8, 8>, N <= 16 plans <16, 16>; D + 2P <= 64 bounds the rest.
+  const int lay = (dmax <= 8 && pmax <= 8) ? 0 : (dmax <= 16 && pmax <= 16) ? 1 : 2;
+  static const int kLayD[3] = {8, 16, 64}, kLayP[3] = {8, 16, 32};
+  ctx->layout = lay;
+  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params, smem_budget, kLayD[lay], kLayP[lay]);
   ctx->slot_bytes = pdg::global_slot_bytes(ctx->caps, nullptr, nullptr);
   ctx->smem_bytes = pdg::smem_slot_bytes(ctx->caps, nullptr, nullptr);
   ctx->profile = *profile;
@@ -380,7 +390,10 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   if (n > 0) {
     // The diagnostics build (per-phase clock64 counters) is a separate
     // instantiation so the product kernel carries no instrumentation.
-    void (*kern)(KernelArgs) = ctx->profiling ? replay_kernel<true> : replay_kernel<false>;
+    void (*const kernels[2][3])(KernelArgs) = {
+        {replay_kernel<false, 8, 8>, replay_kernel<false, 16, 16>, replay_kernel<false, 64, 32>},
+        {replay_kernel<true, 8, 8>, replay_kernel<true, 16, 16>, replay_kernel<true, 64, 32>}};
+    void (*kern)(KernelArgs) = kernels[ctx->profiling ? 1 : 0][ctx->layout];
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
     kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;

@@ -221,12 +221,13 @@ struct DevParams {
 
 // Per-session runtime state (SessionRt + the one PrefillTask in flight).
 struct SessRt {
-  ufx_t itl_fx;      // search mode: exact fixed-point sum of this session's ITL samples
+  double itl_lo;     // search mode: bracket [itl_lo, itl_hi] of the exact sum of this
+  double itl_hi;     //   session's ITL samples (directed rounding)
   double t_enq;      // enqueue time of the current task (== created for r >= 2)
   double itl_sum;    // exact mode: sequential fold of this session's ITL samples
   double bind_time;  // admission time
   int32_t itl_cnt;
-  int32_t itl_inex;  // ITL samples without an exact fixed-point image
+  int32_t itl_pad;
   int32_t join;      // step index at which the current round joined the batch
   int32_t ctx;       // context_len
   int32_t seg_hint;  // bound worker's open-segment index when the round joined
@@ -265,23 +266,17 @@ struct PrefillW {  // shared memory
 // the same ITL sample count per step: step j (first <= j < first + n) ends
 // at t0 + (j - first) * gap exactly (each step adds exactly `gap`).
 struct Seg {
-  Pfx pfx;       // window prefix before this segment
-  ufx_t p1;      // sum of fx(gap) over every step before this segment (one per step)
   double t0;     // end time of step `first`
   double gap;    // every step's ITL gap (end - previous end)
   int32_t first; // first step index
   int32_t n;     // steps
   uint32_t cnt;  // ITL samples per step (cohort members past their first token)
-  int32_t inex;  // gap has no exact fixed-point image (and cnt > 0)
-  int32_t inex1; // steps before this segment whose gap has no exact image
-  int32_t gx;    // gap has an exact fixed-point image
+  int32_t reserved;
 };
 
 struct DecodeW {  // shared memory
   TaskQueue q;  // local prefill queue
   Seg sg;       // the open (newest) segment of the step log
-  ufx_t sg_prod;       // fx(sg.gap) * sg.cnt
-  ufx_t sg_fx;         // fx(sg.gap)
   int64_t kv_used;
   int64_t kv_cap;
   uint64_t fh_top;     // cached finisher-heap minimum (valid when fh_n > 0)
@@ -319,6 +314,8 @@ struct Caps {
   int32_t maxdec;  // longest decode round (steps a per-session fold may reach back)
   int32_t pmax;
   int32_t dmax;
+  int32_t pres;    // PrefillW / DecodeW entries reserved in shared memory (>= pmax, dmax);
+  int32_t dres;    // the device engine addresses them at compile-time offsets (EngineT<.., kD, kP>)
 };
 
 struct EngState;
@@ -351,7 +348,26 @@ struct GlobalSlot {
 PDG_HD size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 PDG_HD size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
-constexpr size_t kEngStateBytes = 2048;  // >= sizeof(EngState), checked below
+constexpr size_t kEngStateBytes = 2560;  // >= sizeof(EngState), checked below
+
+// Shared-memory layout of a slot: EngState, DecodeW[dres], PrefillW[pres],
+// the mt19937_64 state, the routing-order scratch, then the session-event
+// heap (the only variable-size part, last). smem_off() gives the same offsets
+// as compile-time constants for the device engine.
+PDG_HD constexpr size_t smem_a16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+struct SmemOff {
+  size_t dw, pw, mt, order, heap;
+};
+PDG_HD constexpr SmemOff smem_off(size_t dres, size_t pres) {
+  return SmemOff{smem_a16(kEngStateBytes), smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres),
+                 smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) + sizeof(PrefillW) * pres),
+                 smem_a16(smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) + sizeof(PrefillW) * pres) +
+                          8 * 312),
+                 smem_a16(smem_a16(smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) +
+                                             sizeof(PrefillW) * pres) +
+                                    8 * 312) +
+                          4 * kMaxSlots)};
+}
 
 PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
   size_t off = 0;
@@ -362,11 +378,11 @@ PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
   };
   SmemSlot t;
   t.es = reinterpret_cast<EngState*>(take(kEngStateBytes));
-  t.pw = reinterpret_cast<PrefillW*>(take(sizeof(PrefillW) * static_cast<size_t>(c.pmax > 0 ? c.pmax : 1)));
-  t.dw = reinterpret_cast<DecodeW*>(take(sizeof(DecodeW) * static_cast<size_t>(c.dmax)));
+  t.dw = reinterpret_cast<DecodeW*>(take(sizeof(DecodeW) * static_cast<size_t>(c.dres)));
+  t.pw = reinterpret_cast<PrefillW*>(take(sizeof(PrefillW) * static_cast<size_t>(c.pres)));
   t.mt = reinterpret_cast<uint64_t*>(take(8 * 312));
-  t.heap = reinterpret_cast<HEv*>(take(sizeof(HEv) * static_cast<size_t>(c.hs)));
   t.order = reinterpret_cast<int32_t*>(take(4 * kMaxSlots));
+  t.heap = reinterpret_cast<HEv*>(take(sizeof(HEv) * static_cast<size_t>(c.hs)));
   if (s) *s = t;
   return off;
 }
@@ -513,6 +529,7 @@ inline const pdsim_profile*& host_profile() {  // host (test) builds only
 #endif
 
 static_assert(sizeof(EngState) <= kEngStateBytes, "EngState outgrew its shared-memory reservation");
+static_assert(kEngStateBytes % 16 == 0, "slot layout alignment");
 
 #if defined(__CUDA_ARCH__)
 #define s_ (reinterpret_cast<EngState*>(pdg_smem))
@@ -520,8 +537,10 @@ static_assert(sizeof(EngState) <= kEngStateBytes, "EngState outgrew its shared-m
 
 // kProf compiles in the per-phase clock64 instrumentation (diagnostics
 // kernel only); the product kernel is EngineT<false>.
-template <bool kProf>
+template <bool kProf, int kD = 0, int kP = 0>
 class EngineT {
+  static constexpr SmemOff kOff = smem_off(static_cast<size_t>(kD), static_cast<size_t>(kP));
+
  public:
   // `es` must point at this warp's EngState (shared memory on the device).
   // On the device `es` must be the EngState at the start of the block's
@@ -667,7 +686,7 @@ class EngineT {
   }
 
   PDG_HD void finish_result(PairResult* out) {
-    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += SHP(s_->SM.dw)[d].kv_used;
+    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += DW(d).kv_used;
     out->att = s_->att_;
     out->att.sessions_total = s_->T.S;
     out->ctr = s_->ctr_;
@@ -689,6 +708,22 @@ class EngineT {
 #endif
 
   PDG_HD void fail() { s_->failed_ = 1; }
+
+  // Slot arrays in shared memory: fixed offsets from the dynamic shared
+  // memory base on the device (one LDS/STS per field, no pointer load).
+#if defined(__CUDA_ARCH__)
+  PDG_HD DecodeW& DW(int d) const { return reinterpret_cast<DecodeW*>(pdg_smem + kOff.dw)[d]; }
+  PDG_HD PrefillW& PW(int p) const { return reinterpret_cast<PrefillW*>(pdg_smem + kOff.pw)[p]; }
+  PDG_HD uint64_t* MT() const { return reinterpret_cast<uint64_t*>(pdg_smem + kOff.mt); }
+  PDG_HD int32_t* ORD() const { return reinterpret_cast<int32_t*>(pdg_smem + kOff.order); }
+  PDG_HD HEv* SHEAP() const { return reinterpret_cast<HEv*>(pdg_smem + kOff.heap); }
+#else
+  DecodeW& DW(int d) const { return s_->SM.dw[d]; }
+  PrefillW& PW(int p) const { return s_->SM.pw[p]; }
+  uint64_t* MT() const { return s_->SM.mt; }
+  int32_t* ORD() const { return s_->SM.order; }
+  HEv* SHEAP() const { return s_->SM.heap; }
+#endif
 
   PDG_HD void advance_to(double t) {
     if (t < s_->now_) s_->ctr_.events_in_order = 0;  // sim_engine.cpp:148-150
@@ -727,9 +762,9 @@ class EngineT {
     }
     {  // warp-uniform stores (every lane writes the same values)
       uint32_t idx;
-      mt64_seed(SHP(s_->SM.mt), &idx, s_->seed_);
+      mt64_seed(MT(), &idx, s_->seed_);
       for (int p = 0; p < s_->PL.P; ++p) {
-        PrefillW& w = SHP(s_->SM.pw)[p];
+        PrefillW& w = PW(p);
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
         w.tw.tail.clear();
@@ -741,21 +776,15 @@ class EngineT {
         w.staged_ready = 0.0;
       }
       for (int d = 0; d < s_->PL.D; ++d) {
-        DecodeW& w = SHP(s_->SM.dw)[d];
+        DecodeW& w = DW(d);
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
-        w.sg.pfx.clear();
-        w.sg.p1 = 0;
-        w.sg.inex1 = 0;
-        w.sg.gx = 1;
-        w.sg_fx = 0;
         w.sg.t0 = 0.0;
         w.sg.gap = 0.0;
         w.sg.first = 0;
         w.sg.n = 0;
         w.sg.cnt = 0;
-        w.sg.inex = 0;
-        w.sg_prod = 0;
+        w.sg.reserved = 0;
         w.seg_end = w.seg_keep = w.seg_head = w.seg_off = 0;
         w.kv_used = 0;
         w.kv_cap = static_cast<int64_t>(PDG_PROF.degrees[s_->PL.ddeg[d]]) * PDG_PROF.gpu_memory_capacity;
@@ -801,7 +830,7 @@ class EngineT {
       // Warp-parallel twist in three dependency phases: elements below 156
       // read only old words; 156..310 read updated words i-156; 311 reads
       // updated words 0 and 155.
-      uint64_t* mt = SHP(s_->SM.mt);
+      uint64_t* mt = MT();
       const int lane = lane_id();
       for (int base = 0; base < 156; base += 32) {
         const int i = base + lane;
@@ -833,11 +862,11 @@ class EngineT {
         __syncwarp();
       }
 #else
-      mt64_twist(SHP(s_->SM.mt));
+      mt64_twist(MT());
 #endif
       s_->mt_idx_ = 0;
     }
-    return mt64_temper(SHP(s_->SM.mt)[s_->mt_idx_++]);
+    return mt64_temper(MT()[s_->mt_idx_++]);
   }
 
   // ---- worker-event slots (registers) ----
@@ -920,7 +949,7 @@ class EngineT {
       *t = h[0].t;
       *key = h[0].key;
     } else {
-      const HEv* h = SHP(s_->SM.heap);
+      const HEv* h = SHEAP();
       *t = h[0].t;
       *key = h[0].key;
     }
@@ -939,7 +968,7 @@ class EngineT {
     e.b = b;
     if (!s_->heap_spilled_ && s_->hn_ >= s_->C.hs) {
       HEv* gh = GLP(s_->G.heap);
-      const HEv* sh = SHP(s_->SM.heap);
+      const HEv* sh = SHEAP();
       for (int k = lane_id(); k < s_->hn_; k += PDG_NL) gh[k] = sh[k];
       warp_sync();
       s_->heap_spilled_ = true;
@@ -952,7 +981,7 @@ class EngineT {
     if (s_->heap_spilled_) {
       heap_sift_up(GLP(s_->G.heap), n, e);
     } else {
-      heap_sift_up(SHP(s_->SM.heap), n, e);
+      heap_sift_up(SHEAP(), n, e);
     }
   }
   PDG_HD static void heap_sift_up(HEv* h, int32_t i, const HEv& e) {
@@ -974,7 +1003,7 @@ class EngineT {
   }
   PDG_HD HEv heap_pop_() {
     const int32_t n = --s_->hn_;
-    const HEv top = s_->heap_spilled_ ? heap_sift_down(GLP(s_->G.heap), n) : heap_sift_down(SHP(s_->SM.heap), n);
+    const HEv top = s_->heap_spilled_ ? heap_sift_down(GLP(s_->G.heap), n) : heap_sift_down(SHEAP(), n);
     if (n == 0) s_->heap_spilled_ = false;
     return top;
   }
@@ -1014,9 +1043,9 @@ class EngineT {
   PDG_HD int bind_session() {  // least KV bytes, lowest index on ties
     if (s_->lazy_) catch_up(s_->now_, s_->cur_kind_);
     int best = 0;
-    int64_t bv = SHP(s_->SM.dw)[0].kv_used;
+    int64_t bv = DW(0).kv_used;
     for (int d = 1; d < s_->PL.D; ++d) {
-      const int64_t v = SHP(s_->SM.dw)[d].kv_used;
+      const int64_t v = DW(d).kv_used;
       if (v < bv) {
         bv = v;
         best = d;
@@ -1027,7 +1056,7 @@ class EngineT {
 
   PDG_COLD bool try_admit(int32_t i) {
     const int best = bind_session();
-    const DecodeW& w = SHP(s_->SM.dw)[best];
+    const DecodeW& w = DW(best);
     const int64_t first = static_cast<int64_t>(GLP(s_->T.incr)[GLP(s_->T.round_off)[i]]) * PDG_PROF.kv_bytes_per_token;
     if (w.kv_used + first > w.kv_cap) return false;
     SessRt& s = GLP(s_->G.sess)[i];
@@ -1037,8 +1066,8 @@ class EngineT {
       s.round = 1;
       s.ctx = 0;
       s.itl_sum = 0.0;
-      s.itl_fx = 0;
-      s.itl_inex = 0;
+      s.itl_lo = 0.0;
+      s.itl_hi = 0.0;
       s.itl_cnt = 0;
       s.join = 0;
       s.postpone = 0;
@@ -1053,7 +1082,7 @@ class EngineT {
   }
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
-  PDG_COLD void start_round(int32_t i, int round, int bound, int32_t ctx) {
+  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx) {
     SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.t_enq = s_->now_;
@@ -1115,21 +1144,51 @@ class EngineT {
   PDG_COLD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
     const int n = s_->PL.P;
     if (n > 0) {
-      int32_t* order = SHP(s_->SM.order);
-      {  // warp-uniform stores (every lane writes the same values)
-        for (int k = 0; k < n; ++k) order[k] = k;
-      }
-      for (int k = n - 1; k > 0; --k) {
-        const int j = static_cast<int>(umod64_small(rng_next(), static_cast<uint32_t>(k + 1)));
-        const int a = order[k], b = order[j];
+#if defined(__CUDA_ARCH__)
+      const uint32_t idx = s_->mt_idx_;
+      const bool packed = n <= 16 && idx + static_cast<uint32_t>(n - 1) <= static_cast<uint32_t>(Mt64::kN);
+#else
+      const bool packed = false;
+#endif
+      uint64_t perm = 0;  // packed scan order, 4 bits per position (n <= 16)
+      int32_t* order = ORD();
+      if (packed) {
+#if defined(__CUDA_ARCH__)
+        // The n-1 draws of one route are consecutive engine outputs with no
+        // twist in between: lane t tempers word idx+t and reduces it mod
+        // n-t (draw t belongs to k = n-1-t); the swaps then run on a
+        // register-packed permutation.
+        const int lane = lane_id();
+        uint32_t j = 0;
+        if (lane < n - 1) j = umod64_small(mt64_temper(MT()[idx + lane]), static_cast<uint32_t>(n - lane));
+        const uint32_t jlo = __reduce_or_sync(0xffffffffu, lane < 8 ? j << (4 * lane) : 0u);
+        const uint32_t jhi = __reduce_or_sync(0xffffffffu, (lane >= 8 && lane < 16) ? j << (4 * (lane - 8)) : 0u);
+        const uint64_t js = (static_cast<uint64_t>(jhi) << 32) | jlo;
+        s_->mt_idx_ = idx + static_cast<uint32_t>(n - 1);
+        perm = 0xfedcba9876543210ull;
+        for (int t = 0; t < n - 1; ++t) {
+          const int k = n - 1 - t;
+          const int jj = static_cast<int>((js >> (4 * t)) & 15u);
+          const uint64_t x = ((perm >> (4 * k)) ^ (perm >> (4 * jj))) & 15u;
+          perm ^= (x << (4 * k)) | (x << (4 * jj));
+        }
+#endif
+      } else {
         {  // warp-uniform stores (every lane writes the same values)
-          order[k] = b;
-          order[j] = a;
+          for (int k = 0; k < n; ++k) order[k] = k;
+        }
+        for (int k = n - 1; k > 0; --k) {
+          const int j = static_cast<int>(umod64_small(rng_next(), static_cast<uint32_t>(k + 1)));
+          const int a = order[k], b = order[j];
+          {  // warp-uniform stores (every lane writes the same values)
+            order[k] = b;
+            order[j] = a;
+          }
         }
       }
       const double thr = dmul(s_->PR.alpha, s_->T.ttft_thres);
       for (int k = 0; k < n; ++k) {
-        const int p = order[k];
+        const int p = packed ? static_cast<int>((perm >> (4 * k)) & 15u) : order[k];
         if (ttft_has_slack(p, thr)) {
           r->local = 0;
           r->p = p;
@@ -1160,7 +1219,7 @@ class EngineT {
   PDG_HD void estimate(int d, int32_t ctx, int32_t incr, int c, bool force_exact, double* lo, double* hi,
                        bool* exact) const {
     if (c < 0) {
-      const DecodeW& w = SHP(s_->SM.dw)[d];
+      const DecodeW& w = DW(d);
       const uint32_t len = w.q.qt - w.q.qh;
       const double own = t_prefill(ctx, incr, w.deg);
       if (force_exact || len <= 2 || !w.q.sum.exact()) {
@@ -1175,8 +1234,8 @@ class EngineT {
       *exact = false;
       return;
     }
-    const PrefillW& w = SHP(s_->SM.pw)[c];
-    const int pd = w.deg, dd = SHP(s_->SM.dw)[d].deg;
+    const PrefillW& w = PW(c);
+    const int pd = w.deg, dd = DW(d).deg;
     const uint32_t len = w.q.qt - w.q.qh;
     const double head = dadd(t_prefill(ctx, incr, pd), dadd(t_kv(ctx, dd, pd), t_kv(incr, pd, dd)));
     if (force_exact || len <= 2 || !w.q.sum.exact()) {
@@ -1312,8 +1371,13 @@ class EngineT {
     return true;
   }
 
-  PDG_HD void ttft_add(int p, double v) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PDG_HD void ttft_add(int p, double v) {
+    const int64_t t0_ = pb();
+    ttft_add_(p, v);
+    pe(18, t0_);
+  }
+  PDG_HD void ttft_add_(int p, double v) {
+    PrefillW& w = PW(p);
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
     if (!window_room(w.tw, GLP(s_->G.tw_t) + base, static_cast<uint32_t>(s_->C.twcap), s_->now_)) return;
@@ -1331,8 +1395,14 @@ class EngineT {
   }
 
   // query(now) <= thr with the sequential windowed mean's semantics.
-  PDG_HD bool ttft_has_slack(int p, double thr) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PDG_HD bool ttft_has_slack(int p, double thr) {
+    const int64_t t0_ = pb();
+    const bool r_ = ttft_has_slack_(p, thr);
+    pe(20, t0_);
+    return r_;
+  }
+  PDG_HD bool ttft_has_slack_(int p, double thr) {
+    PrefillW& w = PW(p);
     const size_t base = static_cast<size_t>(p) * s_->C.twcap;
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
     window_trim(w.tw, GLP(s_->G.tw_t) + base, mask, s_->now_);
@@ -1351,7 +1421,7 @@ class EngineT {
   PDG_HD Seg* seg_ring(int d) const { return GLP(s_->G.seg) + static_cast<size_t>(d) * s_->C.segcap; }
   // Segment i of worker d (i == seg_end is the open one, in shared memory).
   PDG_HD Seg seg_at(int d, int32_t i) const {
-    const DecodeW& w = SHP(s_->SM.dw)[d];
+    const DecodeW& w = DW(d);
     if (i == w.seg_end) return w.sg;
     return seg_ring(d)[static_cast<uint32_t>(i) & static_cast<uint32_t>(s_->C.segcap - 1)];
   }
@@ -1359,19 +1429,16 @@ class EngineT {
   PDG_HD static double seg_time(const Seg& g, int32_t j) {
     return dadd(g.t0, dmul(static_cast<double>(j - g.first), g.gap));
   }
-  // Prefix after the open segment (the window's running total).
-  PDG_HD Pfx tail_pfx(const DecodeW& w) const {
-    Pfx t = w.sg.pfx;
-    t.sum += w.sg_prod * static_cast<ufx_t>(static_cast<uint32_t>(w.sg.n));
-    t.terms += static_cast<int64_t>(w.sg.cnt) * w.sg.n;
-    t.inexact += w.sg.n > 0 ? w.sg.inex : 0;
-    return t;
-  }
 
   // Appends n consecutive steps (first index `first`, first end time t0,
   // each with ITL gap `gap` and `cnt` ITL samples) to worker d's log.
-  PDG_HD void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    PDG_HD void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
+    const int64_t t0_ = pb();
+    seg_append_(d, first, n, t0, gap, cnt);
+    pe(16, t0_);
+  }
+  PDG_HD void seg_append_(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
+    DecodeW& w = DW(d);
     if (w.sg.n > 0 && gap == w.sg.gap && cnt == w.sg.cnt && first == w.sg.first + w.sg.n) {
       w.sg.n = w.sg.n + n;  // extends the open segment (t0 continues the progression)
       return;
@@ -1387,33 +1454,20 @@ class EngineT {
           return;
         }
       }
-      const Seg closed = w.sg;
-      const Pfx next_pfx = tail_pfx(w);
-      const ufx_t next_p1 = closed.p1 + w.sg_fx * static_cast<ufx_t>(static_cast<uint32_t>(closed.n));
-      const int32_t next_inex1 = closed.inex1 + (closed.gx ? 0 : closed.n);
-      seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = closed;
+      seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = w.sg;
       w.seg_end = end + 1;
-      w.sg.pfx = next_pfx;
-      w.sg.p1 = next_p1;
-      w.sg.inex1 = next_inex1;
     }
-    fx_t f;
-    const bool exact = to_fx(gap, &f);
-    w.sg.gx = exact ? 1 : 0;
-    w.sg_fx = static_cast<ufx_t>(f);
     w.sg.t0 = t0;
     w.sg.gap = gap;
     w.sg.first = first;
     w.sg.n = n;
     w.sg.cnt = cnt;
-    w.sg.inex = (cnt > 0 && !exact) ? 1 : 0;
-    w.sg_prod = cnt > 0 ? static_cast<ufx_t>(f) * static_cast<ufx_t>(cnt) : static_cast<ufx_t>(0);
   }
 
   // Frees ring slots no longer needed: behind the ITL window head and before
   // any step an active round can still fold (rounds span <= maxdec steps).
   PDG_HD void seg_reclaim(int d, int32_t cur_step) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     const int32_t oldest_needed = cur_step - s_->C.maxdec - 1;
     int32_t keep = w.seg_keep;
     while (keep < w.seg_head && keep < w.seg_end) {
@@ -1427,7 +1481,7 @@ class EngineT {
   // Advances the ITL window head past steps that ended at or before
   // now - window (coordinator.cpp:32-40: the interval is (now - w, now]).
   PDG_HD void seg_trim(int d, double now) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     const double cutoff = dsub(now, s_->PR.stat_window);
     int32_t h = w.seg_head, off = w.seg_off;
     for (;;) {
@@ -1463,22 +1517,42 @@ class EngineT {
   }
 
   // Windowed ITL mean <= thr (coordinator.cpp:32-47 over run-length steps).
-  PDG_HD bool itl_has_slack(int d, double thr) {
+    PDG_HD bool itl_has_slack(int d, double thr) {
+    const int64_t t0_ = pb();
+    const bool r_ = itl_has_slack_(d, thr);
+    pe(19, t0_);
+    return r_;
+  }
+  PDG_HD bool itl_has_slack_(int d, double thr) {
     if (s_->lazy_) catch_up_worker(d, s_->now_, s_->cur_kind_);
     seg_trim(d, s_->now_);
-    const DecodeW& w = SHP(s_->SM.dw)[d];
-    const Pfx tail = tail_pfx(w);
-    const Seg h = seg_at(d, w.seg_head);
-    Pfx head = h.pfx;
-    if (w.seg_head <= w.seg_end && w.seg_off > 0) {
-      const ufx_t prod = w.seg_head == w.seg_end ? w.sg_prod : head_prod(h);
-      head.sum += prod * static_cast<ufx_t>(static_cast<uint32_t>(w.seg_off));
-      head.terms += static_cast<int64_t>(h.cnt) * w.seg_off;
-      if (w.seg_off >= h.n) head.inexact += h.n > 0 ? h.inex : 0;
+    const DecodeW& w = DW(d);
+    // Exact window sum S = sum over in-window steps of cnt * gap, bracketed
+    // with directed rounding; lanes take segments, the bounds combine in any
+    // order. The reference's fold differs from S by <= gamma_{n-1} S.
+    const int32_t h0 = w.seg_head, h1 = w.seg_end, off = w.seg_off;
+    int64_t terms = 0;
+    double lo = 0.0, hi = 0.0;
+    for (int32_t base = h0; base <= h1; base += PDG_NL) {
+      const int32_t i = base + lane_id();
+      if (i <= h1) {
+        const Seg g = seg_at(d, i);
+        const int32_t nn = g.n - (i == h0 ? off : 0);
+        if (nn > 0 && g.cnt > 0) {
+          const int64_t c = static_cast<int64_t>(g.cnt) * nn;
+          terms += c;
+          lo = add_rd(lo, mul_rd(static_cast<double>(c), g.gap));
+          hi = add_ru(hi, mul_ru(static_cast<double>(c), g.gap));
+        }
+      }
     }
-    const int64_t terms = tail.terms - head.terms;
+    for (int m = PDG_NL / 2; m > 0; m >>= 1) {
+      terms += static_cast<int64_t>(shfl_xor_u64(static_cast<uint64_t>(terms), m));
+      lo = add_rd(lo, bitsd(shfl_xor_u64(dbits(lo), m)));
+      hi = add_ru(hi, bitsd(shfl_xor_u64(dbits(hi), m)));
+    }
     if (terms == 0) return 0.0 <= thr;  // an empty window reads 0
-    const int dec = window_mean_le(tail, head, thr);
+    const int dec = mean_le_bracket(lo, hi, terms, thr);
     if (dec >= 0) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
@@ -1491,50 +1565,44 @@ class EngineT {
     }
     return ddiv(sum, static_cast<double>(terms)) <= thr;
   }
-  PDG_HD static ufx_t head_prod(const Seg& g) {
-    fx_t f;
-    to_fx(g.gap, &f);
-    return g.cnt > 0 ? static_cast<ufx_t>(f) * static_cast<ufx_t>(g.cnt) : static_cast<ufx_t>(0);
-  }
 
-  // Exact fixed-point sum of the ITL gaps of steps (j0, k] of worker d (one
-  // sample per step) and the number of those gaps without an exact image.
-  // Step k is in the open segment; the segment holding j0 is at or after
-  // `hint` (the open-segment index when the round joined).
-  PDG_HD ufx_t seg_sum(int d, int32_t j0, int32_t k, int32_t hint, int32_t* inex) {
-    const DecodeW& w = SHP(s_->SM.dw)[d];
+  // Bracket [lo, hi] of the sum of the ITL gaps of steps (j0, k] of worker
+  // d (one sample per step), where step k is the step ending now. Every gap
+  // is fl(e_j - e_{j-1}) of consecutive step end times, so the sum is within
+  // a relative u of e_k - e_j0 (exactly equal when the subtractions are
+  // exact); e_j0 comes from the segment holding step j0, at or after `hint`
+  // (the open-segment index when the round joined).
+  PDG_HD void seg_span(int d, int32_t j0, int32_t hint, double* lo, double* hi) {
+    const int64_t t0_ = pb();
+    seg_span_(d, j0, hint, lo, hi);
+    pe(22, t0_);
+  }
+  PDG_HD void seg_span_(int d, int32_t j0, int32_t hint, double* lo, double* hi) {
+    const DecodeW& w = DW(d);
     if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
       fail();
-      *inex = 0;
-      return 0;
+      *lo = *hi = 0.0;
+      return;
     }
-    // prefix through step k (open segment)
-    const int32_t nk = k - w.sg.first + 1;
-    const ufx_t pk = w.sg.p1 + w.sg_fx * static_cast<ufx_t>(static_cast<uint32_t>(nk));
-    const int32_t ik = w.sg.inex1 + (w.sg.gx ? 0 : nk);
-    // prefix through step j0
-    const Seg* ring = seg_ring(d);
-    const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
-    ufx_t pj = 0;
-    int32_t ij = 0;
     const int32_t gi = seg_find(d, j0, hint);
-    if (gi >= 0) {
-      const Seg& g = gi == w.seg_end ? w.sg : ring[static_cast<uint32_t>(gi) & mask];
-      const int32_t nj = j0 - g.first + 1;  // >= 0 (j0 >= g.first - 1)
-      fx_t f;
-      to_fx(g.gap, &f);
-      pj = g.p1 + static_cast<ufx_t>(f) * static_cast<ufx_t>(static_cast<uint32_t>(nj < 0 ? 0 : nj));
-      ij = g.inex1 + (g.gx ? 0 : (nj < 0 ? 0 : nj));
+    if (gi < 0) {
+      fail();
+      *lo = *hi = 0.0;
+      return;
     }
-    *inex = ik - ij;
-    return pk - pj;
+    const Seg g = seg_at(d, gi);
+    const double ej = seg_time(g, j0);
+    const double now = s_->now_;
+    *lo = mul_rd(sub_rd(now, ej), 1.0 - 0x1p-51);
+    *hi = mul_ru(sub_ru(now, ej), 1.0 + 0x1p-51);
+    if (*lo < 0.0) *lo = 0.0;
   }
 
   // Index of the first segment at or after `hint` that holds step j (i.e.
   // j < first + n; the open segment has index seg_end), or -1. Segments are
   // ordered by first step; lanes test 32 candidates per ballot.
   PDG_HD int32_t seg_find(int d, int32_t j, int32_t hint) const {
-    const DecodeW& w = SHP(s_->SM.dw)[d];
+    const DecodeW& w = DW(d);
     const int32_t end = w.seg_end;
     const Seg* ring = seg_ring(d);
     const uint32_t mask = static_cast<uint32_t>(s_->C.segcap - 1);
@@ -1566,7 +1634,7 @@ class EngineT {
   // `hint` is the open-segment index when the round joined: the segment
   // holding step a is at or after it.
   PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s, int32_t hint) {
-    const DecodeW& w = SHP(s_->SM.dw)[d];
+    const DecodeW& w = DW(d);
     if (a > k) return s;
     if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
       fail();
@@ -1805,7 +1873,7 @@ class EngineT {
 
   // ---- prefill workers (sim_engine.cpp:354-453) ----
   PDG_HD void enqueue_remote(int p, int32_t i, int32_t ctx, int32_t incr) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PrefillW& w = PW(p);
     const double cost = t_prefill(ctx, incr, w.deg);
     if (!queue_push(w.q, GLP(s_->G.pq_s) + static_cast<size_t>(p) * s_->C.qcap, GLP(s_->G.pq_c) + static_cast<size_t>(p) * s_->C.qcap, i, cost))
       return;
@@ -1813,8 +1881,13 @@ class EngineT {
     try_start_compute(p);
   }
 
-  PDG_HD void try_stage(int p) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PDG_HD void try_stage(int p) {
+    const int64_t t0_ = pb();
+    try_stage_(p);
+    pe(23, t0_);
+  }
+  PDG_HD void try_stage_(int p) {
+    PrefillW& w = PW(p);
     if (w.staged || w.q.qh == w.q.qt) return;
     double cost;
     const int32_t stg = select_next(w.q, GLP(s_->G.pq_s) + static_cast<size_t>(p) * s_->C.qcap,
@@ -1823,7 +1896,7 @@ class EngineT {
     double ready = s_->now_;
     if (hist > 0) {
       // Lazy history read from the bound decode worker (sim_engine.cpp:368-383).
-      const int dd = SHP(s_->SM.dw)[GLP(s_->G.sess)[stg].bound].deg;
+      const int dd = DW(GLP(s_->G.sess)[stg].bound).deg;
       ready = dadd(s_->now_, t_kv(hist, dd, w.deg));
     }
     {  // warp-uniform stores (every lane writes the same values)
@@ -1837,7 +1910,7 @@ class EngineT {
   }
 
   PDG_HD void try_start_compute(int p) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PrefillW& w = PW(p);
     if (w.computing || !w.staged || w.pending || w.staged_ready > s_->now_) return;
     const double done = dadd(s_->now_, w.stg_cost);
     {  // warp-uniform stores (every lane writes the same values)
@@ -1851,10 +1924,10 @@ class EngineT {
   }
 
   PDG_HD void on_prefill_done(int p) {
-    PrefillW& w = SHP(s_->SM.pw)[p];
+    PrefillW& w = PW(p);
     const int32_t i = w.cur;
     w.computing = 0;  // warp-uniform store
-    const int dd = SHP(s_->SM.dw)[GLP(s_->G.sess)[i].bound].deg;
+    const int dd = DW(GLP(s_->G.sess)[i].bound).deg;
     heap_push(dadd(s_->now_, t_kv(l_incr_of(i), w.deg, dd)), kKvTransferDone, static_cast<uint32_t>(i),
               static_cast<uint32_t>(p));
     try_stage(p);
@@ -1862,7 +1935,7 @@ class EngineT {
   }
 
   PDG_HD void on_history_read(int p) {
-    SHP(s_->SM.pw)[p].pending = 0;  // warp-uniform store
+    PW(p).pending = 0;  // warp-uniform store
     try_start_compute(p);
   }
 
@@ -1899,7 +1972,7 @@ class EngineT {
     const int32_t ridx = GLP(s_->T.round_off)[i] + round - 1;
     const int32_t incr = GLP(s_->T.incr)[ridx];
     const int32_t dec = GLP(s_->T.dec)[ridx];
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     interrupt_run(d);
     const int32_t join = w.steps;  // first token in the next step started
     const uint64_t key =
@@ -1922,7 +1995,7 @@ class EngineT {
 
   // ---- decode workers (sim_engine.cpp:488-583) ----
   PDG_HD void enqueue_local(int d, int32_t i, int32_t ctx, int32_t incr) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     const double cost = t_prefill(ctx, incr, w.deg);
     if (!queue_push(w.q, GLP(s_->G.dq_s) + static_cast<size_t>(d) * s_->C.qcap, GLP(s_->G.dq_c) + static_cast<size_t>(d) * s_->C.qcap, i, cost))
       return;
@@ -1936,7 +2009,7 @@ class EngineT {
     pe(kProfAdvance, t0);
   }
   PDG_HD void advance_decode_(int d) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     if (w.stepping || w.prefilling) return;
     if (w.q.qh != w.q.qt) {
       // Local prefill preempts decoding until the queue drains.
@@ -1997,7 +2070,7 @@ class EngineT {
       const int mine = base + lane_id();
       bool need = false;
       if (mine < D) {
-        const DecodeW& w = SHP(s_->SM.dw)[mine];
+        const DecodeW& w = DW(mine);
         need = w.stepping && w.steps - 1 < w.run_b && w.cur_end <= t;
       }
       uint32_t m = ballot(need);
@@ -2016,7 +2089,7 @@ class EngineT {
     pe(kProfCatchUp, t0);
   }
   PDG_HD void catch_up_worker_(int d, double t, uint32_t kind) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     const int64_t kvb = PDG_PROF.kv_bytes_per_token;
     while (w.stepping && w.steps - 1 < w.run_b) {
       const double e = w.cur_end;
@@ -2043,6 +2116,7 @@ class EngineT {
       // Bulk: the following steps add exactly the same gap while the end
       // time stays in one binade; complete all of them that end before t.
       const int32_t room = w.run_b - (k + 1);
+      const int64_t tb0_ = pb();
       if (room > 0 && next < t) {
         const double g = dsub(next, e);
         const int64_t m = stable_run(e, dur, g, t, room);
@@ -2057,6 +2131,7 @@ class EngineT {
           }
         }
       }
+      pe(21, tb0_);
       // warp-uniform stores
       w.last_step_t = end;
       w.kv_used = kv + static_cast<int64_t>(cohort) * done * kvb;
@@ -2129,7 +2204,7 @@ class EngineT {
   // A join or a local prefill on a worker whose in-flight step is silent:
   // that step's end becomes an explicit event (its successor differs).
   PDG_HD void interrupt_run(int d) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     if (!s_->lazy_ || !w.stepping) return;
     catch_up_worker(d, s_->now_, s_->cur_kind_);
     const int32_t k = w.steps - 1;
@@ -2140,7 +2215,7 @@ class EngineT {
   }
 
   PDG_HD void on_local_prefill_done(int d) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     const int32_t i = w.cur;
     w.prefilling = 0;  // warp-uniform store
     complete_task(i, true, -1, d);
@@ -2148,7 +2223,7 @@ class EngineT {
   }
 
   PDG_HD void on_decode_step(int d) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    DecodeW& w = DW(d);
     if (s_->lazy_) catch_up_worker(d, s_->now_, kDecodeStep);
     const int32_t k = w.steps - 1;  // index of the step that just ended
     const int32_t cohort = w.cohort_n;
@@ -2179,20 +2254,20 @@ class EngineT {
       const int32_t dec = GLP(s_->T.dec)[ridx];
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
-      ufx_t fxs = s.itl_fx;
-      int32_t inex = s.itl_inex;
+      double ilo = s.itl_lo, ihi = s.itl_hi;
       if (s_->exact_itl_) {
         sum = seg_fold(d, s.join + 1, k, sum, s.seg_hint);
       } else if (dec > 1) {
-        int32_t ri;
-        fxs += seg_sum(d, s.join, k, s.seg_hint, &ri);
-        inex += ri;
+        double rlo, rhi;
+        seg_span(d, s.join, s.seg_hint, &rlo, &rhi);
+        ilo = add_rd(ilo, rlo);
+        ihi = add_ru(ihi, rhi);
       }
       const bool last = s.round == GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
       {  // warp-uniform stores (every lane writes the same values)
         s.itl_sum = sum;
-        s.itl_fx = fxs;
-        s.itl_inex = inex;
+        s.itl_lo = ilo;
+        s.itl_hi = ihi;
         s.itl_cnt += dec - 1;
         s.ctx += dec;
         --w.batch_n;
@@ -2230,12 +2305,7 @@ class EngineT {
       itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
     } else {
       // search mode: certified decision of fl(fold / cnt) <= itl_thres
-      ExactSum es;
-      es.sum = static_cast<fx_t>(s.itl_fx);
-      es.terms = cnt;
-      es.inexact = s.itl_inex;
-      es.reserved = 0;
-      const int dec = mean_le_certified(es, s_->T.itl_thres);
+      const int dec = mean_le_bracket(s.itl_lo, s.itl_hi, cnt, s_->T.itl_thres);
       if (dec < 0) {  // inside the error band: replay this pair with exact folds
         s_->abort_ = 1;
         return;
@@ -2244,7 +2314,7 @@ class EngineT {
     }
     const bool slo_ok = ttft_ok && itl_ok;
     {  // warp-uniform stores (every lane writes the same values)
-      SHP(s_->SM.dw)[d].kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
+      DW(d).kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
       if (s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
         o.session_id = GLP(s_->T.sid)[i];
@@ -2266,8 +2336,13 @@ class EngineT {
   }
 
   // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
-  PDG_HD void fh_push(int d, uint64_t key) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    PDG_HD void fh_push(int d, uint64_t key) {
+    const int64_t t0_ = pb();
+    fh_push_(d, key);
+    pe(17, t0_);
+  }
+  PDG_HD void fh_push_(int d, uint64_t key) {
+    DecodeW& w = DW(d);
     const int32_t n = w.fh_n;
     if (n >= s_->C.fcap) {
       fail();
@@ -2290,8 +2365,13 @@ class EngineT {
     }
   }
 
-  PDG_HD void fh_pop(int d) {
-    DecodeW& w = SHP(s_->SM.dw)[d];
+    PDG_HD void fh_pop(int d) {
+    const int64_t t0_ = pb();
+    fh_pop_(d);
+    pe(17, t0_);
+  }
+  PDG_HD void fh_pop_(int d) {
+    DecodeW& w = DW(d);
     uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
     {  // warp-uniform stores (every lane writes the same values)
       const int32_t n = w.fh_n - 1;
@@ -2319,7 +2399,7 @@ class EngineT {
   }
 };
 
-using Engine = EngineT<false>;
+using Engine = EngineT<false>;  // host (test) build: pointer-based slot layout
 
 #if defined(__CUDA_ARCH__)
 #undef s_

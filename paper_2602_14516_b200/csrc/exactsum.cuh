@@ -102,6 +102,64 @@ PDG_HD int mean_le_certified(const ExactSum& s, double thr) {
   return -1;
 }
 
+// ---- directed rounding (rigorous brackets). Host (test) builds move one
+// ulp outward from round-to-nearest, a valid and slightly looser bound.
+PDG_HD double add_rd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dadd_rd(a, b);
+#else
+  return __builtin_nextafter(a + b, -__builtin_huge_val());
+#endif
+}
+PDG_HD double add_ru(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dadd_ru(a, b);
+#else
+  return __builtin_nextafter(a + b, __builtin_huge_val());
+#endif
+}
+PDG_HD double sub_rd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dsub_rd(a, b);
+#else
+  return __builtin_nextafter(a - b, -__builtin_huge_val());
+#endif
+}
+PDG_HD double sub_ru(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dsub_ru(a, b);
+#else
+  return __builtin_nextafter(a - b, __builtin_huge_val());
+#endif
+}
+PDG_HD double mul_rd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dmul_rd(a, b);
+#else
+  return __builtin_nextafter(a * b, -__builtin_huge_val());
+#endif
+}
+PDG_HD double mul_ru(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dmul_ru(a, b);
+#else
+  return __builtin_nextafter(a * b, __builtin_huge_val());
+#endif
+}
+
+// Decides fl(fold(x_1..x_n) / n) <= thr for non-negative terms whose exact
+// sum S is known to lie in [lo, hi]: the fold lies in
+// [lo (1 - gamma), hi (1 + gamma)]; the margin is 16x gamma_{n-1} plus slack
+// for the rounding of these products. 1 true, 0 false, -1 undecided.
+PDG_HD int mean_le_bracket(double lo, double hi, int64_t n, double thr) {
+  if (n <= 0 || n >= (1ll << 40) || !(hi < 1e300)) return -1;
+  const double nt = static_cast<double>(n) * thr;
+  const double m = fold_margin(n);
+  if (hi * (1.0 + m) <= nt * (1.0 - m)) return 1;
+  if (lo * (1.0 - m) >= nt * (1.0 + m)) return 0;
+  return -1;
+}
+
 // Running prefix of a lazily trimmed window: the window's exact sum is the
 // difference of two prefixes. Sums wrap modulo 2^128 (unsigned arithmetic),
 // which keeps every in-window difference exact.

@@ -323,8 +323,11 @@ inline double curve_max_upto(const pdsim_curve& c, double hi) {
 
 // Workspace capacities: provable upper bounds for every ring and heap of a
 // replay.
+// `dres`/`pres` (0: dmax/pmax) are the worker entries reserved in shared
+// memory; the device picks them from a few compiled layouts.
 inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax, int dmax,
-                         const pdsim_profile& prof, const pdsim_sched_params& prm, size_t smem_budget = 0) {
+                         const pdsim_profile& prof, const pdsim_sched_params& prm, size_t smem_budget = 0,
+                         int dres = 0, int pres = 0) {
   Caps c{};
   int64_t S = 1, R = 1, maxdec = 1, maxincr = 1, tdec = 1;
   for (const PackedTrace* t : traces) {
@@ -354,6 +357,8 @@ inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax
   c.S = static_cast<int32_t>(S);
   c.pmax = std::max(pmax, 0);
   c.dmax = std::max(dmax, 1);
+  c.dres = std::max(dres, c.dmax);
+  c.pres = std::max(pres, std::max(c.pmax, 1));
   c.hcap = static_cast<int32_t>(S + 2 * c.pmax + c.dmax + 8);
   // Session-event heap entries kept in shared memory (the rest spills).
   c.hs = 1;

@@ -138,8 +138,8 @@ def test_engine_heap_spill_to_global_matches_golden():
 
 @pytest.mark.parametrize("entry", CASES, ids=golden_cases.ids())
 def test_engine_search_mode_counts_match_golden(entry):
-    """Without record arrays the engine runs its search-mode paths (exact
-    fixed-point per-session ITL sums with certified verdicts); counters and
+    """Without record arrays the engine runs its search-mode paths (per-session
+    ITL sums bracketed with directed rounding, certified verdicts); counters and
     attainment must still equal the reference's."""
     c = entry["case"]
     trace, plan, prof, params = parity.build_case(c)

@@ -33,7 +33,8 @@ def main(cfg="C2"):
                       for k, name in enumerate(["select", "arrival", "interaction", "writeback", "decode_step",
                                                 "local_prefill_done", "prefill_done", "history_read",
                                                 "~route", "~enqueue", "~catch_up", "~finisher", "~advance_decode",
-                                                "~complete_task", "~heap", "~dequeue"])},
+                                                "~complete_task", "~heap", "~dequeue", "~seg_append", "~fh", "~ttft_add",
+                                                "~itl_slack", "~ttft_slack", "~bulk", "~seg_sum", "~try_stage"])},
            "replayed_pairs": prof[2]}
     print(json.dumps(out, indent=1))
 
