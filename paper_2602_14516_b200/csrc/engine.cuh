@@ -266,6 +266,9 @@ struct PrefillW {  // shared memory
 // the same ITL sample count per step: step j (first <= j < first + n) ends
 // at t0 + (j - first) * gap exactly (each step adds exactly `gap`).
 struct Seg {
+  double plo;     // bracket [plo, phi] of the exact ITL-sample sum over every
+  double phi;     //   step before this segment (directed rounding)
+  int64_t pterms; // ITL samples before this segment
   double t0;     // end time of step `first`
   double gap;    // every step's ITL gap (end - previous end)
   int32_t first; // first step index
@@ -779,6 +782,9 @@ class EngineT {
         DecodeW& w = DW(d);
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
+        w.sg.plo = 0.0;
+        w.sg.phi = 0.0;
+        w.sg.pterms = 0;
         w.sg.t0 = 0.0;
         w.sg.gap = 0.0;
         w.sg.first = 0;
@@ -1454,8 +1460,13 @@ class EngineT {
           return;
         }
       }
-      seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = w.sg;
+      const Seg c = w.sg;
+      seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = c;
       w.seg_end = end + 1;
+      const int64_t k = static_cast<int64_t>(c.cnt) * c.n;
+      w.sg.plo = add_rd(c.plo, mul_rd(static_cast<double>(k), c.gap));
+      w.sg.phi = add_ru(c.phi, mul_ru(static_cast<double>(k), c.gap));
+      w.sg.pterms = c.pterms + k;
     }
     w.sg.t0 = t0;
     w.sg.gap = gap;
@@ -1528,29 +1539,21 @@ class EngineT {
     seg_trim(d, s_->now_);
     const DecodeW& w = DW(d);
     // Exact window sum S = sum over in-window steps of cnt * gap, bracketed
-    // with directed rounding; lanes take segments, the bounds combine in any
-    // order. The reference's fold differs from S by <= gamma_{n-1} S.
-    const int32_t h0 = w.seg_head, h1 = w.seg_end, off = w.seg_off;
-    int64_t terms = 0;
-    double lo = 0.0, hi = 0.0;
-    for (int32_t base = h0; base <= h1; base += PDG_NL) {
-      const int32_t i = base + lane_id();
-      if (i <= h1) {
-        const Seg g = seg_at(d, i);
-        const int32_t nn = g.n - (i == h0 ? off : 0);
-        if (nn > 0 && g.cnt > 0) {
-          const int64_t c = static_cast<int64_t>(g.cnt) * nn;
-          terms += c;
-          lo = add_rd(lo, mul_rd(static_cast<double>(c), g.gap));
-          hi = add_ru(hi, mul_ru(static_cast<double>(c), g.gap));
-        }
-      }
-    }
-    for (int m = PDG_NL / 2; m > 0; m >>= 1) {
-      terms += static_cast<int64_t>(shfl_xor_u64(static_cast<uint64_t>(terms), m));
-      lo = add_rd(lo, bitsd(shfl_xor_u64(dbits(lo), m)));
-      hi = add_ru(hi, bitsd(shfl_xor_u64(dbits(hi), m)));
-    }
+    // by the difference of two directed-rounding prefix brackets: after the
+    // open segment (tail) and before the first in-window step (head). The
+    // reference's fold differs from S by <= gamma_{n-1} S.
+    const Seg& o = w.sg;
+    const int64_t ko = static_cast<int64_t>(o.cnt) * o.n;
+    const double tlo = add_rd(o.plo, mul_rd(static_cast<double>(ko), o.gap));
+    const double thi = add_ru(o.phi, mul_ru(static_cast<double>(ko), o.gap));
+    const Seg h = seg_at(d, w.seg_head);
+    const int64_t kh = static_cast<int64_t>(h.cnt) * (w.seg_off < h.n ? w.seg_off : h.n);
+    const double hlo = add_rd(h.plo, mul_rd(static_cast<double>(kh), h.gap));
+    const double hhi = add_ru(h.phi, mul_ru(static_cast<double>(kh), h.gap));
+    const int64_t terms = o.pterms + ko - (h.pterms + kh);
+    double lo = sub_rd(tlo, hhi);
+    const double hi = sub_ru(thi, hlo);
+    if (lo < 0.0) lo = 0.0;
     if (terms == 0) return 0.0 <= thr;  // an empty window reads 0
     const int dec = mean_le_bracket(lo, hi, terms, thr);
     if (dec >= 0) return dec == 1;
