@@ -102,13 +102,16 @@ def c1():
                     "llama3-8b, fixed P:2x1 D:2x1, toolbench 1k sessions x 4 fixed rounds @8/s, 1 replay")
 
 
-def c2(sessions=10000, rate=16.0, seed=5, total_gpus=8):
+def c2(sessions=10000, rate=16.0, seed=5, total_gpus=8, replicas=1):
+    """C2; with replicas > 1 (the multi-GPU weak-scaling form) trace replica
+    k uses gen seed seed + k."""
     st = trace_stats("toolbench")
-    tr = native.gen_trace(st, rate, sessions, seed)
+    trs = [native.gen_trace(st, rate, sessions, seed + k) for k in range(replicas)]
     plans = native.enumerate_plans(DEGREES, total_gpus)
-    return Workload("C2", "llama3-8b", [tr], plans, abi.default_params(), ENGINE_SEED, total_gpus,
+    rep = "" if replicas == 1 else f" x {replicas} replicas (seeds {seed}..{seed + replicas - 1})"
+    return Workload("C2", "llama3-8b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
                     f"llama3-8b, all {len(plans)} N={total_gpus} P/D plans over degrees {{1,2,4,8}}, "
-                    f"toolbench {sessions} sessions @{rate}/s")
+                    f"toolbench {sessions} sessions @{rate}/s{rep}")
 
 
 def c3(sessions=50000, rate=20.0, replicas=16, total_gpus=8):
