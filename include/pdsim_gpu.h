@@ -294,9 +294,11 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
  * fold, 12 advance_decode, 13 complete_task, 14 session-event heap,
  * 15 queue dequeue (reorder), 16 step-log append, 17 finisher heap,
  * 18 TTFT window add, 19 ITL slack test, 20 TTFT slack test, 21 bulk silent
- * steps, 22 per-round ITL sum, 23 prefill staging. `replayed` counts pairs
+ * steps, 22 per-round ITL sum, 23 prefill staging, 24 catch-up calls with
+ * nothing to do (count), 25 stable_run, 26 catch-up iterations (count),
+ * 27 admission catch-up over all decode workers. `replayed` counts pairs
  * whose fast attempt was replayed in exact mode. */
-#define PDSIM_PROF_BUCKETS 24
+#define PDSIM_PROF_BUCKETS 28
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
 int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts,
                                int64_t* replayed);

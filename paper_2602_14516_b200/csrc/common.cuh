@@ -68,13 +68,22 @@ PDG_HD double bitsd(uint64_t u) {
 }
 
 // ---- exact integer helpers without the u64 division subroutine ----
-// floor(a / d) for a < 2^53, 1 <= d < 2^53: the correctly rounded fp64
-// quotient is n or n + 1 (rounding is monotonic and n is representable);
-// one exact integer check fixes it.
+// floor(a / d) for a < 2^53, 1 <= d < 2^53 without a division subroutine:
+// a hardware reciprocal estimate refined by two Newton steps gives the
+// quotient to within one; one exact integer check on each side fixes it.
 PDG_HD uint64_t udiv53(uint64_t a, uint64_t d) {
 #if defined(__CUDA_ARCH__)
-  uint64_t q = static_cast<uint64_t>(__ddiv_rz(static_cast<double>(a), static_cast<double>(d)));
-  if (q * d > a) --q;
+  const double dd = static_cast<double>(d);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(dd));
+  r = __fma_rn(__fma_rn(-dd, r, 1.0), r, r);
+  r = __fma_rn(__fma_rn(-dd, r, 1.0), r, r);
+  uint64_t q = static_cast<uint64_t>(__dmul_rz(static_cast<double>(a), r));
+  if (q * d > a) {
+    --q;
+  } else if ((q + 1) * d <= a) {
+    ++q;
+  }
   return q;
 #else
   return a / d;

@@ -1046,25 +1046,88 @@ class EngineT {
     s_->adm_head_ = i + 1;
   }
 
-  PDG_HD int bind_session() {  // least KV bytes, lowest index on ties
-    if (s_->lazy_) catch_up(s_->now_, s_->cur_kind_);
-    int best = 0;
-    int64_t bv = DW(0).kv_used;
-    for (int d = 1; d < s_->PL.D; ++d) {
-      const int64_t v = DW(d).kv_used;
-      if (v < bv) {
-        bv = v;
-        best = d;
+  // Least KV bytes, lowest index on ties (coordinator.cpp:60-72). In lazy
+  // mode a worker's KV bytes include the silent steps of its in-flight run
+  // that end before now; lanes project them per worker without advancing
+  // the run (the step log is materialised when the worker is next observed).
+  PDG_HD int bind_session(int64_t* kv_best) {
+    const int64_t tc0_ = pb();
+    const int D = s_->PL.D;
+    const double t = s_->now_;
+    const uint32_t kind = s_->cur_kind_;
+    const bool lazy = s_->lazy_ != 0;
+    const int64_t kvb = PDG_PROF.kv_bytes_per_token;
+    uint64_t key = ~0ull;
+    bool ab = false;
+    for (int base = 0; base < D; base += PDG_NL) {
+      const int d = base + lane_id();
+      if (d < D) {
+        const DecodeW& w = DW(d);
+        int64_t kv = w.kv_used;
+        if (lazy) kv += static_cast<int64_t>(w.cohort_n) * silent_done(w, t, kind, &ab) * kvb;
+        const uint64_t k = (static_cast<uint64_t>(kv) << 6) | static_cast<uint64_t>(d);
+        if (k < key) key = k;
       }
     }
-    return best;
+    for (int m = PDG_NL / 2; m > 0; m >>= 1) {
+      const uint64_t o = shfl_xor_u64(key, m);
+      if (o < key) key = o;
+    }
+    if (ballot(ab)) s_->abort_ = 1;
+    *kv_best = static_cast<int64_t>(key >> 6);
+    pe(27, tc0_);
+    return static_cast<int>(key & 63u);
+  }
+
+  // Silent steps of w's in-flight run that end before t: exactly the steps
+  // catch_up_worker(d, t, kind) would advance, without advancing them.
+  PDG_HD int64_t silent_done(const DecodeW& w, double t, uint32_t kind, bool* abort) const {
+    if (!w.stepping) return 0;
+    const int32_t run_b = w.run_b;
+    int32_t k = w.steps - 1;
+    double e = w.cur_end;
+    const double dur = w.dur;
+    int64_t total = 0;
+    while (k < run_b) {
+      if (e > t) break;
+      if (e == t) {
+        if (kind == kDecodeStep) *abort = true;
+        break;
+      }
+      int32_t done = 1;
+      double end = e;
+      double next = dadd(e, dur);
+      if (!(next > e)) {
+        *abort = true;
+        break;
+      }
+      const int32_t room = run_b - (k + 1);
+      if (room > 0 && next < t) {
+        const double g = dsub(next, e);
+        const int64_t m = stable_run(e, dur, g, t, room);
+        if (m > 0) {
+          end = dadd(next, dmul(static_cast<double>(m - 1), g));
+          done += static_cast<int32_t>(m);
+          next = dadd(end, dur);
+          if (!(next > end)) {
+            *abort = true;
+            break;
+          }
+        }
+      }
+      total += done;
+      k += done;
+      e = next;
+    }
+    return total;
   }
 
   PDG_COLD bool try_admit(int32_t i) {
-    const int best = bind_session();
+    int64_t kv_best;
+    const int best = bind_session(&kv_best);
     const DecodeW& w = DW(best);
     const int64_t first = static_cast<int64_t>(GLP(s_->T.incr)[GLP(s_->T.round_off)[i]]) * PDG_PROF.kv_bytes_per_token;
-    if (w.kv_used + first > w.kv_cap) return false;
+    if (kv_best + first > w.kv_cap) return false;
     SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.bound = static_cast<int8_t>(best);
@@ -2094,9 +2157,11 @@ class EngineT {
   PDG_HD void catch_up_worker_(int d, double t, uint32_t kind) {
     DecodeW& w = DW(d);
     const int64_t kvb = PDG_PROF.kv_bytes_per_token;
+    if (kProf && !(w.stepping && w.steps - 1 < w.run_b && w.cur_end <= t)) pe(24, pdg_clock());
     while (w.stepping && w.steps - 1 < w.run_b) {
       const double e = w.cur_end;
       if (e > t) break;
+      if (kProf) pe(26, pdg_clock());
       if (e == t) {
         if (kind == kDecodeStep) s_->abort_ = 1;
         break;
@@ -2122,7 +2187,9 @@ class EngineT {
       const int64_t tb0_ = pb();
       if (room > 0 && next < t) {
         const double g = dsub(next, e);
+        const int64_t ts0_ = pb();
         const int64_t m = stable_run(e, dur, g, t, room);
+        pe(25, ts0_);
         if (m > 0) {
           seg_append(d, k + 1, static_cast<int32_t>(m), next, g, static_cast<uint32_t>(cohort));
           end = dadd(next, dmul(static_cast<double>(m - 1), g));

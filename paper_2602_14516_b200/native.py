@@ -259,10 +259,10 @@ class Context:
         self._check(lib().pdsim_gpu_set_profiling(self._h, 1 if enable else 0))
 
     def profile_counters(self):
-        """(cycles[24], counts[24], replayed_pairs) of the last search
+        """(cycles[28], counts[28], replayed_pairs) of the last search
         (bucket meanings: include/pdsim_gpu.h, PDSIM_PROF_BUCKETS)."""
-        cy = (C.c_int64 * 24)()
-        n = (C.c_int64 * 24)()
+        cy = (C.c_int64 * 28)()
+        n = (C.c_int64 * 28)()
         rp = C.c_int64(0)
         self._check(lib().pdsim_gpu_profile_counters(self._h, cy, n, C.byref(rp)))
         return list(cy), list(n), rp.value

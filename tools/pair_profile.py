@@ -11,7 +11,7 @@ from paper_2602_14516_b200 import abi, native, workloads  # noqa: E402
 NAMES = ["select", "arrival", "interaction", "writeback", "decode_step", "local_prefill_done", "prefill_done",
          "history_read", "~route", "~enqueue", "~catch_up", "~finisher", "~advance_decode", "~complete_task",
          "~heap", "~dequeue", "~seg_append", "~fh", "~ttft_add", "~itl_slack", "~ttft_slack", "~bulk", "~seg_sum",
-         "~try_stage"]
+         "~try_stage", "#catch_up_idle", "~stable_run", "#catch_up_iter", "~bind_catch_up"]
 
 
 def phases(prof):
