@@ -25,11 +25,15 @@ $(PKG)/build/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(PKG)/build
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 
+$(PKG)/build/planner_host.o: $(CSRC)/planner_host.cpp $(HDRS)
+	@mkdir -p $(PKG)/build
+	$(CXX) $(HOSTFLAGS) -c $< -o $@
+
 $(PKG)/build/pdsim_cpp.o: $(CSRC)/pdsim_cpp.cpp $(HDRS) $(CPPHDRS)
 	@mkdir -p $(PKG)/build
 	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
 
-$(LIB): $(PKG)/build/capi.o $(PKG)/build/host_gen.o $(PKG)/build/pdsim_cpp.o
+$(LIB): $(PKG)/build/capi.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 # C++ drop-in API check program (links the product library; runs on a GPU box).

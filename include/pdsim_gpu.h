@@ -364,6 +364,63 @@ int64_t pdsim_enumerate_plans(const int32_t* degrees, int32_t n_degrees,
                               int32_t total_gpus, pdsim_plan* out,
                               int64_t capacity);
 
+/* ---- surrogate planner -------------------------------- */
+
+/* PhaseSimResult (planner.hpp:62-66); status is PDSIM_OK or the error the
+ * reference would throw (PDSIM_ERR_CONFIG: no prefill tasks / no sessions /
+ * no inter-token samples). */
+typedef struct pdsim_phase_result {
+  double p95;
+  int64_t sample_count;
+  int32_t infeasible;
+  int32_t status;
+} pdsim_phase_result;
+
+/* Batched single-replica phase simulations on the device, one CTA per job:
+ * job k = simulate_prefill_replica(traces[k], profile, degrees[k])
+ * (planner.cpp:75-104) and simulate_decode_replica(traces[k], profile,
+ * degrees[k]) (planner.cpp:106-226). A degree missing from the profile is a
+ * PDSIM_ERR_DOMAIN for the whole call (t_prefill/t_decode, perf_model.cpp
+ * :158-188). */
+int pdsim_gpu_phase_sims(pdsim_gpu_ctx* ctx, int32_t n_jobs, const pdsim_trace* traces,
+                         const int32_t* degrees, const pdsim_profile* profile,
+                         pdsim_phase_result* prefill, pdsim_phase_result* decode);
+
+/* LatencyCoefficients (planner.hpp:55-60) over the sorted unique degree list:
+ * degree i is feasible for a phase when infeasible_* [i] == 0 (tau_* [i] is
+ * then its P95 coefficient). */
+typedef struct pdsim_coefficients {
+  int32_t n_degrees;
+  int32_t degrees[PDSIM_MAX_DEGREES];
+  int32_t reserved;
+  double tau_pre[PDSIM_MAX_DEGREES];
+  double tau_dec[PDSIM_MAX_DEGREES];
+  int8_t infeasible_pre[PDSIM_MAX_DEGREES];
+  int8_t infeasible_dec[PDSIM_MAX_DEGREES];
+} pdsim_coefficients;
+
+/* estimate_coefficients (planner.cpp:228-283) for n_sets (rate, seed)
+ * settings in ONE device launch: for set s and degree n the host generates
+ * gen_trace(stats, rates[s] * n / total_gpus, 256, seeds[s] + 0x9E37...15 * n)
+ * with the reference RNG, and both phase sims of every (set, degree) run on
+ * the GPU. set_status[s] is the first error the reference would throw for
+ * set s (PDSIM_OK otherwise); argument errors fail the whole call. */
+int pdsim_gpu_estimate_coefficients(pdsim_gpu_ctx* ctx, const pdsim_trace_stats* stats, int32_t n_sets,
+                                    const double* rates, const uint64_t* seeds, const pdsim_profile* profile,
+                                    const int32_t* degrees, int32_t n_degrees, int32_t total_gpus,
+                                    pdsim_coefficients* out, int32_t* set_status);
+
+/* solve (planner.cpp:482-578), host C++: the exact min-Z assignment with the
+ * reference tie-break chain. plan/objective_z/gpus_used are written when
+ * *feasible is 1. Errors: PDSIM_ERR_CONFIG as check_coefficients/solve. */
+int pdsim_solve(const pdsim_coefficients* coeffs, int32_t total_gpus, pdsim_plan* plan, double* objective_z,
+                int32_t* gpus_used, int32_t* feasible);
+
+/* top_k (planner.cpp:605-657), host C++: the k best plans in solve order.
+ * Returns the number written (<= k) or -1 on error (pdsim_last_error). */
+int64_t pdsim_top_k(const pdsim_coefficients* coeffs, int32_t total_gpus, int32_t k, pdsim_plan* plans,
+                    double* objective_z, int32_t* gpus_used);
+
 /* Device-free CPU argmax helper used by multi-rank callers after the NCCL
  * reduction: max count, ties -> smallest index, negative = invalid. */
 int32_t pdsim_argmax_candidates(const int64_t* candidate_slo_ok,

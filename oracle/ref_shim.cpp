@@ -10,9 +10,12 @@
 //   - pdsim::gen_trace     (proj/src/workload.cpp:170-229)
 //   - pdsim::synth_profile (proj/src/perf_model.cpp:207-273)
 //   - pdsim::top_k         (proj/src/planner.cpp:605-657, enumeration pinning)
+//   - the surrogate planner: simulate_prefill_replica / simulate_decode_replica
+//     / estimate_coefficients / solve / top_k (proj/src/planner.cpp:75-657)
 //   - the CSV writers      (proj/src/metrics.cpp:366-474, FNV-1a fingerprints)
 // plus a std::thread pool replaying (candidate, replica) pairs: the reference's
 // CPU plan-search baseline.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -482,6 +485,90 @@ int64_t ref_top_k_plans(const int32_t* degrees, int32_t n_degrees, int32_t total
     n = static_cast<int64_t>(plans.size());
     for (std::size_t i = 0; out && i < plans.size() && static_cast<int64_t>(i) < capacity; ++i) {
       plan_to_pod(plans[i], &out[i]);
+    }
+  });
+  return n;
+}
+
+
+// ---- surrogate planner (planner.cpp:75-657) ----
+namespace {
+pdsim::LatencyCoefficients coeffs_from_pod(const pdsim_coefficients& c) {
+  pdsim::LatencyCoefficients out;
+  for (int i = 0; i < c.n_degrees; ++i) {
+    if (c.infeasible_pre[i]) out.infeasible_pre.insert(c.degrees[i]); else out.tau_pre[c.degrees[i]] = c.tau_pre[i];
+    if (c.infeasible_dec[i]) out.infeasible_dec.insert(c.degrees[i]); else out.tau_dec[c.degrees[i]] = c.tau_dec[i];
+  }
+  return out;
+}
+std::vector<int> coeff_degrees(const pdsim_coefficients& c) {
+  return std::vector<int>(c.degrees, c.degrees + c.n_degrees);
+}
+}  // namespace
+
+int ref_phase_sims(const pdsim_trace* tr, const pdsim_profile* prof, int32_t degree, pdsim_phase_result* pre,
+                   pdsim_phase_result* dec) {
+  const pdsim::Trace t = trace_from_pod(*tr);
+  const pdsim::PerfProfile p = profile_from_pod(*prof);
+  const int rc1 = guarded([&] {
+    const pdsim::PhaseSimResult r = pdsim::simulate_prefill_replica(t, p, degree);
+    *pre = pdsim_phase_result{r.p95, r.sample_count, r.infeasible ? 1 : 0, PDSIM_OK};
+  });
+  if (rc1 != PDSIM_OK) *pre = pdsim_phase_result{0.0, 0, 0, rc1};
+  const int rc2 = guarded([&] {
+    const pdsim::PhaseSimResult r = pdsim::simulate_decode_replica(t, p, degree);
+    *dec = pdsim_phase_result{r.p95, r.sample_count, r.infeasible ? 1 : 0, PDSIM_OK};
+  });
+  if (rc2 != PDSIM_OK) *dec = pdsim_phase_result{0.0, 0, 0, rc2};
+  return PDSIM_OK;
+}
+
+int ref_estimate_coefficients(const pdsim_trace_stats* stats, const char* name, double rate,
+                              const pdsim_profile* prof, const int32_t* degrees, int32_t n_degrees,
+                              int32_t total_gpus, uint64_t seed, pdsim_coefficients* out) {
+  return guarded([&] {
+    const std::vector<int> ds(degrees, degrees + n_degrees);
+    const pdsim::LatencyCoefficients c = pdsim::estimate_coefficients(stats_from_pod(*stats, name), rate,
+                                                                      profile_from_pod(*prof), ds, total_gpus, seed);
+    std::memset(out, 0, sizeof(*out));
+    std::vector<int> ts = ds;
+    std::sort(ts.begin(), ts.end());
+    ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+    out->n_degrees = static_cast<int32_t>(ts.size());
+    for (std::size_t k = 0; k < ts.size(); ++k) {
+      const int n = ts[k];
+      out->degrees[k] = n;
+      out->infeasible_pre[k] = c.infeasible_pre.count(n) ? 1 : 0;
+      out->infeasible_dec[k] = c.infeasible_dec.count(n) ? 1 : 0;
+      out->tau_pre[k] = c.tau_pre.count(n) ? c.tau_pre.at(n) : 0.0;
+      out->tau_dec[k] = c.tau_dec.count(n) ? c.tau_dec.at(n) : 0.0;
+    }
+  });
+}
+
+int ref_solve(const pdsim_coefficients* c, int32_t total_gpus, pdsim_plan* plan, double* z, int32_t* gpus,
+              int32_t* feasible) {
+  return guarded([&] {
+    const pdsim::DeploymentPlan p = pdsim::solve(coeffs_from_pod(*c), total_gpus, coeff_degrees(*c));
+    *feasible = p.feasible ? 1 : 0;
+    if (p.feasible) {
+      plan_to_pod(p, plan);
+      *z = p.objective_z;
+      *gpus = p.gpus_used;
+    }
+  });
+}
+
+int64_t ref_top_k(const pdsim_coefficients* c, int32_t total_gpus, int32_t k, pdsim_plan* plans, double* z,
+                  int32_t* gpus) {
+  int64_t n = -1;
+  guarded([&] {
+    const auto ps = pdsim::top_k(coeffs_from_pod(*c), total_gpus, coeff_degrees(*c), k);
+    n = static_cast<int64_t>(ps.size());
+    for (std::size_t i = 0; i < ps.size(); ++i) {
+      plan_to_pod(ps[i], &plans[i]);
+      z[i] = ps[i].objective_z;
+      gpus[i] = ps[i].gpus_used;
     }
   });
   return n;

@@ -47,6 +47,16 @@ def lib():
                                       C.c_int32, P(abi.Attainment), P(C.c_int8), P(C.c_double)]
         L.ref_top_k_plans.argtypes = [P(C.c_int32), C.c_int32, C.c_int32, P(abi.Plan), C.c_int64]
         L.ref_top_k_plans.restype = C.c_int64
+        L.ref_phase_sims.argtypes = [P(abi.Trace), P(abi.Profile), C.c_int32, P(abi.PhaseResult),
+                                     P(abi.PhaseResult)]
+        L.ref_estimate_coefficients.argtypes = [P(abi.TraceStats), C.c_char_p, C.c_double, P(abi.Profile),
+                                                P(C.c_int32), C.c_int32, C.c_int32, C.c_uint64,
+                                                P(abi.Coefficients)]
+        L.ref_solve.argtypes = [P(abi.Coefficients), C.c_int32, P(abi.Plan), P(C.c_double), P(C.c_int32),
+                                P(C.c_int32)]
+        L.ref_top_k.argtypes = [P(abi.Coefficients), C.c_int32, C.c_int32, P(abi.Plan), P(C.c_double),
+                                P(C.c_int32)]
+        L.ref_top_k.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -161,3 +171,37 @@ def top_k_plans(degrees, total_gpus, capacity=1 << 20):
     out = (abi.Plan * max(n, 1))()
     lib().ref_top_k_plans(ds, len(degrees), total_gpus, out, n)
     return list(out)[:n]
+
+
+# ---- surrogate planner (reference planner.cpp:75-657) ----
+
+def phase_sims(trace, profile, degree):
+    """(prefill PhaseResult, decode PhaseResult) of the reference sims; a
+    result's status carries the error the reference threw (0 = ok)."""
+    pre, dec = abi.PhaseResult(), abi.PhaseResult()
+    lib().ref_phase_sims(C.byref(trace), C.byref(profile), degree, C.byref(pre), C.byref(dec))
+    return pre, dec
+
+
+def estimate_coefficients(stats, rate, profile, degrees, total_gpus, seed, name="custom"):
+    out = abi.Coefficients()
+    dg = (C.c_int32 * len(degrees))(*degrees)
+    rc = lib().ref_estimate_coefficients(C.byref(stats), name.encode(), rate, C.byref(profile), dg, len(degrees),
+                                         total_gpus, seed, C.byref(out))
+    return out, rc
+
+
+def solve(coeffs, total_gpus):
+    plan, z, g, f = abi.Plan(), C.c_double(), C.c_int32(), C.c_int32()
+    _check(lib().ref_solve(C.byref(coeffs), total_gpus, C.byref(plan), C.byref(z), C.byref(g), C.byref(f)))
+    return (plan, z.value, g.value) if f.value else None
+
+
+def top_k(coeffs, total_gpus, k):
+    plans = (abi.Plan * k)()
+    zs = (C.c_double * k)()
+    gs = (C.c_int32 * k)()
+    n = lib().ref_top_k(C.byref(coeffs), total_gpus, k, plans, zs, gs)
+    if n < 0:
+        raise RefError(1, lib().ref_last_error().decode())
+    return [(plans[i], zs[i], gs[i]) for i in range(n)]

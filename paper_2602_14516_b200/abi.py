@@ -229,6 +229,52 @@ class TraceStats(C.Structure):
     ]
 
 
+class PhaseResult(C.Structure):
+    """PhaseSimResult (planner.hpp:62-66) + the status the reference would throw."""
+    _fields_ = [
+        ("p95", C.c_double),
+        ("sample_count", C.c_int64),
+        ("infeasible", C.c_int32),
+        ("status", C.c_int32),
+    ]
+
+
+class Coefficients(C.Structure):
+    """LatencyCoefficients (planner.hpp:55-60) over the sorted degree list."""
+    _fields_ = [
+        ("n_degrees", C.c_int32),
+        ("degrees", C.c_int32 * MAX_DEGREES),
+        ("reserved", C.c_int32),
+        ("tau_pre", C.c_double * MAX_DEGREES),
+        ("tau_dec", C.c_double * MAX_DEGREES),
+        ("infeasible_pre", C.c_int8 * MAX_DEGREES),
+        ("infeasible_dec", C.c_int8 * MAX_DEGREES),
+    ]
+
+    def as_dict(self):
+        n = self.n_degrees
+        return {
+            "tau_pre": {self.degrees[i]: self.tau_pre[i] for i in range(n) if not self.infeasible_pre[i]},
+            "tau_dec": {self.degrees[i]: self.tau_dec[i] for i in range(n) if not self.infeasible_dec[i]},
+            "infeasible_pre": sorted(self.degrees[i] for i in range(n) if self.infeasible_pre[i]),
+            "infeasible_dec": sorted(self.degrees[i] for i in range(n) if self.infeasible_dec[i]),
+        }
+
+
+def make_coefficients(tau_pre, tau_dec, infeasible_pre=(), infeasible_dec=()):
+    """Coefficients from {degree: tau} dicts (+ infeasible degree sets)."""
+    c = Coefficients()
+    degs = sorted(set(tau_pre) | set(tau_dec) | set(infeasible_pre) | set(infeasible_dec))
+    c.n_degrees = len(degs)
+    for i, d in enumerate(degs):
+        c.degrees[i] = d
+        c.infeasible_pre[i] = 1 if d in infeasible_pre else 0
+        c.infeasible_dec[i] = 1 if d in infeasible_dec else 0
+        c.tau_pre[i] = tau_pre.get(d, 0.0)
+        c.tau_dec[i] = tau_dec.get(d, 0.0)
+    return c
+
+
 STRUCTS = {
     "pdsim_curve": Curve,
     "pdsim_profile": Profile,
@@ -245,6 +291,8 @@ STRUCTS = {
     "pdsim_search_output": SearchOutput,
     "pdsim_synth_spec": SynthSpec,
     "pdsim_trace_stats": TraceStats,
+    "pdsim_phase_result": PhaseResult,
+    "pdsim_coefficients": Coefficients,
 }
 
 

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -24,6 +25,7 @@
 
 #include "engine.cuh"
 #include "pack.hpp"
+#include "planner.cuh"
 #include "pdsim_gpu.h"
 
 namespace {
@@ -81,6 +83,8 @@ struct pdsim_gpu_ctx {
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
   DevBuf d_dec, d_ttft, d_sess;
+  // surrogate-planner phase sims
+  DevBuf d_ph_data, d_ph_traces, d_ph_jobs, d_ph_out, d_ph_scratch, d_ph_counter, d_ph_profile;
   // diagnostics
   int profiling = 0;
   int layout = 0;  // index of the compiled shared-memory layout (stage_impl)
@@ -263,9 +267,10 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   for (auto& t : ctx->packed) tp.push_back(&t);
   // Shared-memory budget per slot: generous when few pairs run at once.
   const int64_t pairs = static_cast<int64_t>(in->n_traces) * in->n_candidates;
-  const size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
-                             : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
-                                                          : (size_t(12) << 10);
+  size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
+                       : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
+                                                    : (size_t(10) << 10);
+  if (const char* v = getenv("PDSIM_SMEM_BUDGET")) smem_budget = static_cast<size_t>(atoll(v));  // tuning only
   // Compiled shared-memory layouts (replay_kernel<.., kD, kP>): N <= 8 plans
   // fit <8, 8>, N <= 16 plans <16, 16>; D + 2P <= 64 bounds the rest.
   const int lay = (dmax <= 8 && pmax <= 8) ? 0 : (dmax <= 16 && pmax <= 16) ? 1 : 2;
@@ -348,8 +353,9 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   size_t free_b = 0, total_b = 0;
   CU(ctx, cudaMemGetInfo(&free_b, &total_b));
   const size_t budget = std::min<size_t>(free_b / 2 + ctx->d_ws.bytes / 2, size_t(64) << 30);
-  const int64_t per_sm = std::max<int64_t>(
+  int64_t per_sm = std::max<int64_t>(
       1, std::min<int64_t>(32, static_cast<int64_t>((size_t(227) << 10) / std::max<size_t>(ctx->smem_bytes, 1))));
+  if (const char* v = getenv("PDSIM_SLOTS_PER_SM")) per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, atoll(v)));  // tuning only
   int64_t slots = std::min<int64_t>(std::max<int64_t>(n, 1), static_cast<int64_t>(ctx->sm_count) * per_sm);
   slots = std::min<int64_t>(slots, static_cast<int64_t>(budget / std::max<size_t>(ctx->slot_bytes, 1)));
   if (slots < 1) return set_err(ctx, PDSIM_ERR_CUDA, "search: workspace of one slot exceeds device memory");
@@ -459,6 +465,108 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     return set_err(ctx, PDSIM_ERR_INTERNAL, "engine capacity or invariant violated in at least one pair");
   }
   return PDSIM_OK;
+}
+
+// Surrogate-planner phase sims (planner.cuh) for jobs (trace, degree index).
+int phase_impl(pdsim_gpu_ctx* ctx, const std::vector<const pdsim_trace*>& traces, const std::vector<int>& trace_of,
+               const std::vector<int>& deg_idx, const pdsim_profile& profile, std::vector<pdg::PhaseOut>* out) {
+  pdg::HostError err;
+  if (!pdg::validate_profile(profile, &err)) return set_err(ctx, err.code, err.msg);
+  const size_t nt = traces.size(), nj = trace_of.size();
+  std::vector<pdg::PackedTrace> packed(nt);
+  int32_t max_r = 1, max_s = 1;
+  int64_t max_tok = 1;
+  size_t total = 0;
+  std::vector<pdg::HostError> perr(nt);
+  std::vector<char> pok(nt, 1);
+  pdg::parallel_for(nt, [&](size_t k) { pok[k] = pdg::pack_trace(*traces[k], &packed[k], &perr[k]) ? 1 : 0; });
+  for (size_t k = 0; k < nt; ++k) {
+    if (!pok[k]) return set_err(ctx, perr[k].code, perr[k].msg);
+    max_r = std::max(max_r, packed[k].R);
+    max_s = std::max(max_s, packed[k].S);
+    max_tok = std::max(max_tok, packed[k].total_decode);
+    total += pdg::align_up(packed[k].arrival.size() * 8 + 256) + pdg::align_up(packed[k].round_off.size() * 4 + 256) +
+             pdg::align_up(packed[k].incr.size() * 4 + 256) * 2 + pdg::align_up(packed[k].delay.size() * 8 + 256);
+  }
+  CU(ctx, ctx->d_ph_data.reserve(std::max<size_t>(total, 256)));
+  std::vector<char> host(std::max<size_t>(total, 256));
+  std::vector<pdg::PhaseTrace> pt(nt);
+  size_t off = 0;
+  char* dbase = ctx->d_ph_data.as<char>();
+  auto put = [&](const void* src, size_t bytes) -> void* {
+    void* dst = dbase + off;
+    if (bytes) memcpy(host.data() + off, src, bytes);
+    off = pdg::align_up(off + bytes + 1);
+    return dst;
+  };
+  for (size_t k = 0; k < nt; ++k) {
+    const pdg::PackedTrace& t = packed[k];
+    pt[k].S = t.S;
+    pt[k].R = t.R;
+    pt[k].total_decode = t.total_decode;
+    pt[k].arrival = static_cast<const double*>(put(t.arrival.data(), t.arrival.size() * 8));
+    pt[k].round_off = static_cast<const int32_t*>(put(t.round_off.data(), t.round_off.size() * 4));
+    pt[k].incr = static_cast<const int32_t*>(put(t.incr.data(), t.incr.size() * 4));
+    pt[k].dec = static_cast<const int32_t*>(put(t.dec.data(), t.dec.size() * 4));
+    pt[k].delay = static_cast<const double*>(put(t.delay.data(), t.delay.size() * 8));
+  }
+  std::vector<pdg::PhaseJob> jobs(nj);
+  for (size_t j = 0; j < nj; ++j) {
+    jobs[j].trace = trace_of[j];
+    jobs[j].deg = deg_idx[j];
+  }
+  int32_t sort_cap = 1;
+  while (sort_cap < max_r) sort_cap <<= 1;
+  const size_t per_cta = pdg::phase_scratch_bytes(sort_cap, max_tok, max_s);
+  // Up to 8 resident 256-thread CTAs per SM; each job is a serial event loop
+  // with CTA-wide reductions, so occupancy hides the barrier latency.
+  int threads = pdg::kPhaseThreads, per_sm = 8;
+  if (const char* v = getenv("PDSIM_PHASE_THREADS")) threads = atoi(v);      // tuning only
+  if (const char* v = getenv("PDSIM_PHASE_CTAS_PER_SM")) per_sm = atoi(v);  // tuning only
+  const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(nj), per_sm * ctx->sm_count));
+  CU(ctx, ctx->d_ph_traces.reserve(sizeof(pdg::PhaseTrace) * nt));
+  CU(ctx, ctx->d_ph_jobs.reserve(sizeof(pdg::PhaseJob) * std::max<size_t>(nj, 1)));
+  CU(ctx, ctx->d_ph_out.reserve(sizeof(pdg::PhaseOut) * std::max<size_t>(nj, 1)));
+  CU(ctx, ctx->d_ph_scratch.reserve(per_cta * static_cast<size_t>(ctas)));
+  CU(ctx, ctx->d_ph_counter.reserve(8));
+  CU(ctx, ctx->d_ph_profile.reserve(sizeof(pdsim_profile)));
+  CU(ctx, cudaMemcpyAsync(ctx->d_ph_data.p, host.data(), off, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->d_ph_traces.p, pt.data(), sizeof(pdg::PhaseTrace) * nt, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->d_ph_jobs.p, jobs.data(), sizeof(pdg::PhaseJob) * nj, cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemcpyAsync(ctx->d_ph_profile.p, &profile, sizeof(pdsim_profile), cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->d_ph_counter.p, 0, 8, ctx->stream));
+  CU(ctx, cudaMemsetAsync(ctx->d_ph_out.p, 0, sizeof(pdg::PhaseOut) * nj, ctx->stream));
+  pdg::PhaseArgs a;
+  a.traces = ctx->d_ph_traces.as<pdg::PhaseTrace>();
+  a.jobs = ctx->d_ph_jobs.as<pdg::PhaseJob>();
+  a.n_jobs = static_cast<int32_t>(nj);
+  a.sort_cap = sort_cap;
+  a.max_s = max_s;
+  a.run_cap = max_tok;
+  a.scratch = ctx->d_ph_scratch.as<char>();
+  a.scratch_bytes = per_cta;
+  a.next_job = ctx->d_ph_counter.as<unsigned long long>();
+  a.out = ctx->d_ph_out.as<pdg::PhaseOut>();
+  a.profile = ctx->d_ph_profile.as<pdsim_profile>();
+  if (nj > 0) {
+    pdg::phase_sim_kernel<<<static_cast<unsigned>(ctas), static_cast<unsigned>(threads), 0, ctx->stream>>>(a);
+    CU(ctx, cudaGetLastError());
+  }
+  out->assign(nj, pdg::PhaseOut());
+  CU(ctx, cudaMemcpyAsync(out->data(), ctx->d_ph_out.p, sizeof(pdg::PhaseOut) * nj, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(ctx, cudaStreamSynchronize(ctx->stream));
+  for (const auto& o : *out) {
+    if (o.pre_status == PDSIM_ERR_INTERNAL || o.dec_status == PDSIM_ERR_INTERNAL) {
+      return set_err(ctx, PDSIM_ERR_INTERNAL, "phase sim: scratch capacity violated");
+    }
+  }
+  return PDSIM_OK;
+}
+
+const char* phase_error_text(int which) {
+  return which == 0 ? "planner: reference trace has no prefill tasks"
+         : which == 1 ? "planner: reference trace has no sessions"
+                      : "planner: reference trace produced no inter-token samples";
 }
 
 }  // namespace
@@ -613,6 +721,132 @@ int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan
   }
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (out->sessions) pdg::sort_outcomes(out->sessions, out->n_sessions);
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_phase_sims(pdsim_gpu_ctx* ctx, int32_t n_jobs, const pdsim_trace* traces, const int32_t* degrees,
+                         const pdsim_profile* profile, pdsim_phase_result* prefill, pdsim_phase_result* decode) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n_jobs < 0 || (n_jobs > 0 && (!traces || !degrees)) || !profile) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "phase_sims: bad arguments");
+  }
+  std::vector<const pdsim_trace*> tv;
+  std::vector<int> trace_of, deg_idx;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const int di = pdg::degree_index(*profile, degrees[j]);
+    if (di < 0) return set_err(ctx, PDSIM_ERR_DOMAIN, "t_prefill: unknown degree " + std::to_string(degrees[j]));
+    tv.push_back(&traces[j]);
+    trace_of.push_back(j);
+    deg_idx.push_back(di);
+  }
+  std::vector<pdg::PhaseOut> out;
+  if (int rc = phase_impl(ctx, tv, trace_of, deg_idx, *profile, &out)) return rc;
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    const pdg::PhaseOut& o = out[static_cast<size_t>(j)];
+    if (prefill) prefill[j] = pdsim_phase_result{o.pre_p95, o.pre_samples, o.pre_infeasible, o.pre_status};
+    if (decode) decode[j] = pdsim_phase_result{o.dec_p95, o.dec_samples, o.dec_infeasible, o.dec_status};
+  }
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_estimate_coefficients(pdsim_gpu_ctx* ctx, const pdsim_trace_stats* stats, int32_t n_sets,
+                                    const double* rates, const uint64_t* seeds, const pdsim_profile* profile,
+                                    const int32_t* degrees, int32_t n_degrees, int32_t total_gpus,
+                                    pdsim_coefficients* out, int32_t* set_status) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!stats || !profile || !out || n_sets < 0 || (n_sets > 0 && (!rates || !seeds))) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "estimate_coefficients: bad arguments");
+  }
+  // Argument checks in the reference order (planner.cpp:232-249).
+  if (total_gpus < 1) return set_err(ctx, PDSIM_ERR_CONFIG, "planner: total_gpus must be >= 1");
+  if (!degrees || n_degrees < 1) return set_err(ctx, PDSIM_ERR_CONFIG, "planner: degree set is empty");
+  std::vector<int> ts(degrees, degrees + n_degrees);
+  std::sort(ts.begin(), ts.end());
+  ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+  if (ts.size() > PDSIM_MAX_DEGREES) return set_err(ctx, PDSIM_ERR_CONFIG, "planner: too many degrees");
+  std::vector<int> di(ts.size());
+  for (size_t k = 0; k < ts.size(); ++k) {
+    di[k] = pdg::degree_index(*profile, ts[k]);
+    if (di[k] < 0) return set_err(ctx, PDSIM_ERR_CONFIG, "planner: degree " + std::to_string(ts[k]) + " not covered by profile");
+  }
+  // Reference-load traces on the host RNG (workload.cpp:170-229).
+  const size_t nd = ts.size();
+  std::vector<pdsim_trace_buf*> bufs(static_cast<size_t>(n_sets) * nd, nullptr);
+  std::vector<pdsim_trace> views(bufs.size());
+  std::vector<int> status(static_cast<size_t>(n_sets), PDSIM_OK);
+  std::vector<std::string> msgs(static_cast<size_t>(n_sets));
+  std::vector<const pdsim_trace*> tv;
+  std::vector<int> trace_of, deg_idx, job_slot;
+  for (int32_t s = 0; s < n_sets; ++s) {
+    if (!(rates[s] > 0.0)) {
+      status[static_cast<size_t>(s)] = PDSIM_ERR_CONFIG;
+      msgs[static_cast<size_t>(s)] = "planner: arrival rate must be > 0";
+    }
+  }
+  // Host generation (libm-bound, must stay on the CPU) on all host threads.
+  std::vector<int> gen_rc(bufs.size(), PDSIM_OK);
+  std::vector<std::string> gen_msg(bufs.size());
+  pdg::parallel_for(bufs.size(), [&](size_t slot) {
+    const size_t s = slot / nd, k = slot % nd;
+    if (status[s] != PDSIM_OK) return;
+    const double share = rates[s] * static_cast<double>(ts[k]) / static_cast<double>(total_gpus);
+    const uint64_t seed = seeds[s] + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(ts[k]);
+    pdsim_trace_buf* b = nullptr;
+    gen_rc[slot] = pdsim_gen_trace(stats, share, 256, seed, &b);  // kCoefficientSessions (planner.cpp:33)
+    if (gen_rc[slot] != PDSIM_OK) {
+      gen_msg[slot] = pdsim_last_error();
+      return;
+    }
+    bufs[slot] = b;
+    pdsim_trace_buf_view(b, &views[slot]);
+  });
+  for (size_t slot = 0; slot < bufs.size(); ++slot) {  // first failing degree of each set, in order
+    const size_t s = slot / nd;
+    if (status[s] == PDSIM_OK && gen_rc[slot] != PDSIM_OK) {
+      status[s] = gen_rc[slot];
+      msgs[s] = gen_msg[slot];
+    }
+  }
+  for (size_t slot = 0; slot < bufs.size(); ++slot) {
+    if (!bufs[slot] || status[slot / nd] != PDSIM_OK) continue;
+    trace_of.push_back(static_cast<int>(tv.size()));
+    tv.push_back(&views[slot]);
+    deg_idx.push_back(di[slot % nd]);
+    job_slot.push_back(static_cast<int>(slot));
+  }
+  std::vector<pdg::PhaseOut> po;
+  const int rc = phase_impl(ctx, tv, trace_of, deg_idx, *profile, &po);
+  for (auto* b : bufs) pdsim_trace_buf_free(b);
+  if (rc) return rc;
+  for (int32_t s = 0; s < n_sets; ++s) {
+    pdsim_coefficients& c = out[s];
+    memset(&c, 0, sizeof(c));
+    c.n_degrees = static_cast<int32_t>(nd);
+    for (size_t k = 0; k < nd; ++k) c.degrees[k] = ts[k];
+  }
+  for (size_t j = 0; j < po.size(); ++j) {
+    const size_t slot = static_cast<size_t>(job_slot[j]), s = slot / nd, k = slot % nd;
+    const pdg::PhaseOut& o = po[j];
+    if (status[s] != PDSIM_OK) continue;
+    // The reference runs degrees in ascending order and throws at the first
+    // failing sim (prefill before decode).
+    if (o.pre_status != PDSIM_OK || o.dec_status != PDSIM_OK) {
+      status[s] = PDSIM_ERR_CONFIG;
+      msgs[s] = phase_error_text(o.pre_status != PDSIM_OK ? 0 : 2);
+      continue;
+    }
+    pdsim_coefficients& c = out[s];
+    c.infeasible_pre[k] = static_cast<int8_t>(o.pre_infeasible);
+    c.infeasible_dec[k] = static_cast<int8_t>(o.dec_infeasible);
+    c.tau_pre[k] = o.pre_infeasible ? 0.0 : o.pre_p95;
+    c.tau_dec[k] = o.dec_infeasible ? 0.0 : o.dec_p95;
+  }
+  for (int32_t s = 0; s < n_sets; ++s) {
+    if (set_status) set_status[s] = status[static_cast<size_t>(s)];
+    if (status[static_cast<size_t>(s)] != PDSIM_OK && !msgs[static_cast<size_t>(s)].empty()) {
+      ctx->err = msgs[static_cast<size_t>(s)];
+    }
+  }
   return PDSIM_OK;
 }
 

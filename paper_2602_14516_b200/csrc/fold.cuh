@@ -89,4 +89,62 @@ PDG_HD double fold_repeat(double s, double g, uint64_t count) {
   return s;
 }
 
+// Number m >= 0 of consecutive steps after a step ending at e0 whose ends
+// E_1 = e0 + g (given, = fl(e0 + dur)), E_2 = fl(E_1 + dur), ... all add
+// exactly g, stay below t, and number at most max_m. Within one binade of
+// the end time the rounded increment of fl(E + dur) is the same integer
+// number of ulps unless dur/ulp is an exact half (then it is constant once
+// the significand is even) — the same argument as fold_repeat (fold.cuh).
+PDG_HD int64_t stable_run(double e0, double dur, double g, double t, int64_t max_m) {
+  const double e1 = dadd(e0, g);
+  if (!(e1 < t) || max_m <= 0) return 0;
+  const uint64_t eb = dbits(e1), db = dbits(dur);
+  const int es = static_cast<int>((eb >> 52) & 0x7ff);
+  const int ed = static_cast<int>((db >> 52) & 0x7ff);
+  if (es == 0 || ed == 0 || es >= 0x7fe || ed > es || es < 53 + 1) return 1;
+  const uint64_t kMant = (1ull << 52) - 1;
+  const uint64_t kTop = (1ull << 53) - 2;
+  const uint64_t S1 = (eb & kMant) | (1ull << 52);
+  const uint64_t G = (db & kMant) | (1ull << 52);
+  const int sh = es - ed;
+  uint64_t k, rem, half;
+  if (sh == 0) {
+    k = G;
+    rem = 0;
+    half = 1;
+  } else if (sh < 64) {
+    k = G >> sh;
+    rem = G & ((1ull << sh) - 1);
+    half = 1ull << (sh - 1);
+  } else {
+    k = 0;
+    rem = 1;
+    half = 2;
+  }
+  uint64_t dstep;
+  if (rem == 0 || rem < half) {
+    dstep = k;
+  } else if (rem > half) {
+    dstep = k + 1;
+  } else {
+    if (S1 & 1ull) return 1;  // tie with an odd significand: one step at a time
+    dstep = k + (k & 1ull);
+  }
+  if (dstep == 0) return 1;
+  // the stable increment must be the gap we were given
+  const double ulp = bitsd(static_cast<uint64_t>(es - 52) << 52);
+  if (dmul(static_cast<double>(dstep), ulp) != g) return 1;
+  if (S1 > kTop) return 1;
+  int64_t m = 1 + static_cast<int64_t>(udiv53(kTop - S1, dstep));
+  const uint64_t tb = dbits(t);
+  const int et = static_cast<int>((tb >> 52) & 0x7ff);
+  if (et == es) {  // t in the same binade: S1 + (j-1) d < T
+    const uint64_t T = (tb & kMant) | (1ull << 52);
+    const int64_t mt = 1 + static_cast<int64_t>(udiv53(T - S1 - 1, dstep));
+    if (mt < m) m = mt;
+  }
+  if (max_m < m) m = max_m;
+  return m;
+}
+
 }  // namespace pdg

@@ -13,6 +13,7 @@
 #include <numeric>
 #include <string>
 #include <unordered_set>
+#include <thread>
 #include <vector>
 
 #include "engine.cuh"
@@ -380,6 +381,23 @@ inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax
   c.segcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(iw + maxdec + 16, 16)));
   c.maxdec = static_cast<int32_t>(maxdec);
   return c;
+}
+
+// Runs f(0..n-1) on all host threads (static interleave; small n runs inline).
+template <class F>
+inline void parallel_for(size_t n, F&& f) {
+  const size_t nt = std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+  if (nt <= 1 || n < 16) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (size_t t = 0; t < nt; ++t) {
+    pool.emplace_back([&, t] {
+      for (size_t i = t; i < n; i += nt) f(i);
+    });
+  }
+  for (auto& th : pool) th.join();
 }
 
 // Host-side sort of session outcomes by id (sim_engine.cpp:165-168).

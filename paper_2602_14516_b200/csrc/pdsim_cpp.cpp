@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -417,6 +418,157 @@ std::vector<DeploymentPlan> enumerate_plans(const std::vector<int>& degrees, int
     d.feasible = true;
     out.push_back(d);
   }
+  return out;
+}
+
+namespace {
+
+pdsim_trace_stats stats_to_pod(const TraceStats& stats) {
+  pdsim_trace_stats s;
+  std::memset(&s, 0, sizeof(s));
+  s.mean_rounds = stats.mean_rounds;
+  s.fixed_rounds = stats.fixed_rounds ? 1 : 0;
+  s.mean_prefill_len = stats.mean_prefill_len;
+  s.mean_decode_len = stats.mean_decode_len;
+  s.length_cv = stats.length_cv;
+  s.first_round_fraction = stats.first_round_fraction;
+  s.mean_interaction_delay = stats.mean_interaction_delay;
+  s.ttft_thres = stats.slo.ttft_thres;
+  s.itl_thres = stats.slo.itl_thres;
+  return s;
+}
+
+// Only the listed degrees enter the table (the reference's check_coefficients
+// requires each of them to be known).
+pdsim_coefficients coeffs_to_pod(const LatencyCoefficients& c, const std::vector<int>& degrees) {
+  std::vector<int> ts = degrees;
+  std::sort(ts.begin(), ts.end());
+  ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+  if (ts.empty() || ts.front() < 1) throw ConfigError("planner: degrees must be >= 1");
+  if (ts.size() > PDSIM_MAX_DEGREES) throw ConfigError("planner: too many degrees");
+  pdsim_coefficients p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_degrees = static_cast<int32_t>(ts.size());
+  for (size_t k = 0; k < ts.size(); ++k) {
+    const int n = ts[k];
+    p.degrees[k] = n;
+    const bool pre = c.tau_pre.count(n) != 0, dec = c.tau_dec.count(n) != 0;
+    if ((!pre && !c.infeasible_pre.count(n)) || (!dec && !c.infeasible_dec.count(n))) {
+      throw ConfigError("planner: no coefficient for degree " + std::to_string(n));
+    }
+    p.infeasible_pre[k] = pre ? 0 : 1;
+    p.infeasible_dec[k] = dec ? 0 : 1;
+    p.tau_pre[k] = pre ? c.tau_pre.at(n) : 0.0;
+    p.tau_dec[k] = dec ? c.tau_dec.at(n) : 0.0;
+  }
+  return p;
+}
+
+DeploymentPlan plan_from_pod(const pdsim_plan& p, double z, int gpus) {
+  DeploymentPlan d;
+  for (int i = 0; i < p.n_prefill_groups; ++i) d.x[p.prefill_degree[i]] = p.prefill_count[i];
+  for (int i = 0; i < p.n_decode_groups; ++i) d.y[p.decode_degree[i]] = p.decode_count[i];
+  d.objective_z = z;
+  d.gpus_used = gpus;
+  d.feasible = true;
+  return d;
+}
+
+PhaseSimResult phase(const Trace& trace, const PerfProfile& profile, int degree, bool prefill) {
+  profile.validate();
+  TraceArrays ta(trace);
+  pdsim_profile prof;
+  profile_to_pod(profile, &prof);
+  pdsim_gpu_ctx* ctx = context(default_device());
+  const int32_t deg = degree;
+  pdsim_phase_result pre, dec;
+  check_ctx(pdsim_gpu_phase_sims(ctx, 1, &ta.view, &deg, &prof, &pre, &dec), ctx);
+  const pdsim_phase_result& r = prefill ? pre : dec;
+  if (r.status != PDSIM_OK) {
+    raise(r.status, prefill ? "planner: reference trace has no prefill tasks"
+                            : (trace.sessions.empty() ? "planner: reference trace has no sessions"
+                                                      : "planner: reference trace produced no inter-token samples"));
+  }
+  PhaseSimResult out;
+  out.p95 = r.p95;
+  out.infeasible = r.infeasible != 0;
+  out.sample_count = r.sample_count;
+  return out;
+}
+
+}  // namespace
+
+PhaseSimResult simulate_prefill_replica(const Trace& trace, const PerfProfile& profile, int degree) {
+  return phase(trace, profile, degree, true);
+}
+
+PhaseSimResult simulate_decode_replica(const Trace& trace, const PerfProfile& profile, int degree) {
+  return phase(trace, profile, degree, false);
+}
+
+std::vector<LatencyCoefficients> estimate_coefficients_batch(const TraceStats& stats, const std::vector<double>& rates,
+                                                             const std::vector<std::uint64_t>& seeds,
+                                                             const PerfProfile& profile,
+                                                             const std::vector<int>& degrees, int total_gpus) {
+  if (rates.size() != seeds.size()) throw ConfigError("planner: rates and seeds differ in length");
+  pdsim_profile prof;
+  profile_to_pod(profile, &prof);
+  const pdsim_trace_stats st = stats_to_pod(stats);
+  std::vector<int32_t> ds(degrees.begin(), degrees.end());
+  pdsim_gpu_ctx* ctx = context(default_device());
+  std::vector<pdsim_coefficients> pods(rates.size());
+  std::vector<int32_t> status(rates.size(), PDSIM_OK);
+  check_ctx(pdsim_gpu_estimate_coefficients(ctx, &st, static_cast<int32_t>(rates.size()), rates.data(), seeds.data(),
+                                            &prof, ds.data(), static_cast<int32_t>(ds.size()), total_gpus,
+                                            pods.data(), status.data()),
+            ctx);
+  std::vector<LatencyCoefficients> out;
+  for (size_t s = 0; s < rates.size(); ++s) {
+    if (status[s] != PDSIM_OK) raise(status[s], pdsim_gpu_last_error(ctx));
+    LatencyCoefficients c;
+    const pdsim_coefficients& p = pods[s];
+    std::string degs;
+    for (int k = 0; k < p.n_degrees; ++k) {
+      const int n = p.degrees[k];
+      if (p.infeasible_pre[k]) c.infeasible_pre.insert(n); else c.tau_pre[n] = p.tau_pre[k];
+      if (p.infeasible_dec[k]) c.infeasible_dec.insert(n); else c.tau_dec[n] = p.tau_dec[k];
+      degs += (k ? "," : "") + std::to_string(n);
+    }
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%g", rates[s]);
+    c.provenance = std::string("rate=") + buf + " sessions=256 gpus=" + std::to_string(total_gpus) +
+                   " seed=" + std::to_string(seeds[s]) + " degrees=[" + degs + "]";  // planner.cpp:273-281
+    out.push_back(std::move(c));
+  }
+  return out;
+}
+
+LatencyCoefficients estimate_coefficients(const TraceStats& stats, double rate, const PerfProfile& profile,
+                                          const std::vector<int>& degrees, int total_gpus, std::uint64_t seed) {
+  return estimate_coefficients_batch(stats, {rate}, {seed}, profile, degrees, total_gpus).front();
+}
+
+DeploymentPlan solve(const LatencyCoefficients& coeffs, int total_gpus, const std::vector<int>& degrees) {
+  const pdsim_coefficients c = coeffs_to_pod(coeffs, degrees);
+  pdsim_plan p;
+  double z = 0.0;
+  int32_t gpus = 0, feasible = 0;
+  check(pdsim_solve(&c, total_gpus, &p, &z, &gpus, &feasible));
+  if (!feasible) return DeploymentPlan{};
+  return plan_from_pod(p, z, gpus);
+}
+
+std::vector<DeploymentPlan> top_k(const LatencyCoefficients& coeffs, int total_gpus, const std::vector<int>& degrees,
+                                  int k) {
+  const pdsim_coefficients c = coeffs_to_pod(coeffs, degrees);
+  if (k < 1) throw ConfigError("top_k: k must be >= 1");
+  std::vector<pdsim_plan> plans(static_cast<size_t>(k));
+  std::vector<double> z(static_cast<size_t>(k));
+  std::vector<int32_t> g(static_cast<size_t>(k));
+  const int64_t n = pdsim_top_k(&c, total_gpus, k, plans.data(), z.data(), g.data());
+  if (n < 0) raise(PDSIM_ERR_CONFIG, pdsim_last_error());
+  std::vector<DeploymentPlan> out;
+  for (int64_t i = 0; i < n; ++i) out.push_back(plan_from_pod(plans[static_cast<size_t>(i)], z[static_cast<size_t>(i)], g[static_cast<size_t>(i)]));
   return out;
 }
 

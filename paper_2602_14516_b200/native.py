@@ -71,6 +71,16 @@ def lib():
         L.pdsim_enumerate_plans.restype = C.c_int64
         L.pdsim_argmax_candidates.argtypes = [P(C.c_int64), C.c_int32]
         L.pdsim_argmax_candidates.restype = C.c_int32
+        L.pdsim_gpu_phase_sims.argtypes = [C.c_void_p, C.c_int32, P(abi.Trace), P(C.c_int32), P(abi.Profile),
+                                           P(abi.PhaseResult), P(abi.PhaseResult)]
+        L.pdsim_gpu_estimate_coefficients.argtypes = [C.c_void_p, P(abi.TraceStats), C.c_int32, P(C.c_double),
+                                                      P(C.c_uint64), P(abi.Profile), P(C.c_int32), C.c_int32,
+                                                      C.c_int32, P(abi.Coefficients), P(C.c_int32)]
+        L.pdsim_solve.argtypes = [P(abi.Coefficients), C.c_int32, P(abi.Plan), P(C.c_double), P(C.c_int32),
+                                  P(C.c_int32)]
+        L.pdsim_top_k.argtypes = [P(abi.Coefficients), C.c_int32, C.c_int32, P(abi.Plan), P(C.c_double),
+                                  P(C.c_int32)]
+        L.pdsim_top_k.restype = C.c_int64
         if L.pdsim_abi_version() != 1:
             raise PdsimError(abi.ERR_INTERNAL, "ABI version mismatch")
         _lib = L
@@ -184,6 +194,27 @@ def search_input(traces, plans, pair_begin=0, pair_end=-1):
     return inp
 
 
+# ---- surrogate planner: exact assignment over coefficients (host C++) ------
+
+def solve(coeffs, total_gpus):
+    """solve (reference planner.cpp:482-578). Returns (plan, objective_z,
+    gpus_used) or None when infeasible."""
+    plan, z, g, f = abi.Plan(), C.c_double(), C.c_int32(), C.c_int32()
+    _check(lib().pdsim_solve(C.byref(coeffs), total_gpus, C.byref(plan), C.byref(z), C.byref(g), C.byref(f)))
+    return (plan, z.value, g.value) if f.value else None
+
+
+def top_k(coeffs, total_gpus, k):
+    """top_k (reference planner.cpp:605-657): [(plan, objective_z, gpus_used)]."""
+    plans = (abi.Plan * k)()
+    zs = (C.c_double * k)()
+    gs = (C.c_int32 * k)()
+    n = lib().pdsim_top_k(C.byref(coeffs), total_gpus, k, plans, zs, gs)
+    if n < 0:
+        _raise(abi.ERR_CONFIG, lib().pdsim_last_error())
+    return [(plans[i], zs[i], gs[i]) for i in range(n)]
+
+
 class Context:
     """A device context (pdsim_gpu_create). One per GPU / process."""
 
@@ -212,6 +243,32 @@ class Context:
 
     def _check(self, rc):
         _check(rc, self._h)
+
+    def phase_sims(self, traces, degrees, profile):
+        """simulate_prefill_replica / simulate_decode_replica (reference
+        planner.cpp:75-226) for jobs (traces[k], degrees[k]) in one launch.
+        Returns [(prefill PhaseResult, decode PhaseResult)]."""
+        n = len(traces)
+        tv = (abi.Trace * max(n, 1))(*traces)
+        dg = (C.c_int32 * max(n, 1))(*degrees)
+        pre = (abi.PhaseResult * max(n, 1))()
+        dec = (abi.PhaseResult * max(n, 1))()
+        self._check(lib().pdsim_gpu_phase_sims(self._h, n, tv, dg, C.byref(profile), pre, dec))
+        return [(pre[k], dec[k]) for k in range(n)]
+
+    def estimate_coefficients(self, stats, rates, seeds, profile, degrees, total_gpus):
+        """estimate_coefficients (reference planner.cpp:228-283) for every
+        (rates[s], seeds[s]) setting in one device launch. Returns
+        [(Coefficients, status)]."""
+        n = len(rates)
+        rs = (C.c_double * max(n, 1))(*rates)
+        ss = (C.c_uint64 * max(n, 1))(*seeds)
+        dg = (C.c_int32 * len(degrees))(*degrees)
+        out = (abi.Coefficients * max(n, 1))()
+        st = (C.c_int32 * max(n, 1))()
+        self._check(lib().pdsim_gpu_estimate_coefficients(self._h, C.byref(stats), n, rs, ss, C.byref(profile), dg,
+                                                          len(degrees), total_gpus, out, st))
+        return [(out[k], st[k]) for k in range(n)]
 
     def set_stream(self, cuda_stream_ptr):
         self._check(lib().pdsim_gpu_set_stream(self._h, C.c_void_p(cuda_stream_ptr or 0)))

@@ -122,6 +122,38 @@ int main() {
   }
   CHECK(sr.best_slo_ok == best);
 
+  // Surrogate planner (planner.hpp:55-113): the coefficient pipeline and the
+  // solver behave like the reference's planner_test properties.
+  {
+    const std::vector<int> ds = {1, 2, 4, 8};
+    const LatencyCoefficients c1 = estimate_coefficients(preset_stats("toolbench"), 8.0, p, ds, 8, 42);
+    const LatencyCoefficients c2 = estimate_coefficients(preset_stats("toolbench"), 8.0, p, ds, 8, 42);
+    CHECK(c1.tau_pre == c2.tau_pre && c1.tau_dec == c2.tau_dec);  // deterministic per seed
+    CHECK(c1.provenance == "rate=8 sessions=256 gpus=8 seed=42 degrees=[1,2,4,8]");
+    for (const auto& [d, tau] : c1.tau_pre) CHECK(tau > 0.0);
+    const std::vector<LatencyCoefficients> batch =
+        estimate_coefficients_batch(preset_stats("toolbench"), {8.0, 8.0}, {42, 42}, p, ds, 8);
+    CHECK(batch.size() == 2 && batch[1].tau_dec == c1.tau_dec);
+    const DeploymentPlan best = solve(c1, 8, ds);
+    const std::vector<DeploymentPlan> ranked = top_k(c1, 8, ds, 5);
+    CHECK(!ranked.empty() && ranked.front() == best);
+    CHECK(best.gpus() <= 8 && best.prefill_replicas() >= 1 && best.decode_replicas() >= 1);
+    bool bad = false;
+    try {
+      LatencyCoefficients missing;
+      missing.tau_pre[1] = 0.1;
+      solve(missing, 8, {1});  // no decode coefficient for degree 1
+    } catch (const ConfigError&) {
+      bad = true;
+    }
+    CHECK(bad);
+    const PhaseSimResult pr = simulate_prefill_replica(gen, p, 2);
+    const PhaseSimResult dr = simulate_decode_replica(gen, p, 2);
+    std::int64_t rounds = 0;
+    for (const SessionSpec& ss : gen.sessions) rounds += static_cast<std::int64_t>(ss.rounds.size());
+    CHECK(pr.p95 > 0.0 && dr.p95 > 0.0 && pr.sample_count == rounds);
+  }
+
   std::printf("cpp_api_test: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
   return failures ? 1 : 0;
 }
