@@ -112,27 +112,56 @@ def shard(n_pairs, rank, world):
     return b, e
 
 
-def cpu_baseline(wl, seconds):
+def cpu_baseline(wl, seconds, gpu_res=None):
     """The reference's own CPU path (oracle/_ref, unmodified reference sources)
-    on all host threads over a bounded sample of the workload's pairs."""
+    on all host threads over a bounded sample of the workload's pairs. When
+    the GPU result of the same search is given, the sampled pairs double as a
+    parity check of the timed run: per-pair attainment must be identical, and
+    when every pair was sampled, so must the argmax."""
     from oracle import refbind
     if not refbind.available():
-        return None
+        return None, None
     n_threads = os.cpu_count() or 1
     pairs = wl.n_pairs
     t_total, rounds, done = 0.0, 0, 0
     chunk = max(n_threads, 1)
+    mism = 0
+    sums = [0] * len(wl.plans)
+    bad = [False] * len(wl.plans)
     while done < pairs and t_total < seconds:
         e = min(pairs, done + chunk)
-        _, _, wall = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed,
-                                         n_threads=n_threads, pair_begin=done, pair_end=e)
+        att, st, wall = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed,
+                                            n_threads=n_threads, pair_begin=done, pair_end=e)
+        if gpu_res is not None:
+            for k in range(e - done):
+                p = done + k
+                c = p // len(wl.traces)
+                g = gpu_res.pair_attainment[p]
+                same = gpu_res.pair_status[p] == st[k] and all(
+                    getattr(g, f) == getattr(att[k], f) for f in ("sessions_total", "sessions_completed", "slo_ok",
+                                                                  "ttft_ok", "itl_ok"))
+                mism += 0 if same else 1
+                if st[k] != 0:
+                    bad[c] = True
+                else:
+                    sums[c] += att[k].slo_ok
         t_total += wall
         rounds += wl.rounds_in(done, e)
         done = e
-    return {"value": rounds / t_total, "unit": UNIT, "cores": n_threads, "kind": "reference",
+    base = {"value": rounds / t_total, "unit": UNIT, "cores": n_threads, "kind": "reference",
             "sample": f"{done}/{pairs} pairs of {wl.name} (first {done} in enumeration order), "
                       f"{t_total:.1f} s on {n_threads} threads, std::thread pool over pdsim::run",
             "replays_per_s": done / t_total}
+    parity = None
+    if gpu_res is not None:
+        parity = {"pairs_checked": done, "pairs_total": pairs, "attainment_mismatches": mism,
+                  "checker": "oracle/_ref (unmodified reference run())"}
+        if done == pairs:
+            key = [(-1 if bad[c] else sums[c], -c) for c in range(len(wl.plans))]
+            ref_best = max(range(len(wl.plans)), key=lambda c: key[c])
+            parity["reference_best_candidate"] = ref_best
+            parity["argmax_identical"] = ref_best == gpu_res.best_candidate
+    return base, parity
 
 
 def run_reference(args, rank, world):
@@ -272,9 +301,9 @@ def run_ours(args, rank, world, local):
         except Exception:
             traffic = None
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(wl, args.cpu_sample_seconds)
+        cpu, parity = cpu_baseline(wl, args.cpu_sample_seconds, gpu_res=res)
 
     if rank == 0:
         line = {
@@ -304,6 +333,8 @@ def run_ours(args, rank, world, local):
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if parity:
+            line["parity"] = parity
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -100,3 +100,38 @@ def test_plan_search_matches_reference_pool(ctx):
     best = max(range(len(plans)), key=lambda c: (sums[c], -c))
     assert res.best_candidate == best
     assert res.best_slo_ok == sums[best]
+
+
+def test_c2_headline_search_matches_reference(ctx):
+    """The bench headline workload itself (C2: 169 N=8 plans, toolbench 10 000
+    sessions @16/s): per-pair attainment, per-candidate sums and the argmax
+    equal the unmodified reference's."""
+    from oracle import refbind
+    from paper_2602_14516_b200 import workloads
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    wl = workloads.c2()
+    res = ctx.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed)
+    att, st_ref, _ = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed)
+    sums = []
+    for p in range(wl.n_pairs):
+        assert res.pair_status[p] == st_ref[p]
+        for f in parity.ATT_FIELDS:
+            assert getattr(res.pair_attainment[p], f) == getattr(att[p], f), (p, f)
+        sums.append(att[p].slo_ok if st_ref[p] == 0 else -1)
+    assert [res.candidate_slo_ok[c] for c in range(len(wl.plans))] == sums
+    assert res.best_candidate == max(range(len(sums)), key=lambda c: (sums[c], -c))
+
+
+def test_saturated_iterative_rag_pair_matches_reference(ctx):
+    """C3's regime (qwen-32b cost model, hotpotqa 8 fixed rounds, overloaded):
+    every record of a saturated replay is bit-identical, including the
+    per-session mean ITL folds over thousands of concurrent decoders."""
+    from paper_2602_14516_b200 import workloads
+    prof = workloads.model_profile("qwen-32b")
+    tr = native.gen_trace(workloads.trace_stats("hotpotqa-8fixed"), 20.0, 3000, 1)
+    for x, y in (({1: 1}, {1: 1}), ({2: 1}, {1: 2, 2: 1})):
+        plan = abi.make_plan(x, y)
+        prm = abi.default_params()
+        got = ctx.run(tr.view, plan, prof, prm, 1)
+        parity.assert_same_run(got, parity.oracle_run(tr.view, plan, prof, prm, 1))
