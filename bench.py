@@ -169,7 +169,8 @@ def run_reference(args, rank, world):
         return
     from paper_2602_14516_b200 import workloads
     from oracle import refbind
-    wl = workloads.CONFIGS[args.config]()
+    # same workload as our arm: at N > 1 the C2 search grows to N replicas
+    wl = workloads.c2(replicas=world) if (args.config == "C2" and world > 1) else workloads.CONFIGS[args.config]()
     n_threads = os.cpu_count() or 1
     # each step = a bounded sample of the pairs (~10 s of CPU work at most)
     probe_end = min(wl.n_pairs, n_threads)
