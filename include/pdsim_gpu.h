@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PDSIM_ABI_VERSION 1
+#define PDSIM_ABI_VERSION 2
 
 #define PDSIM_MAX_DEGREES 8     /* profile degree set size */
 #define PDSIM_MAX_BREAKPOINTS 7 /* per piecewise curve; segments = bps + 1 */
@@ -202,6 +202,15 @@ typedef struct pdsim_attainment {
  * (NULL to skip); when given they must hold n_rounds decisions / TTFT samples
  * and n_sessions outcomes. Decisions and TTFT samples come in the reference
  * push order; sessions are sorted by session id (sim_engine.cpp:165-168). */
+/* ItlSample (sim_engine.hpp:66-72). */
+typedef struct pdsim_itl_sample {
+  int64_t session_id;
+  int32_t round;        /* 1-based */
+  int32_t token_index;  /* position within the round (>= 2) */
+  double completion_time;
+  double value;
+} pdsim_itl_sample;
+
 typedef struct pdsim_run_output {
   pdsim_decision* decisions;
   pdsim_ttft_sample* ttft_samples;
@@ -211,6 +220,12 @@ typedef struct pdsim_run_output {
   int64_t n_sessions;    /* out: completed sessions */
   pdsim_counters counters;     /* out */
   pdsim_attainment attainment; /* out */
+  /* Optional per-token ITL samples in the reference's push order
+   * (sim_engine.cpp:536-556): NULL skips them. At most itl_capacity are
+   * written; n_itl is the total (sum over rounds of decode_len - 1 bounds it). */
+  pdsim_itl_sample* itl_samples;
+  int64_t itl_capacity;
+  int64_t n_itl;         /* out */
 } pdsim_run_output;
 
 /* Batched search: pairs are (candidate c, trace replica r), pair index

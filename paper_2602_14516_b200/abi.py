@@ -143,6 +143,17 @@ class Attainment(C.Structure):
     ]
 
 
+class ItlSample(C.Structure):
+    """ItlSample (sim_engine.hpp:66-72)."""
+    _fields_ = [
+        ("session_id", C.c_int64),
+        ("round", C.c_int32),
+        ("token_index", C.c_int32),
+        ("completion_time", C.c_double),
+        ("value", C.c_double),
+    ]
+
+
 class RunOutput(C.Structure):
     _fields_ = [
         ("decisions", C.POINTER(Decision)),
@@ -153,6 +164,9 @@ class RunOutput(C.Structure):
         ("n_sessions", C.c_int64),
         ("counters", Counters),
         ("attainment", Attainment),
+        ("itl_samples", C.POINTER(ItlSample)),
+        ("itl_capacity", C.c_int64),
+        ("n_itl", C.c_int64),
     ]
 
 
@@ -287,6 +301,7 @@ STRUCTS = {
     "pdsim_counters": Counters,
     "pdsim_attainment": Attainment,
     "pdsim_run_output": RunOutput,
+    "pdsim_itl_sample": ItlSample,
     "pdsim_search_input": SearchInput,
     "pdsim_search_output": SearchOutput,
     "pdsim_synth_spec": SynthSpec,

@@ -82,7 +82,7 @@ struct pdsim_gpu_ctx {
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
-  DevBuf d_dec, d_ttft, d_sess;
+  DevBuf d_dec, d_ttft, d_sess, d_steps, d_spans;
   // surrogate-planner phase sims
   DevBuf d_ph_data, d_ph_traces, d_ph_jobs, d_ph_out, d_ph_scratch, d_ph_counter, d_ph_profile;
   // diagnostics
@@ -650,7 +650,7 @@ int pdsim_gpu_stage(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsi
 int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin, int64_t pair_end, uint64_t seed,
                             pdsim_search_output* out) {
   if (int rc = check_ctx(ctx)) return rc;
-  pdg::Records rec{nullptr, nullptr, nullptr};
+  pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const int rc = search_impl(ctx, pair_begin, pair_end, seed, out, rec, nullptr);
   if (out && rc == PDSIM_OK) out->h2d_bytes = 0;
   return rc;
@@ -661,7 +661,7 @@ int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, cons
   if (int rc = check_ctx(ctx)) return rc;
   int64_t h2d = 0;
   if (int rc = stage_impl(ctx, in, profile, params, &h2d)) return rc;
-  pdg::Records rec{nullptr, nullptr, nullptr};
+  pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const int rc = search_impl(ctx, in->pair_begin, in->pair_end, seed, out, rec, nullptr);
   if (out) out->h2d_bytes = h2d;
   return rc;
@@ -685,7 +685,7 @@ int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan
     return set_err(ctx, PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
   }
   const pdg::PackedTrace& t = ctx->packed[0];
-  pdg::Records rec{nullptr, nullptr, nullptr};
+  pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const size_t R = static_cast<size_t>(std::max(t.R, 1)), S = static_cast<size_t>(std::max(t.S, 1));
   if (out->decisions) {
     CU(ctx, ctx->d_dec.reserve(sizeof(pdsim_decision) * R));
@@ -698,6 +698,14 @@ int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan
   if (out->sessions) {
     CU(ctx, ctx->d_sess.reserve(sizeof(pdsim_session_outcome) * S));
     rec.sessions = ctx->d_sess.as<pdsim_session_outcome>();
+  }
+  if (out->itl_samples) {  // materialised ITL samples: step log + round spans
+    const size_t cap = static_cast<size_t>(std::max<int64_t>(t.total_decode, 1));
+    CU(ctx, ctx->d_steps.reserve(sizeof(pdg::StepRec) * cap));
+    CU(ctx, ctx->d_spans.reserve(sizeof(pdg::SpanRec) * R));
+    rec.steps = ctx->d_steps.as<pdg::StepRec>();
+    rec.spans = ctx->d_spans.as<pdg::SpanRec>();
+    rec.steps_cap = static_cast<int64_t>(cap);
   }
   pdg::PairResult res;
   memset(&res, 0, sizeof(res));
@@ -719,8 +727,28 @@ int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan
     CU(ctx, cudaMemcpyAsync(out->sessions, rec.sessions, sizeof(pdsim_session_outcome) * out->n_sessions,
                             cudaMemcpyDeviceToHost, ctx->stream));
   }
+  out->n_itl = 0;
+  std::vector<pdg::StepRec> steps;
+  std::vector<pdg::SpanRec> spans;
+  if (out->itl_samples) {
+    if (res.n_steps > rec.steps_cap) return set_err(ctx, PDSIM_ERR_INTERNAL, "run: step log capacity exceeded");
+    steps.resize(static_cast<size_t>(res.n_steps));
+    spans.resize(static_cast<size_t>(res.n_spans));
+    if (res.n_steps > 0) {
+      CU(ctx, cudaMemcpyAsync(steps.data(), rec.steps, sizeof(pdg::StepRec) * steps.size(), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    }
+    if (res.n_spans > 0) {
+      CU(ctx, cudaMemcpyAsync(spans.data(), rec.spans, sizeof(pdg::SpanRec) * spans.size(), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    }
+  }
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (out->sessions) pdg::sort_outcomes(out->sessions, out->n_sessions);
+  if (out->itl_samples) {
+    out->n_itl = pdg::expand_itl(steps.data(), res.n_steps, spans.data(), res.n_spans, t,
+                                 ctx->plans[0].D, out->itl_samples, out->itl_capacity);
+  }
   return PDSIM_OK;
 }
 

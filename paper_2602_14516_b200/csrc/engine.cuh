@@ -415,10 +415,31 @@ PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
 }
 
 // Optional per-pair record outputs (drop-in SimResult vectors).
+// ITL materialisation (records mode): decode steps in event order and the
+// step interval of every decoded round; the host expands them into the
+// reference's per-token ItlSample stream (pack.hpp expand_itl).
+struct StepRec {
+  double t;    // step end time
+  double gap;  // the step's ITL value (end - previous step end)
+  int32_t d;   // decode worker
+  int32_t k;   // step index on that worker
+};
+struct SpanRec {
+  int32_t sess;   // session index
+  int32_t round;  // 1-based
+  int32_t d;      // decode worker
+  int32_t join;   // step of the round's first token
+  int32_t end;    // step of its last token
+  int32_t reserved;
+};
+
 struct Records {
   pdsim_decision* decisions;        // [R]
   pdsim_ttft_sample* ttft;          // [R]
   pdsim_session_outcome* sessions;  // [S], termination order
+  StepRec* steps;                   // [steps_cap] (optional: ITL materialisation)
+  SpanRec* spans;                   // [R]
+  int64_t steps_cap;
 };
 
 struct PairResult {
@@ -426,6 +447,8 @@ struct PairResult {
   pdsim_counters ctr;
   int64_t n_decisions;
   int64_t n_ttft;
+  int64_t n_steps;      // ITL materialisation records written
+  int64_t n_spans;
   int64_t events;       // dynamic events processed (diagnostics)
   int64_t cycles;       // device clock64() ticks for this pair (0 on host)
   int64_t exact_folds;  // certified comparisons that fell back to a fold
@@ -512,6 +535,8 @@ struct EngState {
   pdsim_counters ctr_;
   int64_t n_dec_;
   int64_t n_ttft_;
+  int64_t n_steps_;
+  int64_t n_spans_;
   int64_t events_;
   int64_t folds_;
   double st_[kMaxSlots];    // worker-event slot times (+inf when empty)
@@ -575,7 +600,8 @@ class EngineT {
     for (int attempt = 0; attempt < 2; ++attempt) {
       init();
       s_->attempts_ = attempt + 1;
-      s_->lazy_ = attempt == 0 ? 1 : 0;
+      // Materialised ITL samples need every step as an event, in order.
+      s_->lazy_ = (attempt == 0 && !s_->REC.steps) ? 1 : 0;
       s_->exact_itl_ = (attempt > 0 || s_->REC.sessions) ? 1 : 0;
       event_loop();
       if (!s_->abort_) break;
@@ -695,6 +721,8 @@ class EngineT {
     out->ctr = s_->ctr_;
     out->n_decisions = s_->n_dec_;
     out->n_ttft = s_->n_ttft_;
+    out->n_steps = s_->n_steps_;
+    out->n_spans = s_->n_spans_;
     out->events = s_->events_;
     out->exact_folds = s_->folds_;
     out->status = s_->failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
@@ -752,6 +780,8 @@ class EngineT {
     s_->ctr_ = pdsim_counters{};
     s_->n_dec_ = 0;
     s_->n_ttft_ = 0;
+    s_->n_steps_ = 0;
+    s_->n_spans_ = 0;
     s_->events_ = 0;
     s_->folds_ = 0;
     s_->ctr_.events_in_order = 1;
@@ -2247,6 +2277,17 @@ class EngineT {
     const int64_t kv = w.kv_used;
     const int64_t tokens = s_->ctr_.tokens_decoded;
     seg_append(d, k, 1, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
+    if (s_->REC.steps) {
+      const int64_t ns = s_->n_steps_;
+      if (ns < s_->REC.steps_cap && lane_id() == 0) {
+        StepRec& r = s_->REC.steps[ns];
+        r.t = now;
+        r.gap = dsub(now, prev);
+        r.d = d;
+        r.k = k;
+      }
+      s_->n_steps_ = ns + 1;  // warp-uniform store
+    }
     // warp-uniform stores
     w.stepping = 0;
     w.last_step_t = now;
@@ -2276,6 +2317,19 @@ class EngineT {
         seg_span(d, s.join, s.seg_hint, &rlo, &rhi);
         ilo = add_rd(ilo, rlo);
         ihi = add_ru(ihi, rhi);
+      }
+      if (s_->REC.spans) {
+        const int64_t nsp = s_->n_spans_;
+        if (lane_id() == 0) {
+          SpanRec& r = s_->REC.spans[nsp];
+          r.sess = i;
+          r.round = s.round;
+          r.d = d;
+          r.join = s.join;
+          r.end = k;
+          r.reserved = 0;
+        }
+        s_->n_spans_ = nsp + 1;  // warp-uniform store
       }
       const bool last = s.round == GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
       {  // warp-uniform stores (every lane writes the same values)

@@ -11,6 +11,9 @@
 #include <cmath>
 #include <cstdint>
 #include <numeric>
+#include <set>
+#include <queue>
+#include <functional>
 #include <string>
 #include <unordered_set>
 #include <thread>
@@ -381,6 +384,66 @@ inline Caps compute_caps(const std::vector<const PackedTrace*>& traces, int pmax
   c.segcap = static_cast<int32_t>(pow2_at_least(std::max<int64_t>(iw + maxdec + 16, 16)));
   c.maxdec = static_cast<int32_t>(maxdec);
   return c;
+}
+
+// Expands a records-mode replay's step log and round spans into the
+// reference's per-token ItlSample stream (sim_engine.cpp:536-556): for each
+// decode step in event order, every member of that worker's batch that is
+// past its round's first token, in cohort order (ascending session id), with
+// token_index = step - join + 1 and the step's gap. Returns the number of
+// samples (writes at most `cap`).
+inline int64_t expand_itl(const StepRec* steps, int64_t n_steps, const SpanRec* spans, int64_t n_spans,
+                          const PackedTrace& t, int n_workers, pdsim_itl_sample* out, int64_t cap) {
+  struct Lane {
+    std::vector<int32_t> order;  // span indices by (first ITL step, rank)
+    size_t next = 0;
+    std::set<std::pair<int32_t, int32_t>> active;  // (rank, span)
+    std::priority_queue<std::pair<int32_t, int32_t>, std::vector<std::pair<int32_t, int32_t>>,
+                        std::greater<std::pair<int32_t, int32_t>>>
+        ends;  // (end step, span)
+  };
+  std::vector<Lane> w(static_cast<size_t>(std::max(n_workers, 1)));
+  for (int64_t j = 0; j < n_spans; ++j) {
+    const SpanRec& sp = spans[j];
+    if (sp.end < sp.join + 1 || sp.d < 0 || sp.d >= n_workers) continue;  // one-token rounds emit nothing
+    w[static_cast<size_t>(sp.d)].order.push_back(static_cast<int32_t>(j));
+  }
+  for (Lane& l : w) {
+    std::sort(l.order.begin(), l.order.end(), [&](int32_t a, int32_t b) {
+      const int32_t sa = spans[a].join + 1, sb = spans[b].join + 1;
+      if (sa != sb) return sa < sb;
+      return t.rank[static_cast<size_t>(spans[a].sess)] < t.rank[static_cast<size_t>(spans[b].sess)];
+    });
+  }
+  int64_t n = 0;
+  for (int64_t q = 0; q < n_steps; ++q) {
+    const StepRec& st = steps[q];
+    if (st.d < 0 || st.d >= n_workers) continue;
+    Lane& l = w[static_cast<size_t>(st.d)];
+    while (l.next < l.order.size() && spans[l.order[l.next]].join + 1 <= st.k) {
+      const int32_t j = l.order[l.next++];
+      l.active.insert({t.rank[static_cast<size_t>(spans[j].sess)], j});
+      l.ends.push({spans[j].end, j});
+    }
+    while (!l.ends.empty() && l.ends.top().first < st.k) {
+      const int32_t j = l.ends.top().second;
+      l.ends.pop();
+      l.active.erase({t.rank[static_cast<size_t>(spans[j].sess)], j});
+    }
+    for (const auto& a : l.active) {
+      const SpanRec& sp = spans[a.second];
+      if (n < cap && out) {
+        pdsim_itl_sample& o = out[n];
+        o.session_id = t.sid[static_cast<size_t>(sp.sess)];
+        o.round = sp.round;
+        o.token_index = st.k - sp.join + 1;
+        o.completion_time = st.t;
+        o.value = st.gap;
+      }
+      ++n;
+    }
+  }
+  return n;
 }
 
 // Runs f(0..n-1) on all host threads (static interleave; small n runs inline).

@@ -648,8 +648,20 @@ SimResult run(const Trace& trace, const DeploymentPlan& plan, const PerfProfile&
   out.decisions = dec.data();
   out.ttft_samples = ttft.data();
   out.sessions = sess.data();
+  // SimResult::itl_samples, as the reference produces them (one per token
+  // after a round's first; PDSIM_RUN_ITL=0 skips the materialisation).
+  std::vector<pdsim_itl_sample> itl;
+  const char* itl_env = std::getenv("PDSIM_RUN_ITL");
+  if (!(itl_env && itl_env[0] == '0')) {
+    int64_t cap = 0;
+    for (int64_t k = 0; k < arrays.view.n_rounds; ++k) cap += std::max<int64_t>(arrays.view.decode_len[k] - 1, 0);
+    itl.resize(static_cast<size_t>(std::max<int64_t>(cap, 1)));
+    out.itl_samples = itl.data();
+    out.itl_capacity = cap;
+  }
   pdsim_gpu_ctx* ctx = context(default_device());
   check_ctx(pdsim_gpu_run(ctx, &arrays.view, &pplan, &prof, &pparams, seed, &out), ctx);
+  if (out.itl_samples && out.n_itl > out.itl_capacity) throw DeviceError("run: ITL sample capacity exceeded");
 
   SimResult r;
   r.trace_name = trace.name;
@@ -666,6 +678,13 @@ SimResult run(const Trace& trace, const DeploymentPlan& plan, const PerfProfile&
     x.rationale = static_cast<RouteRationale>(d.rationale);
     if (d.has_estimate) x.estimated_cost = d.estimated_cost;
     r.decisions.push_back(x);
+  }
+  if (out.itl_samples) {
+    r.itl_samples.reserve(static_cast<size_t>(out.n_itl));
+    for (int64_t k = 0; k < out.n_itl; ++k) {
+      const pdsim_itl_sample& x = itl[static_cast<size_t>(k)];
+      r.itl_samples.push_back({x.session_id, x.round, x.token_index, x.completion_time, x.value});
+    }
   }
   for (int64_t k = 0; k < out.n_ttft; ++k) {
     const pdsim_ttft_sample& t = ttft[static_cast<size_t>(k)];

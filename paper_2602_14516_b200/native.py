@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpdsim_gpu.so")
 
 _lib = None
+ABI_VERSION = 2  # include/pdsim_gpu.h PDSIM_ABI_VERSION
 
 
 class PdsimError(RuntimeError):
@@ -81,7 +82,7 @@ def lib():
         L.pdsim_top_k.argtypes = [P(abi.Coefficients), C.c_int32, C.c_int32, P(abi.Plan), P(C.c_double),
                                   P(C.c_int32)]
         L.pdsim_top_k.restype = C.c_int64
-        if L.pdsim_abi_version() != 1:
+        if L.pdsim_abi_version() != ABI_VERSION:
             raise PdsimError(abi.ERR_INTERNAL, "ABI version mismatch")
         _lib = L
     return _lib
@@ -156,7 +157,8 @@ def enumerate_plans(degrees, total_gpus):
 # ---- device context -----------------------------------------------------------
 
 class RunResult:
-    """Mirror of SimResult (sim_engine.hpp:105-114) minus raw ITL samples."""
+    """Mirror of SimResult (sim_engine.hpp:105-114); itl_samples is filled
+    when run(..., itl=True)."""
 
     def __init__(self, out, dec, ttft, sess):
         self.counters = out.counters
@@ -167,6 +169,8 @@ class RunResult:
         self.n_decisions = out.n_decisions
         self.n_ttft = out.n_ttft
         self.n_sessions = out.n_sessions
+        self.n_itl = out.n_itl
+        self.itl_samples = []
 
 
 class SearchResult:
@@ -273,11 +277,12 @@ class Context:
     def set_stream(self, cuda_stream_ptr):
         self._check(lib().pdsim_gpu_set_stream(self._h, C.c_void_p(cuda_stream_ptr or 0)))
 
-    def run(self, trace, plan, profile, params, seed, records=True):
-        """Drop-in for pdsim::run: one replay on the GPU."""
+    def run(self, trace, plan, profile, params, seed, records=True, itl=False):
+        """Drop-in for pdsim::run: one replay on the GPU. With itl=True the
+        per-token ITL samples are materialised too (SimResult::itl_samples)."""
         S, R = trace.n_sessions, trace.n_rounds
         out = abi.RunOutput()
-        dec = ttft = sess = None
+        dec = ttft = sess = itls = None
         if records:
             dec = (abi.Decision * max(R, 1))()
             ttft = (abi.TtftSample * max(R, 1))()
@@ -285,9 +290,16 @@ class Context:
             out.decisions = C.cast(dec, C.POINTER(abi.Decision))
             out.ttft_samples = C.cast(ttft, C.POINTER(abi.TtftSample))
             out.sessions = C.cast(sess, C.POINTER(abi.SessionOutcome))
+        if itl:
+            cap = sum(max(trace.decode_len[k] - 1, 0) for k in range(R))  # one sample per token after the first
+            itls = (abi.ItlSample * max(cap, 1))()
+            out.itl_samples = C.cast(itls, C.POINTER(abi.ItlSample))
+            out.itl_capacity = cap
         self._check(lib().pdsim_gpu_run(self._h, C.byref(trace), C.byref(plan), C.byref(profile),
                                         C.byref(params), seed, C.byref(out)))
-        return RunResult(out, dec, ttft, sess)
+        r = RunResult(out, dec, ttft, sess)
+        r.itl_samples = [itls[k] for k in range(min(out.n_itl, out.itl_capacity))] if itl else []
+        return r
 
     def _outputs(self, n_pairs, n_cand):
         att = (abi.Attainment * max(n_pairs, 1))()

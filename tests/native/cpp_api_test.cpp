@@ -4,6 +4,7 @@
 // determinism, config errors, and a small batched search. Needs a B200.
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <string>
 
@@ -121,6 +122,30 @@ int main() {
     if (ok > best) best = ok;
   }
   CHECK(sr.best_slo_ok == best);
+
+  // SimResult::itl_samples: one per token after each round's first, and every
+  // session's mean_itl is the sequential mean of its samples in push order
+  // (sim_engine.cpp:544-556, 602).
+  {
+    const SimResult r = run(gen, simple_plan(2, 2), p, SchedulerParams{}, 5);
+    std::map<std::int64_t, std::pair<double, std::int64_t>> acc;
+    for (const ItlSample& x : r.itl_samples) {
+      auto& a = acc[x.session_id];
+      a.first += x.value;
+      a.second += 1;
+      CHECK(x.token_index >= 2 && x.value > 0.0);
+    }
+    std::int64_t expect = 0;
+    for (const SessionOutcome& o : r.sessions) {
+      const auto it = acc.find(o.session_id);
+      const double mean = it == acc.end() ? 0.0 : it->second.first / static_cast<double>(it->second.second);
+      CHECK(mean == o.mean_itl);
+      for (const SessionSpec& ss : gen.sessions)
+        if (ss.session_id == o.session_id)
+          for (const Round& rd : ss.rounds) expect += rd.decode_len - 1;
+    }
+    CHECK(static_cast<std::int64_t>(r.itl_samples.size()) == expect);
+  }
 
   // Surrogate planner (planner.hpp:55-113): the coefficient pipeline and the
   // solver behave like the reference's planner_test properties.

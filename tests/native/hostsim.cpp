@@ -70,7 +70,16 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   dt.rank = t.rank.data();
   dt.by_rank = t.by_rank.data();
   const pdg::DevParams dprm = pdg::to_dev_params(*params);
-  pdg::Records rec{out->decisions, out->ttft_samples, out->sessions};
+  pdg::Records rec{out->decisions, out->ttft_samples, out->sessions, nullptr, nullptr, 0};
+  std::vector<pdg::StepRec> steps;
+  std::vector<pdg::SpanRec> spans;
+  if (out->itl_samples) {
+    steps.resize(static_cast<size_t>(std::max<int64_t>(t.total_decode, 1)));
+    spans.resize(static_cast<size_t>(std::max<int32_t>(t.R, 1)));
+    rec.steps = steps.data();
+    rec.spans = spans.data();
+    rec.steps_cap = static_cast<int64_t>(steps.size());
+  }
   pdg::host_profile() = prof;
   pdg::Engine eng(sslot.es, dt, dp, dprm, caps, sslot, gslot, rec, seed);
   pdg::PairResult res;
@@ -86,6 +95,11 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   out->counters = res.ctr;
   out->attainment = res.att;
   if (out->sessions) pdg::sort_outcomes(out->sessions, out->n_sessions);
+  out->n_itl = 0;
+  if (out->itl_samples) {
+    out->n_itl = pdg::expand_itl(steps.data(), res.n_steps, spans.data(), res.n_spans, t, dp.D, out->itl_samples,
+                                 out->itl_capacity);
+  }
   return PDSIM_OK;
 }
 
@@ -105,6 +119,7 @@ extern "C" int hostsim_run_counts(const pdsim_trace* trace, const pdsim_plan* pl
   o.decisions = nullptr;
   o.ttft_samples = nullptr;
   o.sessions = nullptr;
+  o.itl_samples = nullptr;
   const int rc = hostsim_run(trace, plan, prof, params, seed, &o);
   out->n_decisions = o.n_decisions;
   out->n_ttft = o.n_ttft;

@@ -68,6 +68,91 @@ def host_run(trace, plan, profile, params, seed):
     return Run(out, dec, ttft, sess)
 
 
+def itl_capacity(trace):
+    return max(sum(max(trace.decode_len[k] - 1, 0) for k in range(trace.n_rounds)), 1)
+
+
+def host_run_itl(trace, plan, profile, params, seed):
+    """Host engine build with materialised ITL samples."""
+    out, dec, ttft, sess = _alloc(trace)
+    cap = itl_capacity(trace)
+    itls = (abi.ItlSample * cap)()
+    out.itl_samples = C.cast(itls, C.POINTER(abi.ItlSample))
+    out.itl_capacity = cap
+    rc = hostsim().hostsim_run(C.byref(trace), C.byref(plan), C.byref(profile), C.byref(params), seed,
+                               C.byref(out))
+    if rc:
+        raise EngineError(rc, hostsim().hostsim_last_error().decode())
+    r = Run(out, dec, ttft, sess)
+    r.itl_samples = [itl_tuple(itls[k]) for k in range(min(out.n_itl, cap))]
+    r.n_itl = out.n_itl
+    return r
+
+
+def itl_tuple(x):
+    return (x.session_id, x.round, x.token_index, x.completion_time, x.value)
+
+
+def reference_itl(trace, plan, profile, params, seed):
+    """The reference's SimResult::itl_samples as tuples (push order)."""
+    from oracle import refbind
+    _, _, arrays, n = refbind.run(trace, plan, profile, params, seed, records=True, itl=True)
+    ids, tm, vs = arrays
+    out = []
+    for k in range(n):
+        out.append((ids[3 * k], ids[3 * k + 1], ids[3 * k + 2], tm[k], vs[k]))
+    return out
+
+
+def to_chars(x):
+    """std::to_chars(double) shortest round-trip form (metrics.cpp:32-36):
+    the shorter of fixed and scientific notation, fixed on ties."""
+    from decimal import Decimal
+    x = float(x)
+    if x == 0.0:
+        return "-0" if str(x).startswith("-") else "0"
+    sign, digits, exp = Decimal(repr(abs(x))).as_tuple()
+    digits = list(digits)
+    while len(digits) > 1 and digits[-1] == 0:
+        digits.pop()
+        exp += 1
+    n = len(digits)
+    ds = "".join(str(d) for d in digits)
+    e10 = exp + n - 1
+    sci = ds[0] + ("." + ds[1:] if n > 1 else "") + "e" + ("-" if e10 < 0 else "+") + f"{abs(e10):02d}"
+    if exp >= 0:
+        fixed = ds + "0" * exp
+    elif -exp < n:
+        fixed = ds[: n + exp] + "." + ds[n + exp:]
+    else:
+        fixed = "0." + "0" * (-exp - n) + ds
+    out = fixed if len(fixed) <= len(sci) else sci
+    return ("-" if x < 0 else "") + out
+
+
+def itl_csv_fnv(samples):
+    """FNV-1a of the reference's itl_samples.csv text (metrics.cpp:402-410)."""
+    h = 1469598103934665603
+    def feed(text):
+        nonlocal h
+        for c in text.encode():
+            h ^= c
+            h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    feed("session_id,round,token_index,completion_time,value\n")
+    for sid, rnd, tok, t, v in samples:
+        feed(f"{sid},{rnd},{tok},{to_chars(t)},{to_chars(v)}\n")
+    return f"{h:016x}"
+
+
+def diff_itl(got, want):
+    if len(got) != len(want):
+        return [f"itl_samples: {len(got)} != {len(want)}"]
+    for k, (a, b) in enumerate(zip(got, want)):
+        if a != b:
+            return [f"itl_samples[{k}]: {a} != {b}"]
+    return []
+
+
 def host_run_counts(trace, plan, profile, params, seed):
     """Counts-only host replay (search mode: no records)."""
     out = abi.RunOutput()

@@ -146,3 +146,36 @@ def test_engine_search_mode_counts_match_golden(entry):
     got = parity.host_run_counts(trace.view, plan, prof, params, c["engine_seed"])
     assert parity.digest(got)["counters"] == entry["expect"]["counters"]
     assert parity.digest(got)["attainment"] == entry["expect"]["attainment"]
+
+
+@pytest.mark.parametrize("preset,rate,plan", [("toolbench", 6.0, ({1: 2}, {1: 2})), ("hotpotqa", 20.0, ({2: 1}, {1: 3})),
+                                              ("dureader", 35.0, ({1: 1}, {1: 1, 2: 1})), ("gaia", 3.0, ({}, {1: 2}))])
+def test_engine_itl_samples_match_reference(preset, rate, plan):
+    """SimResult::itl_samples materialised from the step log and round spans
+    (pack.hpp expand_itl) equal the reference's per-token push order."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    tr = native.gen_trace(native.preset_stats(preset), rate, 150, 9)
+    p = abi.make_plan(*plan)
+    for prm in (abi.default_params(), abi.default_params(routing=abi.ROUTING_ALWAYS_LOCAL, window=5)):
+        got = parity.host_run_itl(tr.view, p, prof, prm, 4)
+        want = parity.reference_itl(tr.view, p, prof, prm, 4)
+        assert got.n_itl == len(want)
+        assert not parity.diff_itl(got.itl_samples, want)
+        # the records stay bit-identical with ITL materialisation on (exact stepping)
+        parity.assert_same_run(got, parity.oracle_run(tr.view, p, prof, prm, 4))
+
+
+def test_itl_csv_hash_emulation_matches_reference():
+    """parity.itl_csv_fnv reproduces the reference's itl_samples.csv bytes."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    tr = native.gen_trace(native.preset_stats("gaia"), 5.0, 60, 3)
+    p = abi.make_plan({1: 1}, {1: 2})
+    _, hashes, _, _ = refbind.run(tr.view, p, prof, abi.default_params(), 1, records=True, itl=True)
+    want = parity.reference_itl(tr.view, p, prof, abi.default_params(), 1)
+    assert parity.itl_csv_fnv(want) == f"{hashes[3]:016x}"

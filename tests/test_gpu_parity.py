@@ -135,3 +135,22 @@ def test_saturated_iterative_rag_pair_matches_reference(ctx):
         prm = abi.default_params()
         got = ctx.run(tr.view, plan, prof, prm, 1)
         parity.assert_same_run(got, parity.oracle_run(tr.view, plan, prof, prm, 1))
+
+
+def test_run_itl_samples_match_reference(ctx):
+    """Drop-in run() with materialised ITL samples: the survey fingerprint
+    scenario's itl_samples.csv hash (1.79 M samples) and a mixed-plan run
+    sample by sample."""
+    from tests import golden_cases
+    entry = [e for e in golden_cases.load() if e["case"]["name"] == "survey_fingerprint"][0]
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    tr = native.gen_trace(native.preset_stats("dureader"), 16.0, 4000, 101)
+    plan = abi.make_plan({1: 2}, {1: 2})
+    got = ctx.run(tr.view, plan, prof, abi.default_params(), 2, itl=True)
+    assert got.n_itl == entry["itl_samples"]
+    assert parity.itl_csv_fnv([parity.itl_tuple(x) for x in got.itl_samples]) == entry["reference_csv_fnv"]["itl"]
+    tr2 = native.gen_trace(native.preset_stats("hotpotqa"), 12.0, 300, 5)
+    plan2 = abi.make_plan({2: 1, 4: 1}, {1: 1, 2: 1})
+    got2 = ctx.run(tr2.view, plan2, prof, abi.default_params(), 3, itl=True)
+    want2 = parity.reference_itl(tr2.view, plan2, prof, abi.default_params(), 3)
+    assert not parity.diff_itl([parity.itl_tuple(x) for x in got2.itl_samples], want2)
