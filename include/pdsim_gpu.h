@@ -366,6 +366,13 @@ int pdsim_profile_validate(const pdsim_profile* profile);
 int pdsim_preset_stats(const char* name, pdsim_trace_stats* out);
 int pdsim_gen_trace(const pdsim_trace_stats* stats, double arrival_rate,
                     int32_t num_sessions, uint64_t seed, pdsim_trace_buf** out);
+/* Batched gen_trace on all host threads: trace k is
+ * gen_trace(stats, rates[k], num_sessions, seeds[k]), bit-identical to n
+ * separate calls. out[k] receives an owned buffer (free each with
+ * pdsim_trace_buf_free); on error every out[k] is NULL and the first failing
+ * k's status is returned. */
+int pdsim_gen_trace_batch(const pdsim_trace_stats* stats, int32_t n, const double* rates, int32_t num_sessions,
+                          const uint64_t* seeds, pdsim_trace_buf** out);
 /* Fills a view whose arrays stay owned by `buf`. */
 int pdsim_trace_buf_view(const pdsim_trace_buf* buf, pdsim_trace* view);
 void pdsim_trace_buf_free(pdsim_trace_buf* buf);

@@ -302,6 +302,28 @@ int pdsim_gen_trace(const pdsim_trace_stats* st, double rate, int32_t num_sessio
   return PDSIM_OK;
 }
 
+int pdsim_gen_trace_batch(const pdsim_trace_stats* st, int32_t n, const double* rates, int32_t num_sessions,
+                          const uint64_t* seeds, pdsim_trace_buf** out) {
+  if (!st || !out || n < 0 || (n > 0 && (!rates || !seeds))) return host_fail(PDSIM_ERR_CONFIG, "null argument");
+  std::vector<int> rc(static_cast<size_t>(n), PDSIM_OK);
+  std::vector<std::string> msg(static_cast<size_t>(n));
+  pdg::parallel_for(static_cast<size_t>(n), [&](size_t k) {
+    out[k] = nullptr;
+    rc[k] = pdsim_gen_trace(st, rates[k], num_sessions, seeds[k], &out[k]);
+    if (rc[k] != PDSIM_OK) msg[k] = pdsim_last_error();
+  });
+  for (int32_t k = 0; k < n; ++k) {
+    if (rc[static_cast<size_t>(k)] != PDSIM_OK) {
+      for (int32_t j = 0; j < n; ++j) {
+        pdsim_trace_buf_free(out[j]);
+        out[j] = nullptr;
+      }
+      return host_fail(rc[static_cast<size_t>(k)], msg[static_cast<size_t>(k)].c_str());
+    }
+  }
+  return PDSIM_OK;
+}
+
 int pdsim_trace_buf_view(const pdsim_trace_buf* b, pdsim_trace* v) {
   if (!b || !v) return host_fail(PDSIM_ERR_CONFIG, "null argument");
   v->n_sessions = static_cast<int64_t>(b->sid.size());

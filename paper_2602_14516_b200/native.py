@@ -66,6 +66,8 @@ def lib():
         L.pdsim_preset_stats.argtypes = [C.c_char_p, P(abi.TraceStats)]
         L.pdsim_gen_trace.argtypes = [P(abi.TraceStats), C.c_double, C.c_int32, C.c_uint64, P(C.c_void_p)]
         L.pdsim_trace_buf_view.argtypes = [C.c_void_p, P(abi.Trace)]
+        L.pdsim_gen_trace_batch.argtypes = [P(abi.TraceStats), C.c_int32, P(C.c_double), C.c_int32,
+                                            P(C.c_uint64), P(C.c_void_p)]
         L.pdsim_trace_buf_free.argtypes = [C.c_void_p]
         L.pdsim_trace_validate.argtypes = [P(abi.Trace)]
         L.pdsim_enumerate_plans.argtypes = [P(C.c_int32), C.c_int32, C.c_int32, P(abi.Plan), C.c_int64]
@@ -142,6 +144,15 @@ def gen_trace(stats, arrival_rate, num_sessions, seed):
     h = C.c_void_p()
     _check(lib().pdsim_gen_trace(C.byref(stats), arrival_rate, num_sessions, seed, C.byref(h)))
     return TraceBuf(h)
+
+
+def gen_traces(stats, rates, num_sessions, seeds):
+    """Batched gen_trace on all host threads (bit-identical to gen_trace)."""
+    n = len(rates)
+    hs = (C.c_void_p * max(n, 1))()
+    _check(lib().pdsim_gen_trace_batch(C.byref(stats), n, (C.c_double * max(n, 1))(*rates), num_sessions,
+                                       (C.c_uint64 * max(n, 1))(*seeds), hs))
+    return [TraceBuf(C.c_void_p(hs[k])) for k in range(n)]
 
 
 def enumerate_plans(degrees, total_gpus):

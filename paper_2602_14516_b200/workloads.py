@@ -116,7 +116,7 @@ def c2(sessions=10000, rate=16.0, seed=5, total_gpus=8, replicas=1):
 
 def c3(sessions=50000, rate=20.0, replicas=16, total_gpus=8):
     st = trace_stats("hotpotqa-8fixed")
-    trs = [native.gen_trace(st, rate, sessions, s) for s in range(1, replicas + 1)]
+    trs = native.gen_traces(st, [rate] * replicas, sessions, list(range(1, replicas + 1)))
     plans = native.enumerate_plans(DEGREES, total_gpus)
     return Workload("C3", "qwen-32b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
                     f"qwen-32b, {len(plans)} plans x {replicas} hotpotqa-8-round replicas of {sessions} sessions")
@@ -126,7 +126,8 @@ def c5(model="llama3-8b", rates=None, seeds=4, sessions=1000, total_gpus=8):
     """One model slice of C5: toolbench 1k-session traces over rates x seeds."""
     rates = rates or [1.0 + 0.5 * k for k in range(32)]
     st = trace_stats("toolbench")
-    trs = [native.gen_trace(st, r, sessions, 1000 + s) for r in rates for s in range(seeds)]
+    rs = [r for r in rates for _ in range(seeds)]
+    trs = native.gen_traces(st, rs, sessions, [1000 + s for _ in rates for s in range(seeds)])
     plans = native.enumerate_plans(DEGREES, total_gpus)
     return Workload("C5", model, trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
                     f"{model}, {len(plans)} plans x {len(trs)} toolbench traces ({len(rates)} rates x {seeds} seeds)")

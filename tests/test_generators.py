@@ -145,3 +145,24 @@ def test_profile_validation_rejects_malformed_curves():
     bad.decode[0].alpha[1] = 0.0
     bad.decode[0].beta[1] = 1e-9  # right segment far below the left limit
     assert native.lib().pdsim_profile_validate(C.byref(bad)) == abi.ERR_CONFIG
+
+
+def test_batched_generation_is_bit_identical():
+    """pdsim_gen_trace_batch (all host threads) equals
+    separate gen_trace calls byte for byte."""
+    st = native.preset_stats("toolbench")
+    rates = [0.5 + 0.75 * k for k in range(24)]
+    seeds = [7 * k + 1 for k in range(24)]
+    batch = native.gen_traces(st, rates, 300, seeds)
+    for tb, r, s in zip(batch, rates, seeds):
+        one = native.gen_trace(st, r, 300, s)
+        a, b = tb.view, one.view
+        assert a.n_sessions == b.n_sessions and a.n_rounds == b.n_rounds
+        for k in range(a.n_sessions):
+            assert a.arrival_time[k] == b.arrival_time[k] and a.session_id[k] == b.session_id[k]
+            assert a.round_offset[k + 1] == b.round_offset[k + 1]
+        for k in range(a.n_rounds):
+            assert (a.incr_input_len[k], a.decode_len[k], a.interaction_delay[k]) == \
+                (b.incr_input_len[k], b.decode_len[k], b.interaction_delay[k])
+    with pytest.raises(native.PdsimError):
+        native.gen_traces(st, [1.0, -1.0], 10, [1, 2])
