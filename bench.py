@@ -236,6 +236,8 @@ def run_ours(args, rank, world, local):
     def step(staged=True):
         res = ctx.search_staged(wl.seed, b, e) if staged else ctx.plan_search(
             my_traces, wl.plans, wl.profile, wl.params, wl.seed, b, e)
+        if world == 1:  # the library's own device argmax (argmax_kernel)
+            return res, res.best_candidate, res.best_slo_ok
         cand = torch.tensor([res.candidate_slo_ok[c] for c in range(C)], dtype=torch.int64, device="cuda")
         bad = (cand < 0).to(torch.int64)
         cnt = torch.clamp(cand, min=0)

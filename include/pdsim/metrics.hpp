@@ -1,0 +1,46 @@
+// pdsim/metrics.hpp — drop-in Report types and build_report (reference
+// proj/include/pdsim/metrics.hpp:32-60, proj/src/metrics.cpp:108-190).
+// The CSV codecs and text/JSON formatting of the reference stay out of scope
+// (document I/O); the aggregation itself is here, and the batched search can
+// compute it per pair on the device (SearchOptions::report).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "pdsim/sim_engine.hpp"
+
+namespace pdsim {
+
+struct MetricStat {
+  double mean = 0.0;
+  double p95 = 0.0;
+  std::int64_t count = 0;
+};
+
+struct Report {
+  std::string trace_name;
+  bool empty = false;  // no sessions and no samples
+  std::int64_t sessions_total = 0;
+  std::int64_t sessions_completed = 0;
+  double slo_attainment = 0.0;
+  double ttft_attainment = 0.0;
+  double itl_attainment = 0.0;
+  MetricStat ttft_initial;
+  MetricStat ttft_incremental;
+  MetricStat itl;
+  double e2e_mean = 0.0;
+  double local_fraction = 0.0;
+};
+
+// Nearest-rank percentile: index ceil(q*n) on the 1-based sorted list; empty
+// input yields 0 (metrics.cpp:125-136). Throws DomainError for q outside (0, 1].
+double percentile_nearest_rank(std::vector<double> values, double q);
+
+Report build_report(const SimResult& result);
+Report build_report_from_samples(const std::string& trace_name, std::int64_t sessions_total,
+                                 const std::vector<TtftSample>& ttft, const std::vector<ItlSample>& itl,
+                                 const std::vector<SessionOutcome>& sessions);
+
+}  // namespace pdsim

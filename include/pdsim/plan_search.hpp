@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "pdsim/metrics.hpp"
 #include "pdsim/perf_model.hpp"
 #include "pdsim/planner.hpp"
 #include "pdsim/sim_engine.hpp"
@@ -27,6 +28,7 @@ struct SearchOptions {
   int device = -1;             // -1: $PDSIM_DEVICE or 0
   std::int64_t pair_begin = 0;  // shard [pair_begin, pair_end) of c * replicas + r
   std::int64_t pair_end = -1;
+  bool report = false;  // per-pair build_report on the device (SearchResult::reports)
 };
 
 struct SearchResult {
@@ -36,6 +38,7 @@ struct SearchResult {
   std::vector<PairAttainment> pairs;
   double kernel_ms = 0.0;
   double device_ms = 0.0;
+  std::vector<Report> reports;  // per pair, when SearchOptions::report
 };
 
 SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<DeploymentPlan>& candidates,

@@ -246,6 +246,29 @@ typedef struct pdsim_search_input {
  *    -1 for a candidate with any invalid pair in this call.
  * best_candidate = argmax candidate_slo_ok, ties -> smallest index (-1 when no
  * candidate is valid). Timings are device (CUDA event) milliseconds. */
+/* MetricStat / Report (metrics.hpp:32-51): build_report (metrics.cpp:138-190)
+ * of one replay — in-order means, nearest-rank P95s, attainment ratios. */
+typedef struct pdsim_metric_stat {
+  double mean;
+  double p95;
+  int64_t count;
+} pdsim_metric_stat;
+
+typedef struct pdsim_report {
+  int64_t sessions_total;
+  int64_t sessions_completed;
+  double slo_attainment;
+  double ttft_attainment;
+  double itl_attainment;
+  pdsim_metric_stat ttft_initial;
+  pdsim_metric_stat ttft_incremental;
+  pdsim_metric_stat itl;
+  double e2e_mean;
+  double local_fraction;
+  int32_t empty;
+  int32_t reserved;
+} pdsim_report;
+
 typedef struct pdsim_search_output {
   pdsim_attainment* pair_attainment;
   pdsim_counters* pair_counters;
@@ -261,6 +284,11 @@ typedef struct pdsim_search_output {
   int64_t kernel_launches;
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  /* Optional per-pair Report (NULL: attainment only). Requesting it replays
+   * every decode step as an event (in-order ITL folds) and keeps per-pair
+   * TTFT values, e2e latencies and an ITL gap histogram on the device; the
+   * report is reduced on the device right after each replay. */
+  pdsim_report* pair_report;
 } pdsim_search_output;
 
 /* ---- context -------------------------------------------------------------- */

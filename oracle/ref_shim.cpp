@@ -574,4 +574,26 @@ int64_t ref_top_k(const pdsim_coefficients* c, int32_t total_gpus, int32_t k, pd
   return n;
 }
 
+// build_report (metrics.cpp:138-190) of one reference replay.
+int ref_report(const pdsim_trace* tr, const pdsim_plan* plan, const pdsim_profile* prof,
+               const pdsim_sched_params* params, uint64_t seed, pdsim_report* out) {
+  return guarded([&] {
+    const pdsim::SimResult res = pdsim::run(trace_from_pod(*tr), plan_from_pod(*plan), profile_from_pod(*prof),
+                                            params_from_pod(*params), seed);
+    const pdsim::Report r = pdsim::build_report(res);
+    std::memset(out, 0, sizeof(*out));
+    out->sessions_total = r.sessions_total;
+    out->sessions_completed = r.sessions_completed;
+    out->slo_attainment = r.slo_attainment;
+    out->ttft_attainment = r.ttft_attainment;
+    out->itl_attainment = r.itl_attainment;
+    out->ttft_initial = pdsim_metric_stat{r.ttft_initial.mean, r.ttft_initial.p95, r.ttft_initial.count};
+    out->ttft_incremental = pdsim_metric_stat{r.ttft_incremental.mean, r.ttft_incremental.p95, r.ttft_incremental.count};
+    out->itl = pdsim_metric_stat{r.itl.mean, r.itl.p95, r.itl.count};
+    out->e2e_mean = r.e2e_mean;
+    out->local_fraction = r.local_fraction;
+    out->empty = r.empty ? 1 : 0;
+  });
+}
+
 }  // extern "C"

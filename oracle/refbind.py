@@ -57,6 +57,8 @@ def lib():
         L.ref_top_k.argtypes = [P(abi.Coefficients), C.c_int32, C.c_int32, P(abi.Plan), P(C.c_double),
                                 P(C.c_int32)]
         L.ref_top_k.restype = C.c_int64
+        L.ref_report.argtypes = [P(abi.Trace), P(abi.Plan), P(abi.Profile), P(abi.SchedParams), C.c_uint64,
+                                 P(abi.Report)]
         _lib = L
     return _lib
 
@@ -205,3 +207,10 @@ def top_k(coeffs, total_gpus, k):
     if n < 0:
         raise RefError(1, lib().ref_last_error().decode())
     return [(plans[i], zs[i], gs[i]) for i in range(n)]
+
+
+def report(trace, plan, profile, params, seed):
+    """build_report (metrics.cpp:138-190) of one reference replay."""
+    out = abi.Report()
+    _check(lib().ref_report(C.byref(trace), C.byref(plan), C.byref(profile), C.byref(params), seed, C.byref(out)))
+    return out

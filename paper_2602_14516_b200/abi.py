@@ -154,6 +154,34 @@ class ItlSample(C.Structure):
     ]
 
 
+class MetricStat(C.Structure):
+    _fields_ = [("mean", C.c_double), ("p95", C.c_double), ("count", C.c_int64)]
+
+
+class Report(C.Structure):
+    """Report (metrics.hpp:38-51)."""
+    _fields_ = [
+        ("sessions_total", C.c_int64),
+        ("sessions_completed", C.c_int64),
+        ("slo_attainment", C.c_double),
+        ("ttft_attainment", C.c_double),
+        ("itl_attainment", C.c_double),
+        ("ttft_initial", MetricStat),
+        ("ttft_incremental", MetricStat),
+        ("itl", MetricStat),
+        ("e2e_mean", C.c_double),
+        ("local_fraction", C.c_double),
+        ("empty", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+    def as_tuple(self):
+        m = lambda x: (x.mean, x.p95, x.count)  # noqa: E731
+        return (self.sessions_total, self.sessions_completed, self.slo_attainment, self.ttft_attainment,
+                self.itl_attainment, m(self.ttft_initial), m(self.ttft_incremental), m(self.itl), self.e2e_mean,
+                self.local_fraction, self.empty)
+
+
 class RunOutput(C.Structure):
     _fields_ = [
         ("decisions", C.POINTER(Decision)),
@@ -197,6 +225,7 @@ class SearchOutput(C.Structure):
         ("kernel_launches", C.c_int64),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("pair_report", C.POINTER(Report)),
     ]
 
 
@@ -302,6 +331,8 @@ STRUCTS = {
     "pdsim_attainment": Attainment,
     "pdsim_run_output": RunOutput,
     "pdsim_itl_sample": ItlSample,
+    "pdsim_metric_stat": MetricStat,
+    "pdsim_report": Report,
     "pdsim_search_input": SearchInput,
     "pdsim_search_output": SearchOutput,
     "pdsim_synth_spec": SynthSpec,

@@ -82,7 +82,7 @@ struct pdsim_gpu_ctx {
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
-  DevBuf d_dec, d_ttft, d_sess, d_steps, d_spans;
+  DevBuf d_dec, d_ttft, d_sess, d_steps, d_spans, d_reports;
   // surrogate-planner phase sims
   DevBuf d_ph_data, d_ph_traces, d_ph_jobs, d_ph_out, d_ph_scratch, d_ph_counter, d_ph_profile;
   // diagnostics
@@ -132,6 +132,7 @@ struct KernelArgs {
   unsigned long long* cand_sum;        // [n_candidates]
   int* cand_bad;                       // [n_candidates]
   pdg::Records rec;                    // single-run records (one pair only)
+  pdsim_report* reports;               // optional per-pair reports [pair_end - pair_begin]
   uint64_t seed;
   int32_t profile;                     // per-phase clock64 instrumentation
   int32_t reserved2;
@@ -168,6 +169,13 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     if (a.pair_invalid[pair]) {
       res.status = PDSIM_PAIR_INVALID;
       res.att.sessions_total = a.traces[r].S;
+      if (a.reports && lane == 0) {
+        pdsim_report rep;
+        memset(&rep, 0, sizeof(rep));
+        rep.sessions_total = a.traces[r].S;
+        rep.empty = 1;
+        a.reports[pair - a.pair_begin] = rep;
+      }
     } else {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
@@ -175,6 +183,11 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       pdg::EngineT<kProf, kD, kP> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
       eng.run(&res);
       res.cycles = clock64() - t0;
+      if (a.reports) {
+        pdsim_report rep;
+        eng.build_report(&rep);
+        if (lane == 0) a.reports[pair - a.pair_begin] = rep;
+      }
     }
     if (lane == 0) {
       a.results[pair - a.pair_begin] = res;
@@ -347,6 +360,17 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   if (b < 0 || b > e || e > total) return set_err(ctx, PDSIM_ERR_CONFIG, "search: bad pair range");
   const int64_t n = e - b;
   const int C = ctx->n_candidates;
+  // Report mode widens the global workspace layout (the shared-memory layout
+  // is unchanged): TTFT values, e2e latencies and the ITL gap histogram.
+  const bool report = out && out->pair_report;
+  pdg::Caps caps = ctx->caps;
+  if (report) {
+    int32_t max_r = 1;
+    for (const auto& t : ctx->packed) max_r = std::max(max_r, t.R);
+    caps.rep_r = max_r;
+    caps.rep_gapcap = 1 << 16;
+  }
+  const size_t slot_bytes = pdg::global_slot_bytes(caps, nullptr, nullptr);
 
   // Workspace slots: one warp each, at most 32 resident per SM, bounded by a
   // memory budget.
@@ -357,9 +381,10 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
       1, std::min<int64_t>(32, static_cast<int64_t>((size_t(227) << 10) / std::max<size_t>(ctx->smem_bytes, 1))));
   if (const char* v = getenv("PDSIM_SLOTS_PER_SM")) per_sm = std::max<int64_t>(1, std::min<int64_t>(per_sm, atoll(v)));  // tuning only
   int64_t slots = std::min<int64_t>(std::max<int64_t>(n, 1), static_cast<int64_t>(ctx->sm_count) * per_sm);
-  slots = std::min<int64_t>(slots, static_cast<int64_t>(budget / std::max<size_t>(ctx->slot_bytes, 1)));
+  slots = std::min<int64_t>(slots, static_cast<int64_t>(budget / std::max<size_t>(slot_bytes, 1)));
   if (slots < 1) return set_err(ctx, PDSIM_ERR_CUDA, "search: workspace of one slot exceeds device memory");
-  CU(ctx, ctx->d_ws.reserve(ctx->slot_bytes * static_cast<size_t>(slots)));
+  CU(ctx, ctx->d_ws.reserve(slot_bytes * static_cast<size_t>(slots)));
+  if (report) CU(ctx, ctx->d_reports.reserve(sizeof(pdsim_report) * static_cast<size_t>(std::max<int64_t>(n, 1))));
   CU(ctx, ctx->d_results.reserve(sizeof(pdg::PairResult) * static_cast<size_t>(std::max<int64_t>(n, 1))));
   CU(ctx, ctx->d_cand_sum.reserve(8 * static_cast<size_t>(C)));
   CU(ctx, ctx->d_cand_bad.reserve(4 * static_cast<size_t>(C)));
@@ -380,9 +405,10 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.pair_begin = b;
   a.pair_end = e;
   a.params = pdg::to_dev_params(ctx->params);
-  a.caps = ctx->caps;
+  a.caps = caps;
   a.ws = ctx->d_ws.as<char>();
-  a.slot_bytes = ctx->slot_bytes;
+  a.slot_bytes = slot_bytes;
+  a.reports = report ? ctx->d_reports.as<pdsim_report>() : nullptr;
   a.smem_bytes = ctx->smem_bytes;
   a.next_pair = ctx->d_counter.as<unsigned long long>();
   a.results = ctx->d_results.as<pdg::PairResult>();
@@ -426,6 +452,10 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   CU(ctx, cudaMemcpyAsync(cbad.data(), ctx->d_cand_bad.p, 4 * static_cast<size_t>(C), cudaMemcpyDeviceToHost,
                           ctx->stream));
   CU(ctx, cudaMemcpyAsync(&best, ctx->d_best.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (report && n > 0) {
+    CU(ctx, cudaMemcpyAsync(out->pair_report, ctx->d_reports.p, sizeof(pdsim_report) * static_cast<size_t>(n),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   float k_ms = 0, d_ms = 0;
   CU(ctx, cudaEventElapsedTime(&k_ms, ctx->ev[1], ctx->ev[2]));

@@ -319,6 +319,8 @@ struct Caps {
   int32_t dmax;
   int32_t pres;    // PrefillW / DecodeW entries reserved in shared memory (>= pmax, dmax);
   int32_t dres;    // the device engine addresses them at compile-time offsets (EngineT<.., kD, kP>)
+  int32_t rep_r;      // report mode: TTFT value slots (max rounds); 0 = no report
+  int32_t rep_gapcap; // report mode: ITL gap histogram entries (power of two)
 };
 
 struct EngState;
@@ -346,6 +348,11 @@ struct GlobalSlot {
   Pfx* tw_p;
   Seg* seg;  // [dmax][segcap]
   uint64_t* fh;
+  double* rep_ttft;    // report mode: [rep_r] TTFT values in push order (incremental negated)
+  double* rep_e2e;     // report mode: [S] e2e latency by session-id rank (NaN = not completed)
+  uint64_t* rep_gkey;  // report mode: ITL gap histogram keys (value bits, 0 = empty)
+  int64_t* rep_gcnt;   //   and sample counts
+  unsigned long long* rep_hist;  // report mode: [256] radix-select digit histogram
 };
 
 PDG_HD size_t align_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
@@ -410,6 +417,12 @@ PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
   t.tw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * P * static_cast<size_t>(c.twcap)));
   t.seg = reinterpret_cast<Seg*>(take(sizeof(Seg) * D * static_cast<size_t>(c.segcap)));
   t.fh = reinterpret_cast<uint64_t*>(take(8 * D * static_cast<size_t>(c.fcap)));
+  const bool rep = c.rep_gapcap > 0;
+  t.rep_ttft = reinterpret_cast<double*>(take(rep ? 8 * static_cast<size_t>(c.rep_r) : 0));
+  t.rep_e2e = reinterpret_cast<double*>(take(rep ? 8 * static_cast<size_t>(c.S) : 0));
+  t.rep_gkey = reinterpret_cast<uint64_t*>(take(rep ? 8 * static_cast<size_t>(c.rep_gapcap) : 0));
+  t.rep_gcnt = reinterpret_cast<int64_t*>(take(rep ? 8 * static_cast<size_t>(c.rep_gapcap) : 0));
+  t.rep_hist = reinterpret_cast<unsigned long long*>(take(rep ? 8 * 256 : 0));
   if (s) *s = t;
   return off;
 }
@@ -537,6 +550,14 @@ struct EngState {
   int64_t n_ttft_;
   int64_t n_steps_;
   int64_t n_spans_;
+  // report mode (metrics.cpp:138-190): in-order folds and counts
+  double rep_init_sum_;
+  double rep_incr_sum_;
+  double rep_itl_sum_;
+  int64_t rep_n_init_;
+  int64_t rep_n_incr_;
+  int64_t rep_n_local_;
+  int64_t rep_n_itl_;
   int64_t events_;
   int64_t folds_;
   double st_[kMaxSlots];    // worker-event slot times (+inf when empty)
@@ -601,7 +622,7 @@ class EngineT {
       init();
       s_->attempts_ = attempt + 1;
       // Materialised ITL samples need every step as an event, in order.
-      s_->lazy_ = (attempt == 0 && !s_->REC.steps) ? 1 : 0;
+      s_->lazy_ = (attempt == 0 && !s_->REC.steps && s_->C.rep_gapcap == 0) ? 1 : 0;
       s_->exact_itl_ = (attempt > 0 || s_->REC.sessions) ? 1 : 0;
       event_loop();
       if (!s_->abort_) break;
@@ -697,6 +718,134 @@ class EngineT {
     }
   }
 
+  // ---- per-pair Report (metrics.cpp:108-190) ----
+  // One decode step's ITL samples: cnt identical values g in push order.
+  PDG_HD void report_itl_step(double g, int32_t cnt) {
+    s_->rep_itl_sum_ = fold_repeat(s_->rep_itl_sum_, g, static_cast<uint64_t>(cnt));
+    s_->rep_n_itl_ += cnt;
+    uint64_t* keys = GLP(s_->G.rep_gkey);
+    int64_t* cnts = GLP(s_->G.rep_gcnt);
+    const uint64_t key = dbits(g);  // g > 0: never the empty key 0
+    const uint32_t mask = static_cast<uint32_t>(s_->C.rep_gapcap - 1);
+    uint32_t h = static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+    bool placed = false;
+    for (uint32_t probe = 0; probe <= mask; ++probe) {  // warp-uniform probe sequence
+      const uint64_t k = keys[h];
+      if (k == key || k == 0) {
+        warp_sync();
+        if (lane_id() == 0) {
+          keys[h] = key;
+          cnts[h] = (k == 0 ? 0 : cnts[h]) + cnt;
+        }
+        warp_sync();
+        placed = true;
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+    if (!placed) fail();  // histogram capacity exceeded: loud failure
+  }
+
+  // k-th smallest (1-based) of the keys item(i) yields for i < n (items
+  // returning false are skipped), weighted: 8 radix passes over 8-bit digits.
+  template <class F>
+  PDG_HD uint64_t report_select(int64_t n, int64_t rank, F item) {
+    unsigned long long* hist = GLP(s_->G.rep_hist);
+    uint64_t prefix = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      warp_sync();
+      for (int b = lane_id(); b < 256; b += PDG_NL) hist[b] = 0;
+      warp_sync();
+      const uint64_t mask_hi = shift == 56 ? 0ull : (~0ull << (shift + 8));
+      for (int64_t i = lane_id(); i < n; i += PDG_NL) {
+        uint64_t key;
+        int64_t w;
+        if (!item(i, &key, &w) || (key & mask_hi) != prefix) continue;
+#if defined(__CUDA_ARCH__)
+        atomicAdd(&hist[(key >> shift) & 255u], static_cast<unsigned long long>(w));
+#else
+        hist[(key >> shift) & 255u] += static_cast<unsigned long long>(w);
+#endif
+      }
+      warp_sync();
+#if defined(__CUDA_ARCH__)
+      __threadfence_block();
+#endif
+      int b = 0;
+      for (; b < 255; ++b) {  // every lane scans the same histogram: uniform result
+        const int64_t c = static_cast<int64_t>(hist[b]);
+        if (rank <= c) break;
+        rank -= c;
+      }
+      prefix |= static_cast<uint64_t>(b) << shift;
+    }
+    warp_sync();
+    return prefix;
+  }
+
+  PDG_HD static int64_t p95_rank(int64_t n) {  // percentile_nearest_rank (metrics.cpp:125-136)
+    int64_t r = static_cast<int64_t>(ceil(dmul(0.95, static_cast<double>(n))));
+    return r < 1 ? 1 : r;
+  }
+
+  // build_report_from_samples (metrics.cpp:138-190) of the pair just replayed.
+  PDG_HD void build_report(pdsim_report* out) {
+    pdsim_report r;
+    memset(&r, 0, sizeof(r));
+    const int64_t completed = s_->att_.sessions_completed, nt = s_->n_ttft_, ni = s_->rep_n_itl_;
+    r.sessions_total = s_->T.S;
+    r.sessions_completed = completed;
+    if (completed == 0 && nt == 0 && ni == 0) {
+      r.empty = 1;
+      *out = r;
+      return;
+    }
+    const double* tv = GLP(s_->G.rep_ttft);
+    const int64_t ntv = nt < s_->C.rep_r ? nt : s_->C.rep_r;
+    for (int kind = 0; kind < 2; ++kind) {
+      pdsim_metric_stat& m = kind == 0 ? r.ttft_initial : r.ttft_incremental;
+      const int64_t c = kind == 0 ? s_->rep_n_init_ : s_->rep_n_incr_;
+      const double sum = kind == 0 ? s_->rep_init_sum_ : s_->rep_incr_sum_;
+      m.count = c;
+      m.mean = c > 0 ? ddiv(sum, static_cast<double>(c)) : 0.0;
+      m.p95 = c > 0 ? bitsd(report_select(ntv, p95_rank(c), [&](int64_t i, uint64_t* key, int64_t* w) {
+                const uint64_t b = dbits(tv[i]);
+                if ((b >> 63) != static_cast<uint64_t>(kind)) return false;
+                *key = b & ~(1ull << 63);
+                *w = 1;
+                return true;
+              }))
+                    : 0.0;
+    }
+    if (nt > 0) r.local_fraction = ddiv(static_cast<double>(s_->rep_n_local_), static_cast<double>(nt));
+    r.itl.count = ni;
+    r.itl.mean = ni > 0 ? ddiv(s_->rep_itl_sum_, static_cast<double>(ni)) : 0.0;
+    if (ni > 0) {
+      const uint64_t* keys = GLP(s_->G.rep_gkey);
+      const int64_t* cnts = GLP(s_->G.rep_gcnt);
+      r.itl.p95 = bitsd(report_select(s_->C.rep_gapcap, p95_rank(ni), [&](int64_t i, uint64_t* key, int64_t* w) {
+        if (keys[i] == 0) return false;
+        *key = keys[i];
+        *w = cnts[i];
+        return true;
+      }));
+    }
+    if (completed > 0) {
+      const double denom = static_cast<double>(completed);
+      r.slo_attainment = ddiv(static_cast<double>(s_->att_.slo_ok), denom);
+      r.ttft_attainment = ddiv(static_cast<double>(s_->att_.ttft_ok), denom);
+      r.itl_attainment = ddiv(static_cast<double>(s_->att_.itl_ok), denom);
+      double sum = 0.0;  // mean_in_order over sessions sorted by id
+      const double* e2e = GLP(s_->G.rep_e2e);
+      for (int32_t k = 0; k < s_->T.S; ++k) {
+        const double v = e2e[k];
+        if (v == v) sum = dadd(sum, v);
+      }
+      r.e2e_mean = ddiv(sum, denom);
+    }
+    *out = r;
+  }
+
   // Inclusive sub-scope timers (no code unless kProf).
   PDG_HD int64_t pb() const { return kProf ? pdg_clock() : 0; }
   PDG_HD void pe(int k, int64_t t0) {
@@ -782,6 +931,16 @@ class EngineT {
     s_->n_ttft_ = 0;
     s_->n_steps_ = 0;
     s_->n_spans_ = 0;
+    s_->rep_init_sum_ = s_->rep_incr_sum_ = s_->rep_itl_sum_ = 0.0;
+    s_->rep_n_init_ = s_->rep_n_incr_ = s_->rep_n_local_ = s_->rep_n_itl_ = 0;
+    if (s_->C.rep_gapcap > 0) {
+      for (int k = lane_id(); k < s_->T.S; k += PDG_NL) GLP(s_->G.rep_e2e)[k] = __builtin_nan("");
+      for (int k = lane_id(); k < s_->C.rep_gapcap; k += PDG_NL) {
+        GLP(s_->G.rep_gkey)[k] = 0;
+        GLP(s_->G.rep_gcnt)[k] = 0;
+      }
+      warp_sync();
+    }
     s_->events_ = 0;
     s_->folds_ = 0;
     s_->ctr_.events_in_order = 1;
@@ -2064,6 +2223,18 @@ class EngineT {
       o.completion_time = s_->now_;
       o.value = value;
     }
+    if (s_->C.rep_gapcap > 0) {  // report mode: TTFT value and in-order folds (metrics.cpp:152-161)
+      const int64_t nt = s_->n_ttft_;
+      if (nt < s_->C.rep_r && lane_id() == 0) GLP(s_->G.rep_ttft)[nt] = round == 1 ? value : -value;
+      if (round == 1) {
+        s_->rep_init_sum_ = dadd(s_->rep_init_sum_, value);
+        ++s_->rep_n_init_;
+      } else {
+        s_->rep_incr_sum_ = dadd(s_->rep_incr_sum_, value);
+        ++s_->rep_n_incr_;
+      }
+      if (local) ++s_->rep_n_local_;
+    }
     ++s_->n_ttft_;
     const int32_t ridx = GLP(s_->T.round_off)[i] + round - 1;
     const int32_t incr = GLP(s_->T.incr)[ridx];
@@ -2277,6 +2448,7 @@ class EngineT {
     const int64_t kv = w.kv_used;
     const int64_t tokens = s_->ctr_.tokens_decoded;
     seg_append(d, k, 1, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
+    if (s_->C.rep_gapcap > 0 && n_itl > 0) report_itl_step(dsub(now, prev), n_itl);
     if (s_->REC.steps) {
       const int64_t ns = s_->n_steps_;
       if (ns < s_->REC.steps_cap && lane_id() == 0) {
@@ -2383,6 +2555,9 @@ class EngineT {
     const bool slo_ok = ttft_ok && itl_ok;
     {  // warp-uniform stores (every lane writes the same values)
       DW(d).kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
+      if (s_->C.rep_gapcap > 0 && lane_id() == 0) {
+        GLP(s_->G.rep_e2e)[GLP(s_->T.rank)[i]] = dsub(s_->now_, GLP(s_->T.arrival)[i]);
+      }
       if (s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
         o.session_id = GLP(s_->T.sid)[i];

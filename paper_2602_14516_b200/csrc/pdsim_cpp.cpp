@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "pdsim/errors.hpp"
+#include "pdsim/metrics.hpp"
 #include "pdsim/perf_model.hpp"
 #include "pdsim/plan_search.hpp"
 #include "pdsim/planner.hpp"
@@ -572,6 +573,81 @@ std::vector<DeploymentPlan> top_k(const LatencyCoefficients& coeffs, int total_g
   return out;
 }
 
+// ---- Report aggregation (metrics.cpp:108-190), host restatement ----
+namespace {
+double mean_in_order(const std::vector<double>& v) {
+  if (v.empty()) return 0.0;
+  double s = 0.0;
+  for (double x : v) s += x;
+  return s / static_cast<double>(v.size());
+}
+MetricStat stat_of(const std::vector<double>& v) {
+  MetricStat m;
+  m.count = static_cast<std::int64_t>(v.size());
+  m.mean = mean_in_order(v);
+  m.p95 = percentile_nearest_rank(v, 0.95);
+  return m;
+}
+}  // namespace
+
+double percentile_nearest_rank(std::vector<double> values, double q) {
+  if (!(q > 0.0 && q <= 1.0)) throw DomainError("percentile: q must be in (0, 1]");
+  if (values.empty()) return 0.0;
+  const std::size_t n = values.size();
+  std::size_t rank = static_cast<std::size_t>(std::ceil(q * static_cast<double>(n)));
+  if (rank < 1) rank = 1;
+  std::nth_element(values.begin(), values.begin() + static_cast<std::ptrdiff_t>(rank - 1), values.end());
+  return values[rank - 1];
+}
+
+Report build_report_from_samples(const std::string& trace_name, std::int64_t sessions_total,
+                                 const std::vector<TtftSample>& ttft, const std::vector<ItlSample>& itl,
+                                 const std::vector<SessionOutcome>& sessions) {
+  Report r;
+  r.trace_name = trace_name;
+  r.sessions_total = sessions_total;
+  r.sessions_completed = static_cast<std::int64_t>(sessions.size());
+  if (sessions.empty() && ttft.empty() && itl.empty()) {
+    r.empty = true;
+    return r;
+  }
+  std::vector<double> initial, incremental;
+  std::int64_t local = 0;
+  for (const TtftSample& s : ttft) {
+    (s.kind == TaskKind::kInitial ? initial : incremental).push_back(s.value);
+    if (s.local) ++local;
+  }
+  r.ttft_initial = stat_of(initial);
+  r.ttft_incremental = stat_of(incremental);
+  if (!ttft.empty()) r.local_fraction = static_cast<double>(local) / static_cast<double>(ttft.size());
+  std::vector<double> gaps;
+  gaps.reserve(itl.size());
+  for (const ItlSample& s : itl) gaps.push_back(s.value);
+  r.itl = stat_of(gaps);
+  if (!sessions.empty()) {
+    std::int64_t slo = 0, t_ok = 0, i_ok = 0;
+    std::vector<double> e2e;
+    e2e.reserve(sessions.size());
+    for (const SessionOutcome& s : sessions) {
+      slo += s.slo_ok;
+      t_ok += s.ttft_ok;
+      i_ok += s.itl_ok;
+      e2e.push_back(s.completion_time - s.arrival_time);
+    }
+    const double denom = static_cast<double>(sessions.size());
+    r.slo_attainment = static_cast<double>(slo) / denom;
+    r.ttft_attainment = static_cast<double>(t_ok) / denom;
+    r.itl_attainment = static_cast<double>(i_ok) / denom;
+    r.e2e_mean = mean_in_order(e2e);
+  }
+  return r;
+}
+
+Report build_report(const SimResult& result) {
+  return build_report_from_samples(result.trace_name, result.total_sessions, result.ttft_samples,
+                                   result.itl_samples, result.sessions);
+}
+
 std::string format_plan(const DeploymentPlan& plan) {
   if (!plan.feasible) return "infeasible";
   auto phase = [](const std::map<int, int>& counts) {
@@ -743,8 +819,32 @@ SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<D
   out.pair_attainment = att.data();
   out.pair_status = status.data();
   out.candidate_slo_ok = r.candidate_slo_ok.data();
+  std::vector<pdsim_report> reps;
+  if (options.report) {
+    reps.resize(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    out.pair_report = reps.data();
+  }
   pdsim_gpu_ctx* ctx = context(options.device >= 0 ? options.device : default_device());
   check_ctx(pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out), ctx);
+  if (options.report) {
+    for (int64_t k = 0; k < n; ++k) {
+      const pdsim_report& p = reps[static_cast<size_t>(k)];
+      Report x;
+      x.trace_name = replicas[static_cast<size_t>((in.pair_begin + k) % static_cast<int64_t>(replicas.size()))].name;
+      x.empty = p.empty != 0;
+      x.sessions_total = p.sessions_total;
+      x.sessions_completed = p.sessions_completed;
+      x.slo_attainment = p.slo_attainment;
+      x.ttft_attainment = p.ttft_attainment;
+      x.itl_attainment = p.itl_attainment;
+      x.ttft_initial = {p.ttft_initial.mean, p.ttft_initial.p95, p.ttft_initial.count};
+      x.ttft_incremental = {p.ttft_incremental.mean, p.ttft_incremental.p95, p.ttft_incremental.count};
+      x.itl = {p.itl.mean, p.itl.p95, p.itl.count};
+      x.e2e_mean = p.e2e_mean;
+      x.local_fraction = p.local_fraction;
+      r.reports.push_back(x);
+    }
+  }
   r.best_candidate = out.best_candidate;
   r.best_slo_ok = out.best_slo_ok;
   r.kernel_ms = out.kernel_ms;

@@ -199,6 +199,7 @@ class SearchResult:
         self.candidate_slo_ok = cand
         self.n_pairs = n_pairs
         self.pair_events, self.pair_cycles = out._diag
+        self.reports = list(out._reports)[:n_pairs] if out._reports is not None else None
 
 
 def search_input(traces, plans, pair_begin=0, pair_end=-1):
@@ -312,7 +313,7 @@ class Context:
         r.itl_samples = [itls[k] for k in range(min(out.n_itl, out.itl_capacity))] if itl else []
         return r
 
-    def _outputs(self, n_pairs, n_cand):
+    def _outputs(self, n_pairs, n_cand, report=False):
         att = (abi.Attainment * max(n_pairs, 1))()
         ctr = (abi.Counters * max(n_pairs, 1))()
         st = (C.c_int8 * max(n_pairs, 1))()
@@ -323,14 +324,21 @@ class Context:
                                C.cast(st, C.POINTER(C.c_int8)), C.cast(cand, C.POINTER(C.c_int64)),
                                C.cast(ev, C.POINTER(C.c_int64)), C.cast(cy, C.POINTER(C.c_int64)))
         out._diag = (ev, cy)
+        out._reports = None
+        if report:
+            reps = (abi.Report * max(n_pairs, 1))()
+            out.pair_report = C.cast(reps, C.POINTER(abi.Report))
+            out._reports = reps
         return out, att, ctr, st, cand
 
-    def plan_search(self, traces, plans, profile, params, seed, pair_begin=0, pair_end=-1):
-        """Replays every (candidate, replica) pair in [pair_begin, pair_end)."""
+    def plan_search(self, traces, plans, profile, params, seed, pair_begin=0, pair_end=-1, report=False):
+        """Replays every (candidate, replica) pair in [pair_begin, pair_end).
+        report=True adds the reference's build_report of every pair
+        (SearchResult.reports)."""
         inp = search_input(traces, plans, pair_begin, pair_end)
         end = len(traces) * len(plans) if pair_end < 0 else pair_end
         n = end - pair_begin
-        out, att, ctr, st, cand = self._outputs(n, len(plans))
+        out, att, ctr, st, cand = self._outputs(n, len(plans), report)
         self._check(lib().pdsim_gpu_plan_search(self._h, C.byref(inp), C.byref(profile), C.byref(params), seed,
                                                 C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
@@ -352,11 +360,11 @@ class Context:
         self._check(lib().pdsim_gpu_stage(self._h, C.byref(inp), C.byref(profile), C.byref(params)))
         self._staged = (len(traces), len(plans))
 
-    def search_staged(self, seed, pair_begin=0, pair_end=-1):
+    def search_staged(self, seed, pair_begin=0, pair_end=-1, report=False):
         nt, nc = self._staged
         end = nt * nc if pair_end < 0 else pair_end
         n = end - pair_begin
-        out, att, ctr, st, cand = self._outputs(n, nc)
+        out, att, ctr, st, cand = self._outputs(n, nc, report)
         self._check(lib().pdsim_gpu_search_staged(self._h, pair_begin, pair_end, seed, C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
 

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "pdsim/errors.hpp"
+#include "pdsim/metrics.hpp"
 #include "pdsim/plan_search.hpp"
 #include "pdsim/planner.hpp"
 #include "pdsim/sim_engine.hpp"
@@ -145,6 +146,26 @@ int main() {
           for (const Round& rd : ss.rounds) expect += rd.decode_len - 1;
     }
     CHECK(static_cast<std::int64_t>(r.itl_samples.size()) == expect);
+  }
+
+  // Report (metrics.cpp:138-190): the device's per-pair report in the search
+  // equals build_report over the drop-in run()'s full SimResult.
+  {
+    SearchOptions so;
+    so.report = true;
+    const std::vector<DeploymentPlan> few = {simple_plan(1, 1), simple_plan(2, 2)};
+    const SearchResult sr2 = plan_search({gen}, few, p, SchedulerParams{}, 3, so);
+    CHECK(sr2.reports.size() == 2);
+    for (size_t c = 0; c < few.size() && c < sr2.reports.size(); ++c) {
+      const Report want = build_report(run(gen, few[c], p, SchedulerParams{}, 3));
+      const Report& got = sr2.reports[c];
+      CHECK(got.sessions_completed == want.sessions_completed && got.slo_attainment == want.slo_attainment);
+      CHECK(got.ttft_initial.mean == want.ttft_initial.mean && got.ttft_initial.p95 == want.ttft_initial.p95);
+      CHECK(got.ttft_incremental.mean == want.ttft_incremental.mean &&
+            got.ttft_incremental.p95 == want.ttft_incremental.p95);
+      CHECK(got.itl.mean == want.itl.mean && got.itl.p95 == want.itl.p95 && got.itl.count == want.itl.count);
+      CHECK(got.e2e_mean == want.e2e_mean && got.local_fraction == want.local_fraction);
+    }
   }
 
   // Surrogate planner (planner.hpp:55-113): the coefficient pipeline and the

@@ -15,6 +15,7 @@
 namespace {
 thread_local std::string g_err;
 size_t g_smem_budget = 0;  // 0: the device default; small values force heap spills
+thread_local pdsim_report* g_report_out = nullptr;  // hostsim_run_report: report mode
 int fail(const pdg::HostError& e) {
   g_err = e.msg;
   return e.code;
@@ -44,7 +45,11 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
     err.set(PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
     return fail(err);
   }
-  const pdg::Caps caps = pdg::compute_caps({&t}, dp.P, dp.D, *prof, *params, g_smem_budget);
+  pdg::Caps caps = pdg::compute_caps({&t}, dp.P, dp.D, *prof, *params, g_smem_budget);
+  if (g_report_out) {
+    caps.rep_r = std::max<int32_t>(t.R, 1);
+    caps.rep_gapcap = 1 << 16;
+  }
   std::vector<char> gws(pdg::global_slot_bytes(caps, nullptr, nullptr) + 256);
   std::vector<char> sws(pdg::smem_slot_bytes(caps, nullptr, nullptr) + 256);
   auto align = [](std::vector<char>& v) {
@@ -85,6 +90,7 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   pdg::PairResult res;
   std::memset(&res, 0, sizeof(res));
   eng.run(&res);
+  if (g_report_out) eng.build_report(g_report_out);
   if (res.status != PDSIM_PAIR_OK) {
     err.set(PDSIM_ERR_INTERNAL, "engine capacity or invariant violated");
     return fail(err);
@@ -126,5 +132,16 @@ extern "C" int hostsim_run_counts(const pdsim_trace* trace, const pdsim_plan* pl
   out->n_sessions = o.n_sessions;
   out->counters = o.counters;
   out->attainment = o.attainment;
+  return rc;
+}
+
+// Report mode (search pair_report path): build_report of the replay.
+extern "C" int hostsim_run_report(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_profile* prof,
+                                  const pdsim_sched_params* params, uint64_t seed, pdsim_report* report) {
+  pdsim_run_output o;
+  std::memset(&o, 0, sizeof(o));
+  g_report_out = report;
+  const int rc = hostsim_run(trace, plan, prof, params, seed, &o);
+  g_report_out = nullptr;
   return rc;
 }

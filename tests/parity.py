@@ -27,6 +27,7 @@ def hostsim():
         L.hostsim_run_counts.argtypes = L.hostsim_run.argtypes
         L.hostsim_fold_repeat.argtypes = [C.c_double, C.c_double, C.c_uint64]
         L.hostsim_fold_repeat.restype = C.c_double
+        L.hostsim_run_report.argtypes = L.hostsim_run.argtypes[:5] + [P(abi.Report)]
         _hostsim = L
     return _hostsim
 
@@ -66,6 +67,16 @@ def host_run(trace, plan, profile, params, seed):
     if rc:
         raise EngineError(rc, hostsim().hostsim_last_error().decode())
     return Run(out, dec, ttft, sess)
+
+
+def host_report(trace, plan, profile, params, seed):
+    """Host engine build in search report mode: build_report of the replay."""
+    out = abi.Report()
+    rc = hostsim().hostsim_run_report(C.byref(trace), C.byref(plan), C.byref(profile), C.byref(params), seed,
+                                      C.byref(out))
+    if rc:
+        raise EngineError(rc, hostsim().hostsim_last_error().decode())
+    return out
 
 
 def itl_capacity(trace):

@@ -179,3 +179,23 @@ def test_itl_csv_hash_emulation_matches_reference():
     _, hashes, _, _ = refbind.run(tr.view, p, prof, abi.default_params(), 1, records=True, itl=True)
     want = parity.reference_itl(tr.view, p, prof, abi.default_params(), 1)
     assert parity.itl_csv_fnv(want) == f"{hashes[3]:016x}"
+
+
+@pytest.mark.parametrize("preset,rate,plan", [("toolbench", 6.0, ({1: 2}, {1: 2})), ("hotpotqa", 25.0, ({2: 1}, {1: 3})),
+                                              ("dureader", 35.0, ({1: 1}, {1: 1, 2: 1})), ("gaia", 3.0, ({}, {1: 2})),
+                                              ("toolbench", 60.0, ({1: 1}, {1: 1}))])
+def test_engine_report_matches_reference(preset, rate, plan):
+    """Search report mode: the reference's build_report (metrics.cpp:138-190)
+    of the pair — in-order means, nearest-rank P95s (TTFT initial /
+    incremental, ITL), attainment ratios, e2e mean, local fraction —
+    bit-identical."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    tr = native.gen_trace(native.preset_stats(preset), rate, 200, 13)
+    p = abi.make_plan(*plan)
+    for prm in (abi.default_params(), abi.default_params(routing=abi.ROUTING_ALWAYS_REMOTE)):
+        got = parity.host_report(tr.view, p, prof, prm, 6)
+        want = refbind.report(tr.view, p, prof, prm, 6)
+        assert got.as_tuple() == want.as_tuple()

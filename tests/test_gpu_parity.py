@@ -154,3 +154,24 @@ def test_run_itl_samples_match_reference(ctx):
     got2 = ctx.run(tr2.view, plan2, prof, abi.default_params(), 3, itl=True)
     want2 = parity.reference_itl(tr2.view, plan2, prof, abi.default_params(), 3)
     assert not parity.diff_itl([parity.itl_tuple(x) for x in got2.itl_samples], want2)
+
+
+def test_search_reports_match_reference(ctx):
+    """Per-pair Report in the batched search: every
+    candidate x replica's build_report equals the reference's, and ranking
+    candidates by it is exact (here: lowest P95 ITL among max attainment)."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    trs = [native.gen_trace(native.preset_stats("hotpotqa"), 14.0, 300, s) for s in (1, 2)]
+    plans = native.enumerate_plans([1, 2, 4], 4)
+    prm = abi.default_params()
+    res = ctx.plan_search([t.view for t in trs], plans, prof, prm, 1, report=True)
+    for p in range(res.n_pairs):
+        c, r = divmod(p, len(trs))
+        want = refbind.report(trs[r].view, plans[c], prof, prm, 1)
+        assert res.reports[p].as_tuple() == want.as_tuple(), (c, r)
+    # attainment-only search is unchanged by report mode
+    plain = ctx.plan_search([t.view for t in trs], plans, prof, prm, 1)
+    assert [plain.candidate_slo_ok[c] for c in range(len(plans))] == [res.candidate_slo_ok[c] for c in range(len(plans))]
