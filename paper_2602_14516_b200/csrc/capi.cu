@@ -141,7 +141,7 @@ struct KernelArgs {
 // One warp per block; the warp replays pairs pulled from an atomic queue.
 // kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
 // addresses slot state at compile-time offsets (engine.cuh smem_off).
-template <bool kProf, int kD, int kP>
+template <bool kProf, int kD, int kP, bool kRec>
 __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
   const int slot_id = blockIdx.x;
   pdg::GlobalSlot gslot;
@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const pdg::DevTrace tr = a.traces[r];
       const pdg::DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      pdg::EngineT<kProf, kD, kP> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
+      pdg::EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
       eng.run(&res);
       res.cycles = clock64() - t0;
-      if (a.reports) {
+      if (kRec && a.reports) {
         pdsim_report rep;
         eng.build_report(&rep);
         if (lane == 0) a.reports[pair - a.pair_begin] = rep;
@@ -422,10 +422,14 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   if (n > 0) {
     // The diagnostics build (per-phase clock64 counters) is a separate
     // instantiation so the product kernel carries no instrumentation.
-    void (*const kernels[2][3])(KernelArgs) = {
-        {replay_kernel<false, 8, 8>, replay_kernel<false, 16, 16>, replay_kernel<false, 64, 32>},
-        {replay_kernel<true, 8, 8>, replay_kernel<true, 16, 16>, replay_kernel<true, 64, 32>}};
-    void (*kern)(KernelArgs) = kernels[ctx->profiling ? 1 : 0][ctx->layout];
+    // [0] attainment-only search, [1] diagnostics (clock64 phases), [2] with
+    // record / report outputs (drop-in run(), ITL samples, pair reports).
+    void (*const kernels[3][3])(KernelArgs) = {
+        {replay_kernel<false, 8, 8, false>, replay_kernel<false, 16, 16, false>, replay_kernel<false, 64, 32, false>},
+        {replay_kernel<true, 8, 8, false>, replay_kernel<true, 16, 16, false>, replay_kernel<true, 64, 32, false>},
+        {replay_kernel<false, 8, 8, true>, replay_kernel<false, 16, 16, true>, replay_kernel<false, 64, 32, true>}};
+    const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
+    void (*kern)(KernelArgs) = kernels[with_rec ? 2 : ctx->profiling ? 1 : 0][ctx->layout];
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
     kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;

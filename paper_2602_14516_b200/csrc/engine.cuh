@@ -586,7 +586,10 @@ static_assert(kEngStateBytes % 16 == 0, "slot layout alignment");
 
 // kProf compiles in the per-phase clock64 instrumentation (diagnostics
 // kernel only); the product kernel is EngineT<false>.
-template <bool kProf, int kD = 0, int kP = 0>
+// kRec compiles in the record / report outputs (drop-in run(), ITL
+// materialisation, per-pair reports); the attainment-only search kernel is
+// built without them.
+template <bool kProf, int kD = 0, int kP = 0, bool kRec = true>
 class EngineT {
   static constexpr SmemOff kOff = smem_off(static_cast<size_t>(kD), static_cast<size_t>(kP));
 
@@ -622,8 +625,8 @@ class EngineT {
       init();
       s_->attempts_ = attempt + 1;
       // Materialised ITL samples need every step as an event, in order.
-      s_->lazy_ = (attempt == 0 && !s_->REC.steps && s_->C.rep_gapcap == 0) ? 1 : 0;
-      s_->exact_itl_ = (attempt > 0 || s_->REC.sessions) ? 1 : 0;
+      s_->lazy_ = (attempt == 0 && !(kRec && (s_->REC.steps || s_->C.rep_gapcap > 0))) ? 1 : 0;
+      s_->exact_itl_ = (attempt > 0 || (kRec && s_->REC.sessions)) ? 1 : 0;
       event_loop();
       if (!s_->abort_) break;
     }
@@ -933,7 +936,7 @@ class EngineT {
     s_->n_spans_ = 0;
     s_->rep_init_sum_ = s_->rep_incr_sum_ = s_->rep_itl_sum_ = 0.0;
     s_->rep_n_init_ = s_->rep_n_incr_ = s_->rep_n_local_ = s_->rep_n_itl_ = 0;
-    if (s_->C.rep_gapcap > 0) {
+    if (kRec && s_->C.rep_gapcap > 0) {
       for (int k = lane_id(); k < s_->T.S; k += PDG_NL) GLP(s_->G.rep_e2e)[k] = __builtin_nan("");
       for (int k = lane_id(); k < s_->C.rep_gapcap; k += PDG_NL) {
         GLP(s_->G.rep_gkey)[k] = 0;
@@ -1351,7 +1354,7 @@ class EngineT {
     const int64_t tr0 = pb();
     const RouteOut r = decide(i, bound, ctx, incr);
     pe(kProfRoute, tr0);
-    if (s_->REC.decisions && lane_id() == 0) {
+    if (kRec && s_->REC.decisions && lane_id() == 0) {
       pdsim_decision& d = s_->REC.decisions[s_->n_dec_];
       d.time = s_->now_;
       d.session_id = GLP(s_->T.sid)[i];
@@ -1588,7 +1591,7 @@ class EngineT {
       est = shfl_d(lo, owner);
       est_exact = shfl_i(ex, owner) != 0;
     }
-    if (!est_exact && s_->REC.decisions) {
+    if (kRec && !est_exact && s_->REC.decisions) {
       double a, b;
       bool e;
       estimate(d, ctx, incr, winner, true, &a, &b, &e);
@@ -2212,7 +2215,7 @@ class EngineT {
     const double created = round == 1 ? GLP(s_->T.arrival)[i] : s.t_enq;
     const double value = dsub(s_->now_, created);
     if (!local) ttft_add(p, value);  // decode workers' TTFT windows are never queried
-    if (s_->REC.ttft && lane_id() == 0) {
+    if (kRec && s_->REC.ttft && lane_id() == 0) {
       pdsim_ttft_sample& o = s_->REC.ttft[s_->n_ttft_];
       o.session_id = GLP(s_->T.sid)[i];
       o.round = round;
@@ -2223,7 +2226,7 @@ class EngineT {
       o.completion_time = s_->now_;
       o.value = value;
     }
-    if (s_->C.rep_gapcap > 0) {  // report mode: TTFT value and in-order folds (metrics.cpp:152-161)
+    if (kRec && s_->C.rep_gapcap > 0) {  // report mode: TTFT value and in-order folds (metrics.cpp:152-161)
       const int64_t nt = s_->n_ttft_;
       if (nt < s_->C.rep_r && lane_id() == 0) GLP(s_->G.rep_ttft)[nt] = round == 1 ? value : -value;
       if (round == 1) {
@@ -2448,8 +2451,8 @@ class EngineT {
     const int64_t kv = w.kv_used;
     const int64_t tokens = s_->ctr_.tokens_decoded;
     seg_append(d, k, 1, now, dsub(now, prev), static_cast<uint32_t>(n_itl));
-    if (s_->C.rep_gapcap > 0 && n_itl > 0) report_itl_step(dsub(now, prev), n_itl);
-    if (s_->REC.steps) {
+    if (kRec && s_->C.rep_gapcap > 0 && n_itl > 0) report_itl_step(dsub(now, prev), n_itl);
+    if (kRec && s_->REC.steps) {
       const int64_t ns = s_->n_steps_;
       if (ns < s_->REC.steps_cap && lane_id() == 0) {
         StepRec& r = s_->REC.steps[ns];
@@ -2490,7 +2493,7 @@ class EngineT {
         ilo = add_rd(ilo, rlo);
         ihi = add_ru(ihi, rhi);
       }
-      if (s_->REC.spans) {
+      if (kRec && s_->REC.spans) {
         const int64_t nsp = s_->n_spans_;
         if (lane_id() == 0) {
           SpanRec& r = s_->REC.spans[nsp];
@@ -2555,10 +2558,10 @@ class EngineT {
     const bool slo_ok = ttft_ok && itl_ok;
     {  // warp-uniform stores (every lane writes the same values)
       DW(d).kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
-      if (s_->C.rep_gapcap > 0 && lane_id() == 0) {
+      if (kRec && s_->C.rep_gapcap > 0 && lane_id() == 0) {
         GLP(s_->G.rep_e2e)[GLP(s_->T.rank)[i]] = dsub(s_->now_, GLP(s_->T.arrival)[i]);
       }
-      if (s_->REC.sessions) {
+      if (kRec && s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
         o.session_id = GLP(s_->T.sid)[i];
         o.arrival_time = GLP(s_->T.arrival)[i];
