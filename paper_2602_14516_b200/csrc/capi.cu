@@ -426,7 +426,8 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     // record / report outputs (drop-in run(), ITL samples, pair reports).
     void (*const kernels[3][3])(KernelArgs) = {
         {replay_kernel<false, 8, 8, false>, replay_kernel<false, 16, 16, false>, replay_kernel<false, 64, 32, false>},
-        {replay_kernel<true, 8, 8, false>, replay_kernel<true, 16, 16, false>, replay_kernel<true, 64, 32, false>},
+        // (diagnostics are built for the N <= 8 layout only; larger plans run uninstrumented)
+        {replay_kernel<true, 8, 8, false>, replay_kernel<false, 16, 16, false>, replay_kernel<false, 64, 32, false>},
         {replay_kernel<false, 8, 8, true>, replay_kernel<false, 16, 16, true>, replay_kernel<false, 64, 32, true>}};
     const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
     void (*kern)(KernelArgs) = kernels[with_rec ? 2 : ctx->profiling ? 1 : 0][ctx->layout];

@@ -589,8 +589,15 @@ static_assert(kEngStateBytes % 16 == 0, "slot layout alignment");
 // kRec compiles in the record / report outputs (drop-in run(), ITL
 // materialisation, per-pair reports); the attainment-only search kernel is
 // built without them.
-template <bool kProf, int kD = 0, int kP = 0, bool kRec = true>
+struct EngineAttach {};
+
+// kLazy: lazy decode stepping (silent steps are not events). The exact
+// engine (kLazy = false) replays a pair whose lazy attempt hit an ambiguous
+// tie, and runs record modes that need every step as an event.
+template <bool kProf, int kD = 0, int kP = 0, bool kRec = true, bool kLazy = true>
 class EngineT {
+  template <bool, int, int, bool, bool>
+  friend class EngineT;
   static constexpr SmemOff kOff = smem_off(static_cast<size_t>(kD), static_cast<size_t>(kP));
 
  public:
@@ -620,17 +627,33 @@ class EngineT {
   PDG_HD void run(PairResult* out) {
     // Lazy decode stepping first; an ambiguous equal-time ordering between a
     // lazily advanced decode step and another decode step aborts the attempt,
-    // and the pair is replayed with every step as an explicit event.
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      init();
-      s_->attempts_ = attempt + 1;
-      // Materialised ITL samples need every step as an event, in order.
-      s_->lazy_ = (attempt == 0 && !(kRec && (s_->REC.steps || s_->C.rep_gapcap > 0))) ? 1 : 0;
-      s_->exact_itl_ = (attempt > 0 || (kRec && s_->REC.sessions)) ? 1 : 0;
-      event_loop();
-      if (!s_->abort_) break;
+    // and the pair is replayed by the exact engine with every step an event.
+    // Materialised ITL samples and reports need every step as an event too.
+    const bool exact_first = kRec && (s_->REC.steps || s_->C.rep_gapcap > 0);
+    if (kLazy && !exact_first) {
+      attempt(0);
+      if (!s_->abort_) {
+        finish_result(out);
+        return;
+      }
     }
-    finish_result(out);
+    EngineT<kProf, kD, kP, kRec, false> exact{EngineAttach{}};
+#if !defined(__CUDA_ARCH__)
+    exact.s_ = s_;
+#endif
+    exact.attempt(kLazy && !exact_first ? 1 : 0);
+    exact.finish_result(out);
+  }
+
+  // Attaches to an engine state already set up by the full constructor.
+  PDG_HD explicit EngineT(EngineAttach) {}
+
+  PDG_HD void attempt(int a) {
+    init();
+    s_->attempts_ = a + 1;
+    s_->lazy_ = kLazy ? 1 : 0;
+    s_->exact_itl_ = (!kLazy || (kRec && s_->REC.sessions)) ? 1 : 0;
+    event_loop();
   }
 
   PDG_HD void event_loop() {
@@ -670,7 +693,7 @@ class EngineT {
       // event at an equal time (sim_engine.cpp:137-143).
       if (s_->next_arr_ < s_->T.S && (src < 0 || s_->next_arr_t_ <= bt)) src = 2;
       if (src < 0) {
-        if (s_->lazy_) catch_up(kInf, 0);  // drain silent steps (none remain)
+        if (kLazy) catch_up(kInf, 0);  // drain silent steps (none remain)
         break;
       }
       if (src == 2) {
@@ -686,7 +709,7 @@ class EngineT {
       const uint32_t kind = static_cast<uint32_t>(bk >> 58);
       // Two decode-step events at the same time: their order is the
       // scheduling order, which lazily materialised steps do not carry.
-      if (s_->lazy_ && src == 0 && kind == kDecodeStep && slot_tie) {
+      if (kLazy && src == 0 && kind == kDecodeStep && slot_tie) {
         s_->abort_ = 1;
         return;
       }
@@ -1247,7 +1270,7 @@ class EngineT {
     const int D = s_->PL.D;
     const double t = s_->now_;
     const uint32_t kind = s_->cur_kind_;
-    const bool lazy = s_->lazy_ != 0;
+    constexpr bool lazy = kLazy;
     const int64_t kvb = PDG_PROF.kv_bytes_per_token;
     uint64_t key = ~0ull;
     bool ab = false;
@@ -1790,7 +1813,7 @@ class EngineT {
     return r_;
   }
   PDG_HD bool itl_has_slack_(int d, double thr) {
-    if (s_->lazy_) catch_up_worker(d, s_->now_, s_->cur_kind_);
+    if (kLazy) catch_up_worker(d, s_->now_, s_->cur_kind_);
     seg_trim(d, s_->now_);
     const DecodeW& w = DW(d);
     // Exact window sum S = sum over in-window steps of cnt * gap, bracketed
@@ -2306,7 +2329,7 @@ class EngineT {
       // catch_up(); only the step where a member finishes is an event.
       int32_t b = steps;
       double b_end = end;
-      if (s_->lazy_ && w.fh_n > 0) {
+      if (kLazy && w.fh_n > 0) {
         const int32_t fin = static_cast<int32_t>(w.fh_top >> 32);
         if (fin > steps) {
           b = fin;
@@ -2423,7 +2446,7 @@ class EngineT {
   // that step's end becomes an explicit event (its successor differs).
   PDG_HD void interrupt_run(int d) {
     DecodeW& w = DW(d);
-    if (!s_->lazy_ || !w.stepping) return;
+    if (!kLazy || !w.stepping) return;
     catch_up_worker(d, s_->now_, s_->cur_kind_);
     const int32_t k = w.steps - 1;
     if (w.run_b <= k) return;
@@ -2442,7 +2465,7 @@ class EngineT {
 
   PDG_HD void on_decode_step(int d) {
     DecodeW& w = DW(d);
-    if (s_->lazy_) catch_up_worker(d, s_->now_, kDecodeStep);
+    if (kLazy) catch_up_worker(d, s_->now_, kDecodeStep);
     const int32_t k = w.steps - 1;  // index of the step that just ended
     const int32_t cohort = w.cohort_n;
     const int32_t n_itl = cohort - w.first_n;
@@ -2485,7 +2508,7 @@ class EngineT {
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
       double ilo = s.itl_lo, ihi = s.itl_hi;
-      if (s_->exact_itl_) {
+      if (!kLazy || (kRec && s_->exact_itl_)) {
         sum = seg_fold(d, s.join + 1, k, sum, s.seg_hint);
       } else if (dec > 1) {
         double rlo, rhi;
@@ -2544,7 +2567,7 @@ class EngineT {
     const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
     const bool ttft_ok = !s.ttft_bad;
     bool itl_ok;
-    if (s_->exact_itl_ || cnt == 0) {
+    if (!kLazy || (kRec && s_->exact_itl_) || cnt == 0) {
       itl_ok = cnt == 0 || mean_itl <= s_->T.itl_thres;
     } else {
       // search mode: certified decision of fl(fold / cnt) <= itl_thres
