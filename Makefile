@@ -21,6 +21,10 @@ $(PKG)/build/capi.o: $(CSRC)/capi.cu $(HDRS)
 	@mkdir -p $(PKG)/build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(PKG)/build/ptxas.log || (cat $(PKG)/build/ptxas.log; false)
 
+$(PKG)/build/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
+	@mkdir -p $(PKG)/build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(PKG)/build/ptxas_l$*.log || (cat $(PKG)/build/ptxas_l$*.log; false)
+
 $(PKG)/build/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(PKG)/build
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
@@ -33,7 +37,7 @@ $(PKG)/build/pdsim_cpp.o: $(CSRC)/pdsim_cpp.cpp $(HDRS) $(CPPHDRS)
 	@mkdir -p $(PKG)/build
 	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
 
-$(LIB): $(PKG)/build/capi.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o
+$(LIB): $(PKG)/build/capi.o $(PKG)/build/replay_l0.o $(PKG)/build/replay_l1.o $(PKG)/build/replay_l2.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 # C++ drop-in API check program (links the product library; runs on a GPU box).

@@ -26,6 +26,7 @@
 #include "engine.cuh"
 #include "pack.hpp"
 #include "planner.cuh"
+#include "replay.cuh"
 #include "pdsim_gpu.h"
 
 namespace {
@@ -113,93 +114,6 @@ int cuda_err(pdsim_gpu_ctx* ctx, cudaError_t e, const char* what) {
 
 // ---------------------------------------------------------------------------
 // Kernels
-
-struct KernelArgs {
-  const pdg::DevTrace* traces;
-  const pdg::DevPlan* plans;
-  const int8_t* pair_invalid;  // [n_candidates * n_traces]
-  int32_t n_traces;
-  int32_t reserved;
-  int64_t pair_begin;
-  int64_t pair_end;
-  pdg::DevParams params;
-  pdg::Caps caps;
-  char* ws;
-  size_t slot_bytes;
-  size_t smem_bytes;
-  unsigned long long* next_pair;
-  pdg::PairResult* results;            // [pair_end - pair_begin]
-  unsigned long long* cand_sum;        // [n_candidates]
-  int* cand_bad;                       // [n_candidates]
-  pdg::Records rec;                    // single-run records (one pair only)
-  pdsim_report* reports;               // optional per-pair reports [pair_end - pair_begin]
-  uint64_t seed;
-  int32_t profile;                     // per-phase clock64 instrumentation
-  int32_t reserved2;
-};
-
-// One warp per block; the warp replays pairs pulled from an atomic queue.
-// kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
-// addresses slot state at compile-time offsets (engine.cuh smem_off).
-template <bool kProf, int kD, int kP, bool kRec>
-__global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
-  const int slot_id = blockIdx.x;
-  pdg::GlobalSlot gslot;
-  pdg::global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
-  pdg::SmemSlot sslot;
-  pdg::smem_slot_bytes(a.caps, &sslot, pdg::pdg_smem);  // EngState first (engine.cuh)
-  {
-    constexpr pdg::SmemOff off = pdg::smem_off(kD, kP);
-    if (a.caps.dres != kD || a.caps.pres != kP || reinterpret_cast<char*>(sslot.dw) != pdg::pdg_smem + off.dw ||
-        reinterpret_cast<char*>(sslot.pw) != pdg::pdg_smem + off.pw || reinterpret_cast<char*>(sslot.heap) != pdg::pdg_smem + off.heap) {
-      __trap();  // host/device slot layouts disagree: never replay on a wrong layout
-    }
-  }
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    unsigned long long ticket = 0;
-    if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
-    ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    const int64_t pair = static_cast<int64_t>(ticket) + a.pair_begin;
-    if (pair >= a.pair_end) break;
-    const int32_t c = static_cast<int32_t>(pair / a.n_traces);
-    const int32_t r = static_cast<int32_t>(pair % a.n_traces);
-    pdg::PairResult res;
-    memset(&res, 0, sizeof(res));
-    if (a.pair_invalid[pair]) {
-      res.status = PDSIM_PAIR_INVALID;
-      res.att.sessions_total = a.traces[r].S;
-      if (a.reports && lane == 0) {
-        pdsim_report rep;
-        memset(&rep, 0, sizeof(rep));
-        rep.sessions_total = a.traces[r].S;
-        rep.empty = 1;
-        a.reports[pair - a.pair_begin] = rep;
-      }
-    } else {
-      const pdg::DevTrace tr = a.traces[r];
-      const pdg::DevPlan pl = a.plans[c];
-      const long long t0 = clock64();
-      pdg::EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
-      eng.run(&res);
-      res.cycles = clock64() - t0;
-      if (kRec && a.reports) {
-        pdsim_report rep;
-        eng.build_report(&rep);
-        if (lane == 0) a.reports[pair - a.pair_begin] = rep;
-      }
-    }
-    if (lane == 0) {
-      a.results[pair - a.pair_begin] = res;
-      if (res.status != PDSIM_PAIR_OK) {
-        atomicOr(&a.cand_bad[c], 1);
-      } else {
-        atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
-      }
-    }
-    __syncwarp();
-  }
-}
 
 // Packed key: (slo_ok + 1) << 32 | (0xffffffff - c); 0 = invalid. One max
 // reduction yields max count with ties to the smallest index.
@@ -339,8 +253,7 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   CU(ctx, ctx->d_invalid.reserve(ctx->pair_invalid.size()));
   CU(ctx, cudaMemcpyAsync(ctx->d_invalid.p, ctx->pair_invalid.data(), ctx->pair_invalid.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
-  CU(ctx, cudaMemcpyToSymbolAsync(pdg::c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice,
-                                  ctx->stream));
+  CU(ctx, pdg::replay_set_profile(profile, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (h2d_bytes) {
     *h2d_bytes = static_cast<int64_t>(off + sizeof(pdg::DevTrace) * dt.size() +
@@ -396,7 +309,7 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   CU(ctx, cudaMemsetAsync(ctx->d_cand_bad.p, 0, 4 * static_cast<size_t>(C), ctx->stream));
   CU(ctx, cudaMemsetAsync(ctx->d_counter.p, 0, 8, ctx->stream));
 
-  KernelArgs a;
+  pdg::KernelArgs a;
   memset(&a, 0, sizeof(a));
   a.traces = ctx->d_traces.as<pdg::DevTrace>();
   a.plans = ctx->d_plans.as<pdg::DevPlan>();
@@ -422,15 +335,13 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   if (n > 0) {
     // The diagnostics build (per-phase clock64 counters) is a separate
     // instantiation so the product kernel carries no instrumentation.
-    // [0] attainment-only search, [1] diagnostics (clock64 phases), [2] with
-    // record / report outputs (drop-in run(), ITL samples, pair reports).
-    void (*const kernels[3][3])(KernelArgs) = {
-        {replay_kernel<false, 8, 8, false>, replay_kernel<false, 16, 16, false>, replay_kernel<false, 64, 32, false>},
-        // (diagnostics are built for the N <= 8 layout only; larger plans run uninstrumented)
-        {replay_kernel<true, 8, 8, false>, replay_kernel<false, 16, 16, false>, replay_kernel<false, 64, 32, false>},
-        {replay_kernel<false, 8, 8, true>, replay_kernel<false, 16, 16, true>, replay_kernel<false, 64, 32, true>}};
+    // variant 0: attainment-only search, 1: diagnostics (clock64 phases;
+    // N <= 8 layout only), 2: record / report outputs (drop-in run(), ITL
+    // samples, pair reports). Each layout's kernels live in their own
+    // translation unit (replay_l*.cu).
     const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
-    void (*kern)(KernelArgs) = kernels[with_rec ? 2 : ctx->profiling ? 1 : 0][ctx->layout];
+    const int variant = with_rec ? 2 : ctx->profiling ? 1 : 0;
+    pdg::ReplayKernel kern = pdg::replay_kernel_for(ctx->layout, variant);
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
     kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;

@@ -1,0 +1,118 @@
+// replay.cuh — the persistent replay kernel (one warp per workspace slot
+// pulling (candidate, replica) pairs from an atomic queue; engine.cuh replays
+// each pair; SLO counts folded into per-candidate integer sums) and its
+// launch table. The kernels of each shared-memory layout are compiled in
+// their own translation unit (replay_l0/l1/l2.cu) so they build in parallel;
+// each unit owns its copy of the __constant__ cost model.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+
+namespace pdg {
+
+struct KernelArgs {
+  const DevTrace* traces;
+  const DevPlan* plans;
+  const int8_t* pair_invalid;  // [n_candidates * n_traces]
+  int32_t n_traces;
+  int32_t reserved;
+  int64_t pair_begin;
+  int64_t pair_end;
+  DevParams params;
+  Caps caps;
+  char* ws;
+  size_t slot_bytes;
+  size_t smem_bytes;
+  unsigned long long* next_pair;
+  PairResult* results;            // [pair_end - pair_begin]
+  unsigned long long* cand_sum;        // [n_candidates]
+  int* cand_bad;                       // [n_candidates]
+  Records rec;                    // single-run records (one pair only)
+  pdsim_report* reports;               // optional per-pair reports [pair_end - pair_begin]
+  uint64_t seed;
+  int32_t profile;                     // per-phase clock64 instrumentation
+  int32_t reserved2;
+};
+
+// One warp per block; the warp replays pairs pulled from an atomic queue.
+// kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
+// addresses slot state at compile-time offsets (engine.cuh smem_off).
+template <bool kProf, int kD, int kP, bool kRec>
+__global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
+  const int slot_id = blockIdx.x;
+  GlobalSlot gslot;
+  global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);
+  SmemSlot sslot;
+  smem_slot_bytes(a.caps, &sslot, pdg_smem);  // EngState first (engine.cuh)
+  {
+    constexpr SmemOff off = smem_off(kD, kP);
+    if (a.caps.dres != kD || a.caps.pres != kP || reinterpret_cast<char*>(sslot.dw) != pdg_smem + off.dw ||
+        reinterpret_cast<char*>(sslot.pw) != pdg_smem + off.pw || reinterpret_cast<char*>(sslot.heap) != pdg_smem + off.heap) {
+      __trap();  // host/device slot layouts disagree: never replay on a wrong layout
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long ticket = 0;
+    if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    const int64_t pair = static_cast<int64_t>(ticket) + a.pair_begin;
+    if (pair >= a.pair_end) break;
+    const int32_t c = static_cast<int32_t>(pair / a.n_traces);
+    const int32_t r = static_cast<int32_t>(pair % a.n_traces);
+    PairResult res;
+    memset(&res, 0, sizeof(res));
+    if (a.pair_invalid[pair]) {
+      res.status = PDSIM_PAIR_INVALID;
+      res.att.sessions_total = a.traces[r].S;
+      if (a.reports && lane == 0) {
+        pdsim_report rep;
+        memset(&rep, 0, sizeof(rep));
+        rep.sessions_total = a.traces[r].S;
+        rep.empty = 1;
+        a.reports[pair - a.pair_begin] = rep;
+      }
+    } else {
+      const DevTrace tr = a.traces[r];
+      const DevPlan pl = a.plans[c];
+      const long long t0 = clock64();
+      EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
+      eng.run(&res);
+      res.cycles = clock64() - t0;
+      if (kRec && a.reports) {
+        pdsim_report rep;
+        eng.build_report(&rep);
+        if (lane == 0) a.reports[pair - a.pair_begin] = rep;
+      }
+    }
+    if (lane == 0) {
+      a.results[pair - a.pair_begin] = res;
+      if (res.status != PDSIM_PAIR_OK) {
+        atomicOr(&a.cand_bad[c], 1);
+      } else {
+        atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+
+using ReplayKernel = void (*)(KernelArgs);
+
+// Kernel of layout (0: <8,8>, 1: <16,16>, 2: <64,32>) and variant (0 search,
+// 1 diagnostics, 2 records/reports); defined across replay_l*.cu.
+ReplayKernel replay_kernel_for(int layout, int variant);
+// Copies the cost model into every translation unit's __constant__ bank.
+cudaError_t replay_set_profile(const pdsim_profile* profile, cudaStream_t stream);
+
+ReplayKernel replay_kernels_l0(int variant);
+ReplayKernel replay_kernels_l1(int variant);
+ReplayKernel replay_kernels_l2(int variant);
+cudaError_t replay_set_profile_l0(const pdsim_profile* profile, cudaStream_t stream);
+cudaError_t replay_set_profile_l1(const pdsim_profile* profile, cudaStream_t stream);
+cudaError_t replay_set_profile_l2(const pdsim_profile* profile, cudaStream_t stream);
+
+}  // namespace pdg

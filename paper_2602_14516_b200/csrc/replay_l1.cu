@@ -1,0 +1,20 @@
+// replay_l1.cu — replay kernels of the <16,16> shared-memory layout
+// (replay.cuh). Kept in its own translation unit for parallel builds.
+#include "replay.cuh"
+
+namespace pdg {
+
+ReplayKernel replay_kernels_l1(int variant) {
+  switch (variant) {
+    case 2:
+      return replay_kernel<false, 16, 16, true>;
+    default:  // diagnostics are built for the <8,8> layout only
+      return replay_kernel<false, 16, 16, false>;
+  }
+}
+
+cudaError_t replay_set_profile_l1(const pdsim_profile* profile, cudaStream_t stream) {
+  return cudaMemcpyToSymbolAsync(c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice, stream);
+}
+
+}  // namespace pdg

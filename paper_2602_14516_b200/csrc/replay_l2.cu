@@ -1,0 +1,20 @@
+// replay_l2.cu — replay kernels of the <64,32> shared-memory layout
+// (replay.cuh). Kept in its own translation unit for parallel builds.
+#include "replay.cuh"
+
+namespace pdg {
+
+ReplayKernel replay_kernels_l2(int variant) {
+  switch (variant) {
+    case 2:
+      return replay_kernel<false, 64, 32, true>;
+    default:  // diagnostics are built for the <8,8> layout only
+      return replay_kernel<false, 64, 32, false>;
+  }
+}
+
+cudaError_t replay_set_profile_l2(const pdsim_profile* profile, cudaStream_t stream) {
+  return cudaMemcpyToSymbolAsync(c_profile, profile, sizeof(pdsim_profile), 0, cudaMemcpyHostToDevice, stream);
+}
+
+}  // namespace pdg
