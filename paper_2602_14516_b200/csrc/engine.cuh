@@ -226,8 +226,9 @@ struct SessRt {
   double t_enq;      // enqueue time of the current task (== created for r >= 2)
   double itl_sum;    // exact mode: sequential fold of this session's ITL samples
   double bind_time;  // admission time
+  double e_join;     // lazy search mode: end time of step `join` (stamped when it starts)
   int32_t itl_cnt;
-  int32_t itl_pad;
+  int32_t next_pend; // lazy search mode: next session waiting for its round's first step
   int32_t join;      // step index at which the current round joined the batch
   int32_t ctx;       // context_len
   int32_t seg_hint;  // bound worker's open-segment index when the round joined
@@ -303,6 +304,8 @@ struct DecodeW {  // shared memory
   int32_t seg_keep;
   int32_t seg_head;
   int32_t seg_off;
+  int32_t pend_head;  // lazy search mode: sessions whose round starts with the next step
+  int32_t pend_pad;
 };
 
 // Capacities (host-computed provable upper bounds, see pack.hpp).
@@ -1023,6 +1026,8 @@ class EngineT {
         w.cur_end = 0.0;
         w.run_b = 0;
         w.run_pad = 0;
+        w.pend_head = -1;
+        w.pend_pad = 0;
       }
     }
     s_->mt_idx_ = Mt64::kN;
@@ -2277,6 +2282,10 @@ class EngineT {
       s.ctx += incr;
       s.join = join;
       s.seg_hint = hint;
+      if (kLazy) {
+        s.next_pend = w.pend_head;
+        w.pend_head = i;
+      }
       w.kv_used += static_cast<int64_t>(incr) * PDG_PROF.kv_bytes_per_token;
       ++w.batch_n;
       ++w.n_new;
@@ -2324,6 +2333,16 @@ class EngineT {
       const int32_t first = w.n_new;
       const int32_t steps = w.steps;  // index of the step starting now
       const double end = dadd(s_->now_, dur);
+      if (kLazy) {  // stamp the end of this step on the rounds starting with it (their e_join)
+        for (int32_t j = w.pend_head; j >= 0;) {
+          SessRt& q = GLP(s_->G.sess)[j];
+          const int32_t nx = q.next_pend;
+          warp_sync();
+          if (lane_id() == 0) q.e_join = end;
+          j = nx;
+        }
+        w.pend_head = -1;
+      }
       // Lazy mode: steps before the next round end of a batch member are
       // "silent" (no state outside this worker changes) and are advanced by
       // catch_up(); only the step where a member finishes is an event.
@@ -2511,8 +2530,12 @@ class EngineT {
       if (!kLazy || (kRec && s_->exact_itl_)) {
         sum = seg_fold(d, s.join + 1, k, sum, s.seg_hint);
       } else if (dec > 1) {
-        double rlo, rhi;
-        seg_span(d, s.join, s.seg_hint, &rlo, &rhi);
+        // ITL samples at steps join+1..k sum to within a relative u of
+        // e_k - e_join (every sample is fl(e_j - e_{j-1})).
+        const double now = s_->now_, ej = s.e_join;
+        double rlo = mul_rd(sub_rd(now, ej), 1.0 - 0x1p-51);
+        const double rhi = mul_ru(sub_ru(now, ej), 1.0 + 0x1p-51);
+        if (rlo < 0.0) rlo = 0.0;
         ilo = add_rd(ilo, rlo);
         ihi = add_ru(ihi, rhi);
       }
