@@ -81,6 +81,7 @@ inline T* GLP(T* p) {
 #endif
 
 constexpr int kMaxSlots = 64;
+constexpr int32_t kSmallHeap = 64;  // session events kept unordered (lanes scan them) up to this count
 constexpr int kSlotsPerLane = kMaxSlots / PDG_NL;
 constexpr double kInf = __builtin_huge_val();
 
@@ -533,6 +534,7 @@ struct EngState {
   uint64_t seq_;
   int32_t hn_;
   int32_t heap_spilled_;
+  int32_t hsmall_;  // session events form an unordered set of <= kSmallHeap entries in shared memory
   int32_t next_arr_;
   int32_t adm_head_;
   int32_t rr_next_;
@@ -680,9 +682,10 @@ class EngineT {
       double bt;
       uint64_t bk;
       bool slot_tie;
-      next_slot_event(nslots, &bt, &bk, &slot_tie);
-      int src = bk == ~0ull ? -1 : 0;  // 0 slot, 1 heap, 2 arrival
-      if (s_->hn_ > 0) {
+      int wid;
+      next_slot_event(nslots, &bt, &bk, &slot_tie, &wid);
+      int src = bk == ~0ull ? -1 : (wid >= kMaxSlots ? 1 : 0);  // 0 slot, 1 session event, 2 arrival
+      if (!s_->hsmall_ && s_->hn_ > 0) {
         double ht;
         uint64_t hk;
         heap_top(&ht, &hk);
@@ -723,7 +726,7 @@ class EngineT {
                                            : (static_cast<int>(bk & 63u) < D ? (kind == kDecodeStep ? kProfDecodeStep : kProfLocalPrefill)
                                               : (static_cast<int>(bk & 63u) < D + P ? kProfPrefillDone : kProfHistory)));
       if (src == 1) {
-        const HEv e = heap_pop();
+        const HEv e = wid >= kMaxSlots ? heap_take(wid - kMaxSlots) : heap_pop();
         if (kind == kInteractionDone) {
           on_interaction_done(static_cast<int32_t>(e.a));
         } else {
@@ -944,6 +947,7 @@ class EngineT {
     s_->seq_ = static_cast<uint64_t>(s_->T.S);  // arrivals took seq 0..S-1
     s_->hn_ = 0;
     s_->heap_spilled_ = false;
+    s_->hsmall_ = 1;
     s_->next_arr_ = 0;
     s_->next_arr_t_ = s_->T.S > 0 ? GLP(s_->T.arrival)[0] : 0.0;
     s_->adm_head_ = 0;
@@ -1100,14 +1104,23 @@ class EngineT {
   // their bit patterns order like unsigned integers: two warp REDUX.MIN on
   // the 32-bit halves find the earliest time; equal times (rare) are broken
   // by the key the same way.
-  PDG_HD void next_slot_event(int nslots, double* bt_out, uint64_t* bk_out, bool* tie_out) const {
+  // Earliest pending event among the worker slots and, while the session
+  // events are a small unordered set, those too: one warp reduction over
+  // (time, key). *id_out is the slot index, or kMaxSlots + the session-event
+  // entry. Times are >= 0 (or +inf), so their bit patterns order like
+  // unsigned integers: two REDUX.MIN on the 32-bit halves find the earliest
+  // time; equal times (rare) are broken by the key the same way.
+  PDG_HD void next_slot_event(int nslots, double* bt_out, uint64_t* bk_out, bool* tie_out, int* id_out) const {
+    const int hn = s_->hsmall_ ? s_->hn_ : 0;
 #if defined(__CUDA_ARCH__)
     const int lane = lane_id();
     uint64_t tb = 0x7ff0000000000000ull;  // +inf
     uint64_t kb = ~0ull;
+    int id = -1;
     if (lane < nslots) {
       tb = dbits(s_->st_[lane]);
       kb = s_->sk_[lane];
+      id = lane;
     }
     if (lane + 32 < nslots) {
       const uint64_t t2 = dbits(s_->st_[lane + 32]);
@@ -1115,6 +1128,19 @@ class EngineT {
       if (t2 < tb || (t2 == tb && k2 < kb)) {
         tb = t2;
         kb = k2;
+        id = lane + 32;
+      }
+    }
+    if (hn > 0) {
+      const HEv* h = SHEAP();
+      for (int j = lane; j < hn; j += 32) {
+        const uint64_t t2 = dbits(h[j].t);
+        const uint64_t k2 = h[j].key;
+        if (t2 < tb || (t2 == tb && k2 < kb)) {
+          tb = t2;
+          kb = k2;
+          id = kMaxSlots + j;
+        }
       }
     }
     const uint32_t hi = static_cast<uint32_t>(tb >> 32);
@@ -1124,7 +1150,7 @@ class EngineT {
     const bool at = hi == mhi && static_cast<uint32_t>(tb) == mlo;
     uint32_t b = __ballot_sync(0xffffffffu, at);
     *tie_out = __popc(b) > 1 && mhi != 0x7ff00000u;
-    if (__popc(b) > 1) {  // several slots share the earliest time: smallest key
+    if (__popc(b) > 1) {  // several entries share the earliest time: smallest key
       const uint32_t khi = at ? static_cast<uint32_t>(kb >> 32) : 0xffffffffu;
       const uint32_t mkhi = __reduce_min_sync(0xffffffffu, khi);
       const uint32_t klo = (at && khi == mkhi) ? static_cast<uint32_t>(kb) : 0xffffffffu;
@@ -1134,21 +1160,26 @@ class EngineT {
     const int src = __ffs(b) - 1;
     *bt_out = bitsd((static_cast<uint64_t>(mhi) << 32) | mlo);
     *bk_out = __shfl_sync(0xffffffffu, static_cast<unsigned long long>(kb), src);
+    *id_out = __shfl_sync(0xffffffffu, id, src);
 #else
     double bt = kInf;
     uint64_t bk = ~0ull;
-    int ties = 0;
-    for (int j = 0; j < nslots; ++j) {
-      if (s_->st_[j] == bt) ++ties;
-      if (before(s_->st_[j], s_->sk_[j], bt, bk)) {
-        if (s_->st_[j] < bt) ties = 1;
-        bt = s_->st_[j];
-        bk = s_->sk_[j];
+    int ties = 0, id = -1;
+    auto take = [&](double t, uint64_t k, int j) {
+      if (t == bt) ++ties;
+      if (before(t, k, bt, bk)) {
+        if (t < bt) ties = 1;
+        bt = t;
+        bk = k;
+        id = j;
       }
-    }
+    };
+    for (int j = 0; j < nslots; ++j) take(s_->st_[j], s_->sk_[j], j);
+    for (int j = 0; j < hn; ++j) take(SHEAP()[j].t, SHEAP()[j].key, kMaxSlots + j);
     *bt_out = bt;
     *bk_out = bk;
     *tie_out = ties > 1 && bt != kInf;
+    *id_out = id;
 #endif
   }
 
@@ -1192,6 +1223,18 @@ class EngineT {
     e.key = mk_key(kind, s_->seq_++, 0);
     e.a = a;
     e.b = b;
+    if (s_->hsmall_) {
+      const int32_t n = s_->hn_;
+      const int32_t cap = s_->C.hs < kSmallHeap ? s_->C.hs : kSmallHeap;
+      if (n < cap) {
+        warp_sync();
+        SHEAP()[n] = e;  // warp-uniform store
+        s_->hn_ = n + 1;
+        return;
+      }
+      heapify(SHEAP(), n);  // the set outgrew the lane scan: order it as a binary heap
+      s_->hsmall_ = 0;
+    }
     if (!s_->heap_spilled_ && s_->hn_ >= s_->C.hs) {
       HEv* gh = GLP(s_->G.heap);
       const HEv* sh = SHEAP();
@@ -1231,7 +1274,39 @@ class EngineT {
     const int32_t n = --s_->hn_;
     const HEv top = s_->heap_spilled_ ? heap_sift_down(GLP(s_->G.heap), n) : heap_sift_down(SHEAP(), n);
     if (n == 0) s_->heap_spilled_ = false;
+    if (!s_->heap_spilled_ && n <= kSmallHeap / 2) s_->hsmall_ = 1;  // a heap is also a valid unordered set
     return top;
+  }
+  // Removes entry j of the small unordered set (the last entry fills the hole).
+  PDG_HD HEv heap_take(int32_t j) {
+    HEv* h = SHEAP();
+    const int32_t n = s_->hn_ - 1;
+    const HEv e = h[j];
+    const HEv last = h[n];
+    warp_sync();
+    if (j != n && lane_id() == 0) h[j] = last;
+    s_->hn_ = n;
+    warp_sync();
+    return e;
+  }
+  PDG_HD static void heapify(HEv* h, int32_t n) {
+    for (int32_t r = n / 2 - 1; r >= 0; --r) {
+      const HEv x = h[r];
+      int32_t i = r;
+      for (;;) {
+        int32_t c = 2 * i + 1;
+        if (c >= n) break;
+        if (c + 1 < n && before(h[c + 1].t, h[c + 1].key, h[c].t, h[c].key)) ++c;
+        if (!before(h[c].t, h[c].key, x.t, x.key)) break;
+        const HEv hc = h[c];
+        warp_sync();
+        h[i] = hc;  // warp-uniform store
+        i = c;
+      }
+      warp_sync();
+      h[i] = x;  // warp-uniform store
+      warp_sync();
+    }
   }
   // Removes h[0] from a heap that now holds n entries (h[n] is the last).
   PDG_HD static HEv heap_sift_down(HEv* h, int32_t n) {
