@@ -275,8 +275,8 @@ struct Seg {
   double gap;    // every step's ITL gap (end - previous end)
   int32_t first; // first step index
   int32_t n;     // steps
-  uint32_t cnt;  // ITL samples per step (cohort members past their first token)
-  int32_t reserved;
+  uint32_t cnt;  // ITL samples per step after the first (cohort members past their first token)
+  uint32_t cnt_first;  // ITL samples of step `first` (differs from cnt when a run starts with joiners)
 };
 
 struct DecodeW {  // shared memory
@@ -1012,7 +1012,7 @@ class EngineT {
         w.sg.first = 0;
         w.sg.n = 0;
         w.sg.cnt = 0;
-        w.sg.reserved = 0;
+        w.sg.cnt_first = 0;
         w.seg_end = w.seg_keep = w.seg_head = w.seg_off = 0;
         w.kv_used = 0;
         w.kv_cap = static_cast<int64_t>(PDG_PROF.degrees[s_->PL.ddeg[d]]) * PDG_PROF.gpu_memory_capacity;
@@ -1803,9 +1803,17 @@ class EngineT {
   }
   PDG_HD void seg_append_(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
     DecodeW& w = DW(d);
-    if (w.sg.n > 0 && gap == w.sg.gap && cnt == w.sg.cnt && first == w.sg.first + w.sg.n) {
-      w.sg.n = w.sg.n + n;  // extends the open segment (t0 continues the progression)
-      return;
+    if (w.sg.n > 0 && gap == w.sg.gap && first == w.sg.first + w.sg.n) {
+      if (cnt == w.sg.cnt) {
+        w.sg.n = w.sg.n + n;  // extends the open segment (t0 continues the progression)
+        return;
+      }
+      if (w.sg.n == 1) {  // a run's first step (joiners emit no sample yet) heads the same segment
+        w.sg.cnt_first = w.sg.cnt;
+        w.sg.cnt = cnt;
+        w.sg.n = 1 + n;
+        return;
+      }
     }
     if (w.sg.n > 0) {
       // close the open segment into the ring
@@ -1821,7 +1829,7 @@ class EngineT {
       const Seg c = w.sg;
       seg_ring(d)[static_cast<uint32_t>(end) & static_cast<uint32_t>(s_->C.segcap - 1)] = c;
       w.seg_end = end + 1;
-      const int64_t k = static_cast<int64_t>(c.cnt) * c.n;
+      const int64_t k = seg_samples(c, 0, c.n);
       w.sg.plo = add_rd(c.plo, mul_rd(static_cast<double>(k), c.gap));
       w.sg.phi = add_ru(c.phi, mul_ru(static_cast<double>(k), c.gap));
       w.sg.pterms = c.pterms + k;
@@ -1831,6 +1839,14 @@ class EngineT {
     w.sg.first = first;
     w.sg.n = n;
     w.sg.cnt = cnt;
+    w.sg.cnt_first = cnt;
+  }
+  // ITL samples of steps [first + a, first + b) of segment g.
+  PDG_HD static int64_t seg_samples(const Seg& g, int32_t a, int32_t b) {
+    if (b > g.n) b = g.n;
+    if (b <= a) return 0;
+    return a == 0 ? static_cast<int64_t>(g.cnt_first) + static_cast<int64_t>(g.cnt) * (b - 1)
+                  : static_cast<int64_t>(g.cnt) * (b - a);
   }
 
   // Frees ring slots no longer needed: behind the ITL window head and before
@@ -1901,11 +1917,11 @@ class EngineT {
     // open segment (tail) and before the first in-window step (head). The
     // reference's fold differs from S by <= gamma_{n-1} S.
     const Seg& o = w.sg;
-    const int64_t ko = static_cast<int64_t>(o.cnt) * o.n;
+    const int64_t ko = seg_samples(o, 0, o.n);
     const double tlo = add_rd(o.plo, mul_rd(static_cast<double>(ko), o.gap));
     const double thi = add_ru(o.phi, mul_ru(static_cast<double>(ko), o.gap));
     const Seg h = seg_at(d, w.seg_head);
-    const int64_t kh = static_cast<int64_t>(h.cnt) * (w.seg_off < h.n ? w.seg_off : h.n);
+    const int64_t kh = seg_samples(h, 0, w.seg_off);
     const double hlo = add_rd(h.plo, mul_rd(static_cast<double>(kh), h.gap));
     const double hhi = add_ru(h.phi, mul_ru(static_cast<double>(kh), h.gap));
     const int64_t terms = o.pterms + ko - (h.pterms + kh);
@@ -1921,7 +1937,7 @@ class EngineT {
       const Seg g = seg_at(d, i);
       const int32_t skip = i == w.seg_head ? w.seg_off : 0;
       if (g.n > skip) {
-        sum = fold_repeat(sum, g.gap, static_cast<uint64_t>(g.cnt) * static_cast<uint64_t>(g.n - skip));
+        sum = fold_repeat(sum, g.gap, static_cast<uint64_t>(seg_samples(g, skip, g.n)));
       }
     }
     return ddiv(sum, static_cast<double>(terms)) <= thr;
