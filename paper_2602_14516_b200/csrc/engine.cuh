@@ -81,7 +81,8 @@ inline T* GLP(T* p) {
 #endif
 
 constexpr int kMaxSlots = 64;
-constexpr int32_t kSmallHeap = 64;  // session events kept unordered (lanes scan them) up to this count
+constexpr int32_t kSmallHeap = 64;
+constexpr int32_t kShortBulk = 16;  // silent stretches up to this long are stepped with plain fp64 adds  // session events kept unordered (lanes scan them) up to this count
 constexpr int kSlotsPerLane = kMaxSlots / PDG_NL;
 constexpr double kInf = __builtin_huge_val();
 
@@ -2525,13 +2526,29 @@ class EngineT {
       if (room > 0 && next < t) {
         const double g = dsub(next, e);
         const int64_t ts0_ = pb();
-        const int64_t m = stable_run(e, dur, g, t, room);
+        int64_t m = 0;
+        double last_end = e, nxt = next;
+        if (room <= kShortBulk) {
+          // Short stretch: step explicitly while each end adds exactly g (two
+          // fp64 ops a step, cheaper than the binade arithmetic).
+          while (m < room && nxt < t && dsub(nxt, last_end) == g) {
+            ++m;
+            last_end = nxt;
+            nxt = dadd(nxt, dur);
+          }
+        } else {
+          m = stable_run(e, dur, g, t, room);
+          if (m > 0) {
+            last_end = dadd(next, dmul(static_cast<double>(m - 1), g));
+            nxt = dadd(last_end, dur);
+          }
+        }
         pe(25, ts0_);
         if (m > 0) {
           seg_append(d, k + 1, static_cast<int32_t>(m), next, g, static_cast<uint32_t>(cohort));
-          end = dadd(next, dmul(static_cast<double>(m - 1), g));
+          end = last_end;
           done += static_cast<int32_t>(m);
-          next = dadd(end, dur);
+          next = nxt;
           if (!(next > end)) {
             s_->abort_ = 1;
             return;
