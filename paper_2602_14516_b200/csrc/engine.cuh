@@ -1400,14 +1400,33 @@ class EngineT {
       const int32_t room = run_b - (k + 1);
       if (room > 0 && next < t) {
         const double g = dsub(next, e);
-        const int64_t m = stable_run(e, dur, g, t, room);
-        if (m > 0) {
-          end = dadd(next, dmul(static_cast<double>(m - 1), g));
-          done += static_cast<int32_t>(m);
-          next = dadd(end, dur);
-          if (!(next > end)) {
-            *abort = true;
-            break;
+        if (room <= kShortBulk) {  // same stepping as catch_up_worker_
+          int32_t m = 0;
+          double last_end = e, nxt = next;
+          while (m < room && nxt < t && dsub(nxt, last_end) == g) {
+            ++m;
+            last_end = nxt;
+            nxt = dadd(nxt, dur);
+          }
+          if (m > 0) {
+            end = last_end;
+            done += m;
+            next = nxt;
+            if (!(next > end)) {
+              *abort = true;
+              break;
+            }
+          }
+        } else {
+          const int64_t m = stable_run(e, dur, g, t, room);
+          if (m > 0) {
+            end = dadd(next, dmul(static_cast<double>(m - 1), g));
+            done += static_cast<int32_t>(m);
+            next = dadd(end, dur);
+            if (!(next > end)) {
+              *abort = true;
+              break;
+            }
           }
         }
       }

@@ -24,6 +24,10 @@ namespace pdg {
 // as a sequential loop (round-to-nearest-even, no FMA). Requires s >= 0,
 // g >= 0 (the engine only folds non-negative latencies).
 PDG_HD double fold_repeat(double s, double g, uint64_t count) {
+  if (count <= 16) {  // short folds: plain adds beat the binade arithmetic
+    for (uint64_t k = 0; k < count; ++k) s = dadd(s, g);
+    return s;
+  }
   const uint64_t kMant = (1ull << 52) - 1;
   const uint64_t kTop = (1ull << 53) - 2;  // stay strictly inside the binade
   while (count > 0) {
