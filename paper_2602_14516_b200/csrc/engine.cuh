@@ -1132,16 +1132,24 @@ class EngineT {
         id = lane + 32;
       }
     }
-    if (hn > 0) {
-      const HEv* h = SHEAP();
-      for (int j = lane; j < hn; j += 32) {
-        const uint64_t t2 = dbits(h[j].t);
-        const uint64_t k2 = h[j].key;
-        if (t2 < tb || (t2 == tb && k2 < kb)) {
-          tb = t2;
-          kb = k2;
-          id = kMaxSlots + j;
-        }
+    static_assert(kSmallHeap <= 64, "two small-set entries per lane");
+    const HEv* h = SHEAP();
+    if (lane < hn) {
+      const uint64_t t2 = dbits(h[lane].t);
+      const uint64_t k2 = h[lane].key;
+      if (t2 < tb || (t2 == tb && k2 < kb)) {
+        tb = t2;
+        kb = k2;
+        id = kMaxSlots + lane;
+      }
+    }
+    if (lane + 32 < hn) {
+      const uint64_t t2 = dbits(h[lane + 32].t);
+      const uint64_t k2 = h[lane + 32].key;
+      if (t2 < tb || (t2 == tb && k2 < kb)) {
+        tb = t2;
+        kb = k2;
+        id = kMaxSlots + lane + 32;
       }
     }
     const uint32_t hi = static_cast<uint32_t>(tb >> 32);
