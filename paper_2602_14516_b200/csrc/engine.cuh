@@ -249,8 +249,15 @@ struct TaskQueue {
 };
 
 // Lazily trimmed window ring (global storage) + running prefix at the tail.
+// Bracket [lo, hi] of an exact running sum (directed rounding).
+struct Brk {
+  double lo;
+  double hi;
+};
+
+// Lazily trimmed window ring (global storage) + running prefix at the tail.
 struct WinState {
-  Pfx tail;
+  Brk tail;  // prefix bracket after the newest sample
   uint32_t head, end;
   uint32_t reserved[2];
 };
@@ -350,7 +357,7 @@ struct GlobalSlot {
   double* dq_c;
   double* tw_t;
   double* tw_v;
-  Pfx* tw_p;
+  Brk* tw_p;  // prefix bracket before each TTFT sample
   Seg* seg;  // [dmax][segcap]
   uint64_t* fh;
   double* rep_ttft;    // report mode: [rep_r] TTFT values in push order (incremental negated)
@@ -419,7 +426,7 @@ PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
   t.dq_c = reinterpret_cast<double*>(take(8 * D * static_cast<size_t>(c.qcap)));
   t.tw_t = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
   t.tw_v = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.twcap)));
-  t.tw_p = reinterpret_cast<Pfx*>(take(sizeof(Pfx) * P * static_cast<size_t>(c.twcap)));
+  t.tw_p = reinterpret_cast<Brk*>(take(sizeof(Brk) * P * static_cast<size_t>(c.twcap)));
   t.seg = reinterpret_cast<Seg*>(take(sizeof(Seg) * D * static_cast<size_t>(c.segcap)));
   t.fh = reinterpret_cast<uint64_t*>(take(8 * D * static_cast<size_t>(c.fcap)));
   const bool rep = c.rep_gapcap > 0;
@@ -993,7 +1000,7 @@ class EngineT {
         PrefillW& w = PW(p);
         w.q.sum.clear();
         w.q.qh = w.q.qt = 0;
-        w.tw.tail.clear();
+        w.tw.tail.lo = w.tw.tail.hi = 0.0;
         w.tw.head = w.tw.end = 0;
         w.deg = s_->PL.pdeg[p];
         w.cur = w.stg = -1;
@@ -1774,9 +1781,10 @@ class EngineT {
     const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
     if (!window_room(w.tw, GLP(s_->G.tw_t) + base, static_cast<uint32_t>(s_->C.twcap), s_->now_)) return;
     const uint32_t k = w.tw.end & mask;
-    const Pfx cur = w.tw.tail;
-    Pfx next = cur;
-    next.add(v, 1);
+    const Brk cur = w.tw.tail;
+    Brk next;
+    next.lo = add_rd(cur.lo, v);
+    next.hi = add_ru(cur.hi, v);
     {  // warp-uniform stores (every lane writes the same values)
       GLP(s_->G.tw_t)[base + k] = s_->now_;
       GLP(s_->G.tw_v)[base + k] = v;
@@ -1800,8 +1808,13 @@ class EngineT {
     window_trim(w.tw, GLP(s_->G.tw_t) + base, mask, s_->now_);
     const uint32_t head = w.tw.head, end = w.tw.end;
     if (head == end) return 0.0 <= thr;  // an empty window reads 0
-    const Pfx hp = GLP(s_->G.tw_p)[base + (head & mask)];
-    const int dec = window_mean_le(w.tw.tail, hp, thr);
+    // Window sum bracket = tail prefix - head prefix (TTFT values are >= 0);
+    // the reference's fold is within gamma_{n-1} of the exact sum.
+    const Brk hp = GLP(s_->G.tw_p)[base + (head & mask)];
+    double lo = sub_rd(w.tw.tail.lo, hp.hi);
+    const double hi = sub_ru(w.tw.tail.hi, hp.lo);
+    if (lo < 0.0) lo = 0.0;
+    const int dec = mean_le_bracket(lo, hi, static_cast<int64_t>(end - head), thr);
     if (dec >= 0) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
