@@ -15,7 +15,9 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpdsim_gpu.so")
+# PDSIM_LIB points at another in-tree build of the same library (A/B timing
+# in tools/ab.py); the default is the package's own libpdsim_gpu.so.
+LIB_PATH = os.environ.get("PDSIM_LIB") or os.path.join(HERE, "libpdsim_gpu.so")
 
 _lib = None
 ABI_VERSION = 2  # include/pdsim_gpu.h PDSIM_ABI_VERSION
