@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "pdsim/metrics.hpp"
@@ -44,5 +45,20 @@ struct SearchResult {
 SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<DeploymentPlan>& candidates,
                          const PerfProfile& profile, const SchedulerParams& params, std::uint64_t engine_seed,
                          const SearchOptions& options = {});
+
+// Batched `pdsim sweep` (pdsim.cpp:501-590): `plan` replayed on each trace
+// (the sweep generates one trace per arrival rate) under every scheduler
+// setting, all pairs in one GPU call. Returns build_report of each replay,
+// indexed [setting * traces.size() + trace]. Every setting is validated
+// first (ConfigError, like the reference's first failing combination).
+std::vector<Report> sweep(const std::vector<Trace>& traces, const DeploymentPlan& plan, const PerfProfile& profile,
+                          const std::vector<SchedulerParams>& settings, std::uint64_t seed,
+                          const SearchOptions& options = {});
+
+// The reference's sweep.csv text (pdsim.cpp:541-586): one row per (rate,
+// setting) in rate-major order, numbers in std::to_chars form. `reports` as
+// returned by sweep() for traces generated at `rates` (same order).
+std::string sweep_csv(const std::vector<double>& rates, const std::vector<SchedulerParams>& settings,
+                      const std::vector<Report>& reports);
 
 }  // namespace pdsim

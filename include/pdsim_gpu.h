@@ -318,6 +318,21 @@ int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in,
                           const pdsim_sched_params* params, uint64_t seed,
                           pdsim_search_output* out);
 
+/* Batched `pdsim sweep` (pdsim.cpp:501-590): one plan replayed on n_traces
+ * traces (the sweep's one trace per arrival rate) under n_settings scheduler
+ * settings (its alpha x beta x window grid, any order). Candidates are the
+ * settings: pair p = k * n_traces + r is setting k on trace r, and every
+ * per-pair / per-candidate output of pdsim_search_output is indexed that way
+ * (pair_report gives the sweep.csv row of each combination; best_candidate is
+ * the setting with the most slo_ok sessions over the traces). Every setting
+ * is validated against every trace before launch (ConfigError, as the
+ * reference's first failing combination would throw). The settings stay
+ * staged for pdsim_gpu_search_staged(). */
+int pdsim_gpu_sweep(pdsim_gpu_ctx* ctx, int32_t n_traces, const pdsim_trace* traces,
+                    const pdsim_plan* plan, int32_t n_settings,
+                    const pdsim_sched_params* settings, const pdsim_profile* profile,
+                    uint64_t seed, pdsim_search_output* out);
+
 /* Resident variant: pdsim_gpu_stage() copies traces + candidates into HBM
  * once; pdsim_gpu_search_staged() replays them with inputs already resident
  * (outputs still land in caller host buffers). */
@@ -470,6 +485,11 @@ int pdsim_solve(const pdsim_coefficients* coeffs, int32_t total_gpus, pdsim_plan
  * Returns the number written (<= k) or -1 on error (pdsim_last_error). */
 int64_t pdsim_top_k(const pdsim_coefficients* coeffs, int32_t total_gpus, int32_t k, pdsim_plan* plans,
                     double* objective_z, int32_t* gpus_used);
+
+/* std::to_chars(double) shortest round-trip text: the reference's CSV number
+ * format (metrics.cpp:32-36; fmt_double, pdsim.cpp:84-88). Writes the text
+ * NUL-terminated; returns its length, or -1 when `cap` is too small. */
+int32_t pdsim_format_double(double value, char* buf, int32_t cap);
 
 /* Device-free CPU argmax helper used by multi-rank callers after the NCCL
  * reduction: max count, ties -> smallest index, negative = invalid. */

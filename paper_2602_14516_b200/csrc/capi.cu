@@ -73,13 +73,14 @@ struct pdsim_gpu_ctx {
   int32_t n_traces = 0, n_candidates = 0;
   pdsim_profile profile{};
   pdsim_sched_params params{};
+  std::vector<pdg::DevParams> cand_params;  // sweep: scheduler settings per candidate (empty: `params`)
   std::vector<pdg::PackedTrace> packed;
   std::vector<pdg::DevPlan> plans;
   std::vector<int8_t> pair_invalid;  // [n_candidates * n_traces], host precheck
   pdg::Caps caps{};
   size_t slot_bytes = 0;   // global workspace per slot
   size_t smem_bytes = 0;   // dynamic shared memory per slot (one warp / block)
-  DevBuf d_trace_data, d_traces, d_plans, d_invalid;
+  DevBuf d_trace_data, d_traces, d_plans, d_invalid, d_cand_params;
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
@@ -150,18 +151,26 @@ int check_ctx(pdsim_gpu_ctx* ctx) {
   return PDSIM_OK;
 }
 
+// `cand_params` (sweep; may be null) gives candidate c its own scheduler
+// settings; `params` then only supplies defaults for unset fields (none).
 int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_profile* profile,
-               const pdsim_sched_params* params, int64_t* h2d_bytes) {
+               const pdsim_sched_params* params, int64_t* h2d_bytes, const pdsim_sched_params* cand_params = nullptr) {
   if (!in || !profile || !params) return set_err(ctx, PDSIM_ERR_CONFIG, "null argument");
   if (in->n_traces < 1 || in->n_candidates < 1 || !in->traces || !in->candidates) {
     return set_err(ctx, PDSIM_ERR_CONFIG, "search: need at least one trace and one candidate");
   }
   ctx->staged = false;
   pdg::HostError err;
-  // Reference validation order (sim_engine.cpp:115-122).
-  for (int r = 0; r < in->n_traces; ++r) {
-    if (!pdg::validate_params(*params, in->traces[r].ttft_thres, in->traces[r].itl_thres, &err)) {
-      return set_err(ctx, err.code, err.msg);
+  // Reference validation order (sim_engine.cpp:115-122): every setting
+  // against every trace, settings in order (the reference sweep throws at
+  // the first invalid combination, pdsim.cpp:547-559).
+  const int n_set = cand_params ? in->n_candidates : 1;
+  const pdsim_sched_params* sets = cand_params ? cand_params : params;
+  for (int k = 0; k < n_set; ++k) {
+    for (int r = 0; r < in->n_traces; ++r) {
+      if (!pdg::validate_params(sets[k], in->traces[r].ttft_thres, in->traces[r].itl_thres, &err)) {
+        return set_err(ctx, err.code, err.msg);
+      }
     }
   }
   ctx->packed.assign(static_cast<size_t>(in->n_traces), pdg::PackedTrace());
@@ -171,9 +180,18 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
     any_sessions |= ctx->packed[static_cast<size_t>(r)].S > 0;
   }
   if (!pdg::validate_profile(*profile, &err)) return set_err(ctx, err.code, err.msg);
-  if (params->reorder && params->window > 8 && any_sessions) {
-    // reorder_and_dequeue throws at the first dequeue (reorder.cpp:86-90).
-    return set_err(ctx, PDSIM_ERR_CONFIG, "reorder: window must be <= 8");
+  for (int k = 0; k < n_set; ++k) {
+    if (sets[k].reorder && sets[k].window > 8 && any_sessions) {
+      // reorder_and_dequeue throws at the first dequeue (reorder.cpp:86-90).
+      return set_err(ctx, PDSIM_ERR_CONFIG, "reorder: window must be <= 8");
+    }
+  }
+  // Window ring capacities follow the longest statistics window of any setting.
+  pdsim_sched_params cap_params = sets[0];
+  for (int k = 1; k < n_set; ++k) cap_params.stat_window = std::max(cap_params.stat_window, sets[k].stat_window);
+  ctx->cand_params.clear();
+  if (cand_params) {
+    for (int k = 0; k < n_set; ++k) ctx->cand_params.push_back(pdg::to_dev_params(sets[k]));
   }
   ctx->plans.assign(static_cast<size_t>(in->n_candidates), pdg::DevPlan());
   int pmax = 0, dmax = 1;
@@ -203,7 +221,7 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   const int lay = (dmax <= 8 && pmax <= 8) ? 0 : (dmax <= 16 && pmax <= 16) ? 1 : 2;
   static const int kLayD[3] = {8, 16, 64}, kLayP[3] = {8, 16, 32};
   ctx->layout = lay;
-  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, *params, smem_budget, kLayD[lay], kLayP[lay]);
+  ctx->caps = pdg::compute_caps(tp, pmax, dmax, *profile, cap_params, smem_budget, kLayD[lay], kLayP[lay]);
   ctx->slot_bytes = pdg::global_slot_bytes(ctx->caps, nullptr, nullptr);
   ctx->smem_bytes = pdg::smem_slot_bytes(ctx->caps, nullptr, nullptr);
   ctx->profile = *profile;
@@ -253,12 +271,17 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   CU(ctx, ctx->d_invalid.reserve(ctx->pair_invalid.size()));
   CU(ctx, cudaMemcpyAsync(ctx->d_invalid.p, ctx->pair_invalid.data(), ctx->pair_invalid.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->cand_params.empty()) {
+    CU(ctx, ctx->d_cand_params.reserve(sizeof(pdg::DevParams) * ctx->cand_params.size()));
+    CU(ctx, cudaMemcpyAsync(ctx->d_cand_params.p, ctx->cand_params.data(),
+                            sizeof(pdg::DevParams) * ctx->cand_params.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
   CU(ctx, pdg::replay_set_profile(profile, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (h2d_bytes) {
     *h2d_bytes = static_cast<int64_t>(off + sizeof(pdg::DevTrace) * dt.size() +
                                       sizeof(pdg::DevPlan) * ctx->plans.size() + ctx->pair_invalid.size() +
-                                      sizeof(pdsim_profile));
+                                      sizeof(pdg::DevParams) * ctx->cand_params.size() + sizeof(pdsim_profile));
   }
   ctx->staged = true;
   return PDSIM_OK;
@@ -318,6 +341,7 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.pair_begin = b;
   a.pair_end = e;
   a.params = pdg::to_dev_params(ctx->params);
+  a.cand_params = ctx->cand_params.empty() ? nullptr : ctx->d_cand_params.as<pdg::DevParams>();
   a.caps = caps;
   a.ws = ctx->d_ws.as<char>();
   a.slot_bytes = slot_bytes;
@@ -609,6 +633,31 @@ int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, cons
   if (int rc = stage_impl(ctx, in, profile, params, &h2d)) return rc;
   pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const int rc = search_impl(ctx, in->pair_begin, in->pair_end, seed, out, rec, nullptr);
+  if (out) out->h2d_bytes = h2d;
+  return rc;
+}
+
+int pdsim_gpu_sweep(pdsim_gpu_ctx* ctx, int32_t n_traces, const pdsim_trace* traces, const pdsim_plan* plan,
+                    int32_t n_settings, const pdsim_sched_params* settings, const pdsim_profile* profile,
+                    uint64_t seed, pdsim_search_output* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!plan || !settings || n_settings < 1) return set_err(ctx, PDSIM_ERR_CONFIG, "sweep: need a plan and at least one setting");
+  // Candidates are the settings, all on the one plan: pair k * n_traces + r.
+  std::vector<pdsim_plan> plans(static_cast<size_t>(n_settings), *plan);
+  pdsim_search_input in;
+  memset(&in, 0, sizeof(in));
+  in.n_traces = n_traces;
+  in.n_candidates = n_settings;
+  in.traces = traces;
+  in.candidates = plans.data();
+  in.pair_begin = 0;
+  in.pair_end = -1;
+  int64_t h2d = 0;
+  if (int rc = stage_impl(ctx, &in, profile, &settings[0], &h2d, settings)) return rc;
+  pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  const int rc = search_impl(ctx, 0, -1, seed, out, rec, nullptr);
+  // The settings stay staged: pdsim_gpu_search_staged() re-runs the sweep
+  // with inputs resident; the next stage()/run() replaces them.
   if (out) out->h2d_bytes = h2d;
   return rc;
 }

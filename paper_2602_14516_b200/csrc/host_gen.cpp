@@ -7,6 +7,7 @@
 // the reference built in oracle/_ref. Compiled with -ffp-contract=off: the
 // reference's `lo + (hi - lo) * u` must round twice.
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -404,6 +405,16 @@ int64_t pdsim_enumerate_plans(const int32_t* degrees, int32_t n_degrees, int32_t
     });
   });
   return count;
+}
+
+int32_t pdsim_format_double(double value, char* buf, int32_t cap) {
+  char tmp[64];
+  const auto res = std::to_chars(tmp, tmp + sizeof(tmp), value);
+  const int32_t n = static_cast<int32_t>(res.ptr - tmp);
+  if (!buf || cap < n + 1) return -1;
+  memcpy(buf, tmp, static_cast<size_t>(n));
+  buf[n] = '\0';
+  return n;
 }
 
 int32_t pdsim_argmax_candidates(const int64_t* v, int32_t n) {

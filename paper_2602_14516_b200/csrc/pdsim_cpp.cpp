@@ -781,6 +781,84 @@ SimResult run(const Trace& trace, const DeploymentPlan& plan, const PerfProfile&
   return r;
 }
 
+Report report_from_pod(const pdsim_report& p, const std::string& name) {
+  Report x;
+  x.trace_name = name;
+  x.empty = p.empty != 0;
+  x.sessions_total = p.sessions_total;
+  x.sessions_completed = p.sessions_completed;
+  x.slo_attainment = p.slo_attainment;
+  x.ttft_attainment = p.ttft_attainment;
+  x.itl_attainment = p.itl_attainment;
+  x.ttft_initial = {p.ttft_initial.mean, p.ttft_initial.p95, p.ttft_initial.count};
+  x.ttft_incremental = {p.ttft_incremental.mean, p.ttft_incremental.p95, p.ttft_incremental.count};
+  x.itl = {p.itl.mean, p.itl.p95, p.itl.count};
+  x.e2e_mean = p.e2e_mean;
+  x.local_fraction = p.local_fraction;
+  return x;
+}
+
+// ---- sweep(): pdsim sweep as one batched GPU call ----
+std::vector<Report> sweep(const std::vector<Trace>& traces, const DeploymentPlan& plan, const PerfProfile& profile,
+                          const std::vector<SchedulerParams>& settings, std::uint64_t seed,
+                          const SearchOptions& options) {
+  if (traces.empty() || settings.empty()) throw ConfigError("sweep: need at least one trace and one setting");
+  for (const SchedulerParams& s : settings) s.validate();
+  plan.validate("plan");
+  pdsim_profile prof;
+  profile_to_pod(profile, &prof);
+  std::vector<std::unique_ptr<TraceArrays>> arrays;
+  std::vector<pdsim_trace> views;
+  for (const Trace& t : traces) {
+    arrays.emplace_back(new TraceArrays(t));
+    views.push_back(arrays.back()->view);
+  }
+  std::vector<pdsim_sched_params> sets;
+  for (const SchedulerParams& s : settings) sets.push_back(params_to_pod(s));
+  const pdsim_plan pp = plan_to_pod(plan);
+  const size_t n = traces.size() * settings.size();
+  std::vector<pdsim_report> reps(n);
+  std::vector<int64_t> cand(settings.size());
+  pdsim_search_output out;
+  std::memset(&out, 0, sizeof(out));
+  out.pair_report = reps.data();
+  out.candidate_slo_ok = cand.data();
+  pdsim_gpu_ctx* ctx = context(options.device >= 0 ? options.device : default_device());
+  check_ctx(pdsim_gpu_sweep(ctx, static_cast<int32_t>(views.size()), views.data(), &pp,
+                            static_cast<int32_t>(sets.size()), sets.data(), &prof, seed, &out),
+            ctx);
+  std::vector<Report> r;
+  r.reserve(n);
+  for (size_t k = 0; k < n; ++k) r.push_back(report_from_pod(reps[k], traces[k % traces.size()].name));
+  return r;
+}
+
+std::string sweep_csv(const std::vector<double>& rates, const std::vector<SchedulerParams>& settings,
+                      const std::vector<Report>& reports) {
+  if (reports.size() != rates.size() * settings.size()) throw ConfigError("sweep_csv: reports do not match the grid");
+  auto f = [](double v) {
+    char buf[64];
+    const int32_t n = pdsim_format_double(v, buf, sizeof(buf));
+    return std::string(buf, static_cast<size_t>(std::max(n, 0)));
+  };
+  std::string csv =
+      "rate,alpha,beta,window,slo_attainment,ttft_attainment,"
+      "itl_attainment,ttft_initial_mean,ttft_initial_p95,ttft_incr_mean,"
+      "ttft_incr_p95,itl_mean,itl_p95,e2e_mean,local_fraction\n";
+  for (size_t r = 0; r < rates.size(); ++r) {
+    for (size_t k = 0; k < settings.size(); ++k) {
+      const Report& rep = reports[k * rates.size() + r];
+      const SchedulerParams& s = settings[k];
+      csv += f(rates[r]) + "," + f(s.alpha) + "," + f(s.beta) + "," + std::to_string(s.window) + "," +
+             f(rep.slo_attainment) + "," + f(rep.ttft_attainment) + "," + f(rep.itl_attainment) + "," +
+             f(rep.ttft_initial.mean) + "," + f(rep.ttft_initial.p95) + "," + f(rep.ttft_incremental.mean) + "," +
+             f(rep.ttft_incremental.p95) + "," + f(rep.itl.mean) + "," + f(rep.itl.p95) + "," + f(rep.e2e_mean) +
+             "," + f(rep.local_fraction) + "\n";
+    }
+  }
+  return csv;
+}
+
 // ---- plan_search(): the batched GPU search ----
 SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<DeploymentPlan>& candidates,
                          const PerfProfile& profile, const SchedulerParams& params, std::uint64_t engine_seed,
@@ -828,21 +906,9 @@ SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<D
   check_ctx(pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out), ctx);
   if (options.report) {
     for (int64_t k = 0; k < n; ++k) {
-      const pdsim_report& p = reps[static_cast<size_t>(k)];
-      Report x;
-      x.trace_name = replicas[static_cast<size_t>((in.pair_begin + k) % static_cast<int64_t>(replicas.size()))].name;
-      x.empty = p.empty != 0;
-      x.sessions_total = p.sessions_total;
-      x.sessions_completed = p.sessions_completed;
-      x.slo_attainment = p.slo_attainment;
-      x.ttft_attainment = p.ttft_attainment;
-      x.itl_attainment = p.itl_attainment;
-      x.ttft_initial = {p.ttft_initial.mean, p.ttft_initial.p95, p.ttft_initial.count};
-      x.ttft_incremental = {p.ttft_incremental.mean, p.ttft_incremental.p95, p.ttft_incremental.count};
-      x.itl = {p.itl.mean, p.itl.p95, p.itl.count};
-      x.e2e_mean = p.e2e_mean;
-      x.local_fraction = p.local_fraction;
-      r.reports.push_back(x);
+      r.reports.push_back(report_from_pod(
+          reps[static_cast<size_t>(k)],
+          replicas[static_cast<size_t>((in.pair_begin + k) % static_cast<int64_t>(replicas.size()))].name));
     }
   }
   r.best_candidate = out.best_candidate;

@@ -21,6 +21,7 @@ struct KernelArgs {
   int64_t pair_begin;
   int64_t pair_end;
   DevParams params;
+  const DevParams* cand_params;  // optional per-candidate settings (sweep); null: `params` for all
   Caps caps;
   char* ws;
   size_t slot_bytes;
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const DevTrace tr = a.traces[r];
       const DevPlan pl = a.plans[c];
       const long long t0 = clock64();
-      EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, a.params, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
+      const DevParams prm = a.cand_params ? a.cand_params[c] : a.params;
+      EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, prm, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
       eng.run(&res);
       res.cycles = clock64() - t0;
       if (kRec && a.reports) {

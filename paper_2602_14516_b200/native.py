@@ -59,6 +59,10 @@ def lib():
         L.pdsim_gpu_plan_search.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams),
                                             C.c_uint64, P(abi.SearchOutput)]
         L.pdsim_gpu_stage.argtypes = [C.c_void_p, P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams)]
+        L.pdsim_gpu_sweep.argtypes = [C.c_void_p, C.c_int32, P(abi.Trace), P(abi.Plan), C.c_int32,
+                                      P(abi.SchedParams), P(abi.Profile), C.c_uint64, P(abi.SearchOutput)]
+        L.pdsim_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int32]
+        L.pdsim_format_double.restype = C.c_int32
         L.pdsim_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.pdsim_gpu_profile_counters.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.pdsim_gpu_search_staged.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, P(abi.SearchOutput)]
@@ -345,6 +349,19 @@ class Context:
                                                 C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
 
+    def sweep(self, traces, plan, profile, settings, seed, report=True):
+        """Batched `pdsim sweep` (include/pdsim_gpu.h pdsim_gpu_sweep): `plan`
+        on every trace under every scheduler setting; pair k * len(traces) + r
+        is setting k on trace r. The settings stay staged (search_staged)."""
+        tv = (abi.Trace * len(traces))(*traces)
+        sv = (abi.SchedParams * len(settings))(*settings)
+        n = len(traces) * len(settings)
+        out, att, ctr, st, cand = self._outputs(n, len(settings), report)
+        self._check(lib().pdsim_gpu_sweep(self._h, len(traces), tv, C.byref(plan), len(settings), sv,
+                                          C.byref(profile), seed, C.byref(out)))
+        self._staged = (len(traces), len(settings))
+        return SearchResult(out, att, ctr, st, cand, n)
+
     def set_profiling(self, enable):
         self._check(lib().pdsim_gpu_set_profiling(self._h, 1 if enable else 0))
 
@@ -369,6 +386,16 @@ class Context:
         out, att, ctr, st, cand = self._outputs(n, nc, report)
         self._check(lib().pdsim_gpu_search_staged(self._h, pair_begin, pair_end, seed, C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
+
+
+def format_double(x):
+    """std::to_chars(double) shortest round-trip text (the reference's CSV
+    number format), from the library."""
+    buf = C.create_string_buffer(64)
+    n = lib().pdsim_format_double(float(x), buf, 64)
+    if n < 0:
+        raise PdsimError(abi.ERR_INTERNAL, "format_double: buffer too small")
+    return buf.value.decode()
 
 
 def argmax_candidates(candidate_slo_ok):

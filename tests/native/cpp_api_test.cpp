@@ -168,6 +168,40 @@ int main() {
     }
   }
 
+  // sweep() (pdsim sweep, pdsim.cpp:501-590): one launch over traces x
+  // settings; each report equals build_report of run() under that setting.
+  {
+    SchedulerParams a, b;
+    a.alpha = 0.5;
+    b.beta = 0.3;
+    b.window = 1;
+    const std::vector<SchedulerParams> sets = {a, b};
+    const Trace gen2 = gen_trace(preset_stats("toolbench"), 16.0, 120, 5);
+    const std::vector<Trace> trs = {gen, gen2};
+    const std::vector<Report> reps = sweep(trs, simple_plan(1, 1), p, sets, 3);
+    CHECK(reps.size() == 4);
+    for (size_t k = 0; k < sets.size(); ++k) {
+      for (size_t r = 0; r < trs.size() && reps.size() == 4; ++r) {
+        const Report want = build_report(run(trs[r], simple_plan(1, 1), p, sets[k], 3));
+        const Report& got = reps[k * trs.size() + r];
+        CHECK(got.slo_attainment == want.slo_attainment && got.itl.p95 == want.itl.p95 &&
+              got.ttft_initial.p95 == want.ttft_initial.p95 && got.e2e_mean == want.e2e_mean);
+      }
+    }
+    const std::string csv = sweep_csv({8.0, 16.0}, sets, reps);
+    CHECK(csv.rfind("rate,alpha,beta,window,", 0) == 0);
+    CHECK(csv.find("\n8,0.5,0.85,3,") != std::string::npos && csv.find("\n16,0.9,0.3,1,") != std::string::npos);
+    bool threw = false;
+    try {
+      SchedulerParams bad;
+      bad.alpha = -1.0;
+      sweep(trs, simple_plan(1, 1), p, {bad}, 3);
+    } catch (const ConfigError&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+
   // Surrogate planner (planner.hpp:55-113): the coefficient pipeline and the
   // solver behave like the reference's planner_test properties.
   {

@@ -131,8 +131,8 @@ def to_chars(x):
     ds = "".join(str(d) for d in digits)
     e10 = exp + n - 1
     sci = ds[0] + ("." + ds[1:] if n > 1 else "") + "e" + ("-" if e10 < 0 else "+") + f"{abs(e10):02d}"
-    if exp >= 0:
-        fixed = ds + "0" * exp
+    if exp >= 0:  # integral: libstdc++ prints the exact integer in fixed form
+        fixed = str(int(abs(x)))
     elif -exp < n:
         fixed = ds[: n + exp] + "." + ds[n + exp:]
     else:

@@ -1,7 +1,7 @@
 """A/B kernel timing of two builds of libpdsim_gpu.so on the same box:
 alternates runs of the staged C2 search in fresh processes.
 
-usage: python tools/ab.py LIB_A LIB_B [rounds]
+usage: python tools/ab.py LIB_A LIB_B [rounds] [config] [pair_begin] [pair_end]
 """
 import os
 import subprocess
@@ -10,25 +10,26 @@ import sys
 CHILD = r'''
 import sys
 from paper_2602_14516_b200 import native, workloads
-wl = workloads.c2()
+cfg, b, e = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+wl = workloads.CONFIGS[cfg]()
 with native.Context(0) as ctx:
     ctx.stage(wl.traces, wl.plans, wl.profile, wl.params)
-    ctx.search_staged(wl.seed)
-    ms = [ctx.search_staged(wl.seed).kernel_ms for _ in range(3)]
+    ctx.search_staged(wl.seed, b, e)
+    ms = [ctx.search_staged(wl.seed, b, e).kernel_ms for _ in range(3)]
 print(min(ms))
 '''
 
 
-def main(a, b, rounds=3):
+def main(a, b, rounds=3, cfg="C2", pb="0", pe="-1"):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {a: [], b: []}
     for _ in range(int(rounds)):
         for lib in (a, b):
             env = dict(os.environ, PDSIM_LIB=os.path.abspath(lib))
-            out = subprocess.run([sys.executable, "-c", CHILD], cwd=root, env=env, capture_output=True, text=True)
+            out = subprocess.run([sys.executable, "-c", CHILD, cfg, pb, pe], cwd=root, env=env, capture_output=True, text=True)
             res[lib].append(float(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else None)
     for lib, v in res.items():
-        print(lib, v, "min", min(x for x in v if x is not None))
+        print(cfg, lib, v, "min", min(x for x in v if x is not None))
 
 
 if __name__ == "__main__":
