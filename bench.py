@@ -204,7 +204,7 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
-    from paper_2602_14516_b200 import native, workloads
+    from paper_2602_14516_b200 import abi, native, workloads
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -289,6 +289,28 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = rounds_all / (float(te.item()) / 1e3)
 
+    # Search mode ARGMAX (exact pruning, include/pdsim_gpu.h): same plan and
+    # count, fewer replays; reported beside the full-replay headline, which
+    # alone defines `value`.
+    arg = None
+    if world == 1:
+        ctx.set_search_mode(abi.SEARCH_ARGMAX)
+        am = []
+        for _ in range(max(2, min(args.steps, 3))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            res_a = ctx.search_staged(wl.seed, b, e)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            am.append(ev0.elapsed_time(ev1))
+        ctx.set_search_mode(abi.SEARCH_FULL)
+        arg = {"planner_wall_ms": statistics.median(am), "best_candidate": res_a.best_candidate,
+               "best_slo_ok": res_a.best_slo_ok, "same_plan_as_full": res_a.best_candidate == best and
+               res_a.best_slo_ok == best_cnt,
+               "pruned_candidates": sum(1 for c in range(C) if res_a.candidate_slo_ok[c] == -2)}
+
     # roofline of the dominant kernel (replay_kernel): algorithmic input bytes
     # per launch (24 B/round + 16 B/session per pair of this shard) / its
     # average CUDA-event duration.
@@ -334,6 +356,8 @@ def run_ours(args, rank, world, local):
                     "ms_per_step": float(te.item())},
             "clocks": clk.summary(),
         }
+        if arg:
+            line["argmax_mode"] = arg
         if cpu:
             line["cpu_baseline"] = cpu
         if parity:

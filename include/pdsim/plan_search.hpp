@@ -30,6 +30,10 @@ struct SearchOptions {
   std::int64_t pair_begin = 0;  // shard [pair_begin, pair_end) of c * replicas + r
   std::int64_t pair_end = -1;
   bool report = false;  // per-pair build_report on the device (SearchResult::reports)
+  // Argmax-only search (PDSIM_SEARCH_ARGMAX): candidates that provably cannot
+  // win stop early; best_candidate / best_slo_ok are unchanged, pruned
+  // candidates get candidate_slo_ok = -2 and pairs valid = false.
+  bool prune = false;
 };
 
 struct SearchResult {

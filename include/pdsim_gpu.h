@@ -70,7 +70,8 @@ enum {
   PDSIM_PAIR_OK = 0,
   PDSIM_PAIR_INVALID = 1, /* run() would throw ConfigError (e.g. KV precheck,
                              sim_engine.cpp:217-231); the candidate is invalid */
-  PDSIM_PAIR_ERROR = 2    /* engine capacity/invariant failure (never expected) */
+  PDSIM_PAIR_ERROR = 2,   /* engine capacity/invariant failure (never expected) */
+  PDSIM_PAIR_PRUNED = 3   /* search mode "argmax": stopped once it could no longer win */
 };
 
 /* ---- inputs --------------------------------------------------------------- */
@@ -357,6 +358,21 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
  * 27 admission catch-up over all decode workers. `replayed` counts pairs
  * whose fast attempt was replayed in exact mode. */
 #define PDSIM_PROF_BUCKETS 28
+
+/* Search modes. FULL (default) replays every pair to completion: every
+ * per-pair and per-candidate output is exact. ARGMAX stops a candidate's
+ * replays once it provably cannot be the argmax (SURVEY.md §8(e) pruning):
+ * its upper bound — the sessions of all its replicas minus those already
+ * known to miss the SLO (a TTFT over threshold is final; an ITL miss is known
+ * at session end) — is below the incumbent's lower bound (slo_ok summed over
+ * the incumbent's completed replicas), or equal with a larger enumeration
+ * index. best_candidate and best_slo_ok are identical to FULL mode; pruned
+ * pairs report PDSIM_PAIR_PRUNED and pruned candidates candidate_slo_ok = -2.
+ * Record/report searches always run FULL. Sharded callers reduce
+ * candidate_slo_ok with the same rule as invalid candidates (any negative
+ * excludes the candidate): the global argmax is never pruned on any shard. */
+enum { PDSIM_SEARCH_FULL = 0, PDSIM_SEARCH_ARGMAX = 1 };
+int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode);
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
 int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts,
                                int64_t* replayed);

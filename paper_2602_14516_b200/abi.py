@@ -15,7 +15,8 @@ MAX_WORKERS = 64
 OK, ERR_CONFIG, ERR_DOMAIN, ERR_CUDA, ERR_INTERNAL, ERR_PARSE = 0, 1, 2, 3, 4, 5
 ROUTING_ADAPTIVE, ROUTING_ALWAYS_REMOTE, ROUTING_ALWAYS_LOCAL = 0, 1, 2
 RATIONALES = ("slack_remote", "slack_local", "argmin", "forced_remote", "forced_local")
-PAIR_OK, PAIR_INVALID, PAIR_ERROR = 0, 1, 2
+PAIR_OK, PAIR_INVALID, PAIR_ERROR, PAIR_PRUNED = 0, 1, 2, 3
+SEARCH_FULL, SEARCH_ARGMAX = 0, 1
 
 
 class Curve(C.Structure):

@@ -80,7 +80,11 @@ struct pdsim_gpu_ctx {
   pdg::Caps caps{};
   size_t slot_bytes = 0;   // global workspace per slot
   size_t smem_bytes = 0;   // dynamic shared memory per slot (one warp / block)
-  DevBuf d_trace_data, d_traces, d_plans, d_invalid, d_cand_params;
+  DevBuf d_trace_data, d_traces, d_plans, d_invalid, d_cand_params, d_cand_inv;
+  std::vector<int8_t> cand_invalid;  // [n_candidates]: some pair of c is invalid (whole search)
+  int64_t total_sessions = 0;        // sum of S over the staged traces
+  int search_mode = 0;               // PDSIM_SEARCH_*
+  DevBuf d_pair_fail, d_best_key;    // argmax mode (pruning) state
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
@@ -208,6 +212,13 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
       ctx->pair_invalid[static_cast<size_t>(c) * in->n_traces + r] =
           pdg::precheck(ctx->packed[static_cast<size_t>(r)], ctx->plans[static_cast<size_t>(c)], *profile) ? 0 : 1;
 
+  ctx->cand_invalid.assign(static_cast<size_t>(in->n_candidates), 0);
+  for (int c = 0; c < in->n_candidates; ++c)
+    for (int r = 0; r < in->n_traces; ++r)
+      ctx->cand_invalid[static_cast<size_t>(c)] |= ctx->pair_invalid[static_cast<size_t>(c) * in->n_traces + r];
+  ctx->total_sessions = 0;
+  for (const auto& t : ctx->packed) ctx->total_sessions += t.S;
+
   std::vector<const pdg::PackedTrace*> tp;
   for (auto& t : ctx->packed) tp.push_back(&t);
   // Shared-memory budget per slot: generous when few pairs run at once.
@@ -271,6 +282,9 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   CU(ctx, ctx->d_invalid.reserve(ctx->pair_invalid.size()));
   CU(ctx, cudaMemcpyAsync(ctx->d_invalid.p, ctx->pair_invalid.data(), ctx->pair_invalid.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
+  CU(ctx, ctx->d_cand_inv.reserve(ctx->cand_invalid.size()));
+  CU(ctx, cudaMemcpyAsync(ctx->d_cand_inv.p, ctx->cand_invalid.data(), ctx->cand_invalid.size(), cudaMemcpyHostToDevice,
+                          ctx->stream));
   if (!ctx->cand_params.empty()) {
     CU(ctx, ctx->d_cand_params.reserve(sizeof(pdg::DevParams) * ctx->cand_params.size()));
     CU(ctx, cudaMemcpyAsync(ctx->d_cand_params.p, ctx->cand_params.data(),
@@ -354,6 +368,19 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.rec = rec;
   a.seed = seed;
   a.profile = ctx->profiling;
+  const bool with_rec0 = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
+  const bool prune = ctx->search_mode == PDSIM_SEARCH_ARGMAX && !with_rec0 && !ctx->profiling && n > 0;
+  if (prune) {
+    CU(ctx, ctx->d_pair_fail.reserve(4 * static_cast<size_t>(n)));
+    CU(ctx, ctx->d_best_key.reserve(8));
+    CU(ctx, cudaMemsetAsync(ctx->d_pair_fail.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
+    CU(ctx, cudaMemsetAsync(ctx->d_best_key.p, 0, 8, ctx->stream));
+    a.prune = 1;
+    a.best_key = ctx->d_best_key.as<unsigned long long>();
+    a.pair_fail = ctx->d_pair_fail.as<int32_t>();
+    a.cand_invalid = ctx->d_cand_inv.as<int8_t>();
+    a.total_sessions = ctx->total_sessions;
+  }
   int64_t launches = 0;
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
@@ -364,7 +391,8 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     // samples, pair reports). Each layout's kernels live in their own
     // translation unit (replay_l*.cu).
     const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
-    const int variant = with_rec ? 2 : ctx->profiling ? 1 : 0;
+    // 3: attainment-only search in argmax mode (Prune, engine.cuh).
+    const int variant = with_rec ? 2 : ctx->profiling ? 1 : prune ? 3 : 0;
     pdg::ReplayKernel kern = pdg::replay_kernel_for(ctx->layout, variant);
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
     kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
@@ -421,7 +449,9 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
       if (out->pair_cycles) out->pair_cycles[k] = res[static_cast<size_t>(k)].cycles;
     }
     if (out->candidate_slo_ok) {
-      for (int c = 0; c < C; ++c) out->candidate_slo_ok[c] = cbad[c] ? -1 : static_cast<int64_t>(csum[c]);
+      for (int c = 0; c < C; ++c) {
+        out->candidate_slo_ok[c] = (cbad[c] & 1) ? -1 : (cbad[c] & 2) ? -2 : static_cast<int64_t>(csum[c]);
+      }
     }
     out->best_candidate = best ? static_cast<int32_t>(0xffffffffull - (best & 0xffffffffull)) : -1;
     out->best_slo_ok = best ? static_cast<int64_t>((best >> 32) - 1) : -1;
@@ -592,6 +622,13 @@ const char* pdsim_gpu_last_error(const pdsim_gpu_ctx* ctx) { return ctx ? ctx->e
 int pdsim_gpu_set_stream(pdsim_gpu_ctx* ctx, void* stream) {
   if (int rc = check_ctx(ctx)) return rc;
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (mode != PDSIM_SEARCH_FULL && mode != PDSIM_SEARCH_ARGMAX) return set_err(ctx, PDSIM_ERR_CONFIG, "unknown search mode");
+  ctx->search_mode = mode;
   return PDSIM_OK;
 }
 

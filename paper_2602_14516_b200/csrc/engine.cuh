@@ -467,6 +467,32 @@ struct Records {
   int64_t steps_cap;
 };
 
+// Exact argmax pruning (search mode), shared by the pairs of
+// one launch. A candidate c is dead once its upper bound (total sessions over
+// its replicas minus sessions already known to miss the SLO) is below the
+// incumbent's lower bound (slo_ok summed over its completed replicas), or
+// equal to it with c after the incumbent in enumeration order: c can then
+// never be the argmax (max count, ties to the smallest index).
+struct Prune {
+  unsigned long long* best;  // incumbent key ((lb + 1) << 32) | (0xffffffff - c); 0 = none; null = off
+  int32_t* pair_fail;        // [pairs of the launch] failures seen per pair (max over attempts)
+  int* cand_bad;             // [C] bit 1 = pruned (bit 0 = invalid)
+  int64_t total_sessions;    // sum of S over all replicas
+  int64_t self;              // this pair's index in pair_fail
+  int64_t fail_base;         // index of (c, replica 0) in pair_fail (may be negative)
+  int32_t c;                 // this pair's candidate
+  int32_t r_lo, r_hi;        // replicas of c inside the launch
+  int32_t reserved;
+};
+
+PDG_HD bool prune_dominated(int64_t ub, unsigned long long key, int32_t c) {
+  if (key == 0) return false;
+  const int64_t lb = static_cast<int64_t>(key >> 32) - 1;
+  const int32_t cs = static_cast<int32_t>(0xffffffffull - (key & 0xffffffffull));
+  if (cs == c) return false;
+  return ub < lb || (ub == lb && c > cs);
+}
+
 struct PairResult {
   pdsim_attainment att;
   pdsim_counters ctr;
@@ -575,6 +601,12 @@ struct EngState {
   int64_t folds_;
   double st_[kMaxSlots];    // worker-event slot times (+inf when empty)
   uint64_t sk_[kMaxSlots];  // worker-event slot keys
+  // argmax search mode (kPrune engines only)
+  Prune PRN;
+  int32_t pruned_;    // the candidate can no longer be the argmax
+  int32_t fails_;     // sessions of this attempt known to miss the SLO
+  int32_t prn_pub_;   // fails_ last published to Prune::pair_fail
+  uint32_t prn_tick_;
 };
 
 #if defined(__CUDACC__)
@@ -607,9 +639,11 @@ struct EngineAttach {};
 // kLazy: lazy decode stepping (silent steps are not events). The exact
 // engine (kLazy = false) replays a pair whose lazy attempt hit an ambiguous
 // tie, and runs record modes that need every step as an event.
-template <bool kProf, int kD = 0, int kP = 0, bool kRec = true, bool kLazy = true>
+// kPrune: argmax search mode (Prune): failures are counted and the
+// candidate is tested against the incumbent every 128 events.
+template <bool kProf, int kD = 0, int kP = 0, bool kRec = true, bool kLazy = true, bool kPrune = false>
 class EngineT {
-  template <bool, int, int, bool, bool>
+  template <bool, int, int, bool, bool, bool>
   friend class EngineT;
   static constexpr SmemOff kOff = smem_off(static_cast<size_t>(kD), static_cast<size_t>(kP));
 
@@ -619,7 +653,8 @@ class EngineT {
   // dynamic shared memory (one warp per block): the engine addresses it
   // directly from the shared-memory base, so `this` carries no state.
   PDG_HD EngineT(EngState* es, const DevTrace& tr, const DevPlan& plan, const DevParams& prm, const Caps& caps,
-                const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed, int profile = 0)
+                const SmemSlot& sm, const GlobalSlot& gm, Records rec, uint64_t seed, int profile = 0,
+                const Prune* prn = nullptr)
 #if !defined(__CUDA_ARCH__)
       : s_(es)
 #endif
@@ -634,6 +669,14 @@ class EngineT {
     s_->G = gm;
     s_->REC = rec;
     s_->seed_ = seed;
+    if (prn) {
+      s_->PRN = *prn;
+    } else {
+      memset(&s_->PRN, 0, sizeof(Prune));
+    }
+    s_->pruned_ = 0;
+    s_->prn_pub_ = 0;
+    s_->prn_tick_ = 0;
     warp_sync();
   }
 
@@ -645,12 +688,12 @@ class EngineT {
     const bool exact_first = kRec && (s_->REC.steps || s_->C.rep_gapcap > 0);
     if (kLazy && !exact_first) {
       attempt(0);
-      if (!s_->abort_) {
+      if (!s_->abort_ || s_->pruned_) {
         finish_result(out);
         return;
       }
     }
-    EngineT<kProf, kD, kP, kRec, false> exact{EngineAttach{}};
+    EngineT<kProf, kD, kP, kRec, false, kPrune> exact{EngineAttach{}};
 #if !defined(__CUDA_ARCH__)
     exact.s_ = s_;
 #endif
@@ -677,6 +720,10 @@ class EngineT {
     int bucket = -1;
     while (!s_->failed_ && !s_->abort_) {
       warp_sync();  // re-converge once per event (handlers store uniform values)
+      if (kPrune && ((++s_->prn_tick_ & 127u) == 0) && prune_check()) {
+        s_->pruned_ = 1;
+        return;
+      }
       if (prof) {
         const int64_t now_c = pdg_clock();
         if (bucket >= 0) {
@@ -914,7 +961,7 @@ class EngineT {
     out->n_spans = s_->n_spans_;
     out->events = s_->events_;
     out->exact_folds = s_->folds_;
-    out->status = s_->failed_ ? PDSIM_PAIR_ERROR : PDSIM_PAIR_OK;
+    out->status = s_->failed_ ? PDSIM_PAIR_ERROR : s_->pruned_ ? PDSIM_PAIR_PRUNED : PDSIM_PAIR_OK;
     out->attempts = s_->attempts_;
     for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
       out->prof_cycles[j] = s_->prof_c_[j];
@@ -928,6 +975,34 @@ class EngineT {
 #endif
 
   PDG_HD void fail() { s_->failed_ = 1; }
+
+  // Publishes this pair's failures, then tests the candidate against the
+  // incumbent (Prune). Failures seen in an aborted lazy attempt are real
+  // (everything before the abort equals the exact replay), hence max().
+  PDG_COLD bool prune_check() {
+    const Prune& p = s_->PRN;
+    const int32_t f_own = s_->fails_;
+#if defined(__CUDA_ARCH__)
+    if (f_own > s_->prn_pub_ && lane_id() == 0) atomicMax(&p.pair_fail[p.self], f_own);
+    warp_sync();
+    long long f = 0;
+    for (int32_t r = p.r_lo + lane_id(); r < p.r_hi; r += 32) {
+      const int64_t j = p.fail_base + r;
+      const int32_t v = j == p.self ? f_own : *reinterpret_cast<volatile int32_t*>(&p.pair_fail[j]);
+      f += v > 0 ? v : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(p.best);
+    const bool dead = (*reinterpret_cast<volatile int*>(&p.cand_bad[p.c]) & 2) ||
+                      prune_dominated(p.total_sessions - f, key, p.c);
+    warp_sync();
+    if (f_own > s_->prn_pub_) s_->prn_pub_ = f_own;  // warp-uniform store
+    if (dead && lane_id() == 0) atomicOr(&p.cand_bad[p.c], 2);
+    return dead;
+#else
+    return false;
+#endif
+  }
 
   // Slot arrays in shared memory: fixed offsets from the dynamic shared
   // memory base on the device (one LDS/STS per field, no pointer load).
@@ -964,6 +1039,7 @@ class EngineT {
     s_->nslots_ = s_->PL.D + 2 * s_->PL.P;
     s_->failed_ = 0;
     s_->abort_ = 0;
+    s_->fails_ = 0;
     s_->heap_spilled_ = 0;
     s_->mt_idx_ = 0;
     s_->att_ = pdsim_attainment{};
@@ -2409,6 +2485,11 @@ class EngineT {
         (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(GLP(s_->T.rank)[i]);
     warp_sync();
     const int32_t hint = w.seg_end;
+    if (kPrune) {
+      const bool newly_bad = value > s_->T.ttft_thres && !s.ttft_bad;  // read by every lane before lane 0 writes
+      warp_sync();
+      if (newly_bad) s_->fails_ += 1;  // warp-uniform store
+    }
     if (lane_id() == 0) {
       if (value > s_->T.ttft_thres) s.ttft_bad = 1;
       s.ctx += incr;
@@ -2770,6 +2851,7 @@ class EngineT {
       }
     }
     ++s_->att_.sessions_completed;
+    if (kPrune && ttft_ok && !itl_ok) s_->fails_ += 1;  // TTFT misses were counted when they happened
     s_->att_.slo_ok += slo_ok;
     s_->att_.ttft_ok += ttft_ok;
     s_->att_.itl_ok += itl_ok;

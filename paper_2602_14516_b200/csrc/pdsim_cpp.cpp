@@ -903,7 +903,11 @@ SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<D
     out.pair_report = reps.data();
   }
   pdsim_gpu_ctx* ctx = context(options.device >= 0 ? options.device : default_device());
-  check_ctx(pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out), ctx);
+  check_ctx(pdsim_gpu_set_search_mode(ctx, options.prune && !options.report ? PDSIM_SEARCH_ARGMAX : PDSIM_SEARCH_FULL),
+            ctx);
+  const int rc = pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out);
+  pdsim_gpu_set_search_mode(ctx, PDSIM_SEARCH_FULL);
+  check_ctx(rc, ctx);
   if (options.report) {
     for (int64_t k = 0; k < n; ++k) {
       r.reports.push_back(report_from_pod(

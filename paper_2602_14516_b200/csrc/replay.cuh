@@ -34,13 +34,17 @@ struct KernelArgs {
   pdsim_report* reports;               // optional per-pair reports [pair_end - pair_begin]
   uint64_t seed;
   int32_t profile;                     // per-phase clock64 instrumentation
-  int32_t reserved2;
+  int32_t prune;                       // search mode "argmax" (Prune, engine.cuh)
+  unsigned long long* best_key;        // prune: incumbent key
+  int32_t* pair_fail;                  // prune: [pair_end - pair_begin]
+  const int8_t* cand_invalid;          // prune: [n_candidates] any pair of c invalid (whole search)
+  int64_t total_sessions;              // prune: sum of S over the replicas
 };
 
 // One warp per block; the warp replays pairs pulled from an atomic queue.
 // kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
 // addresses slot state at compile-time offsets (engine.cuh smem_off).
-template <bool kProf, int kD, int kP, bool kRec>
+template <bool kProf, int kD, int kP, bool kRec, bool kPrune = false>
 __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
   const int slot_id = blockIdx.x;
   GlobalSlot gslot;
@@ -65,7 +69,15 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     const int32_t r = static_cast<int32_t>(pair % a.n_traces);
     PairResult res;
     memset(&res, 0, sizeof(res));
-    if (a.pair_invalid[pair]) {
+    bool skip = false;
+    if (kPrune) {  // a dead candidate's remaining replicas are not replayed
+      const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
+      skip = (*reinterpret_cast<volatile int*>(&a.cand_bad[c]) & 2) || prune_dominated(a.total_sessions, key, c);
+    }
+    if (skip) {
+      res.status = PDSIM_PAIR_PRUNED;
+      res.att.sessions_total = a.traces[r].S;
+    } else if (a.pair_invalid[pair]) {
       res.status = PDSIM_PAIR_INVALID;
       res.att.sessions_total = a.traces[r].S;
       if (a.reports && lane == 0) {
@@ -80,7 +92,23 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       const DevPlan pl = a.plans[c];
       const long long t0 = clock64();
       const DevParams prm = a.cand_params ? a.cand_params[c] : a.params;
-      EngineT<kProf, kD, kP, kRec> eng(sslot.es, tr, pl, prm, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0);
+      Prune prn;
+      memset(&prn, 0, sizeof(prn));
+      if (kPrune) {
+        prn.best = a.best_key;
+        prn.pair_fail = a.pair_fail;
+        prn.cand_bad = a.cand_bad;
+        prn.total_sessions = a.total_sessions;
+        prn.self = pair - a.pair_begin;
+        prn.fail_base = static_cast<int64_t>(c) * a.n_traces - a.pair_begin;
+        const int64_t lo = a.pair_begin - static_cast<int64_t>(c) * a.n_traces;
+        const int64_t hi = a.pair_end - static_cast<int64_t>(c) * a.n_traces;
+        prn.r_lo = static_cast<int32_t>(lo < 0 ? 0 : lo);
+        prn.r_hi = static_cast<int32_t>(hi > a.n_traces ? a.n_traces : hi);
+        prn.c = c;
+      }
+      EngineT<kProf, kD, kP, kRec, true, kPrune> eng(sslot.es, tr, pl, prm, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0,
+                                       &prn);
       eng.run(&res);
       res.cycles = clock64() - t0;
       if (kRec && a.reports) {
@@ -91,10 +119,16 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     }
     if (lane == 0) {
       a.results[pair - a.pair_begin] = res;
-      if (res.status != PDSIM_PAIR_OK) {
+      if (res.status == PDSIM_PAIR_PRUNED) {
+        atomicOr(&a.cand_bad[c], 2);
+      } else if (res.status != PDSIM_PAIR_OK) {
         atomicOr(&a.cand_bad[c], 1);
       } else {
-        atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+        const unsigned long long old = atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+        if (kPrune && !a.cand_invalid[c]) {  // completed replicas: a lower bound of c's count
+          const unsigned long long lb = old + static_cast<unsigned long long>(res.att.slo_ok);
+          atomicMax(a.best_key, ((lb + 1ull) << 32) | (0xffffffffull - static_cast<unsigned>(c)));
+        }
       }
     }
     __syncwarp();

@@ -10,6 +10,8 @@ ReplayKernel replay_kernels_l0(int variant) {
       return replay_kernel<true, 8, 8, false>;
     case 2:
       return replay_kernel<false, 8, 8, true>;
+    case 3:
+      return replay_kernel<false, 8, 8, false, true>;
     default:
       return replay_kernel<false, 8, 8, false>;
   }

@@ -8,6 +8,8 @@ ReplayKernel replay_kernels_l1(int variant) {
   switch (variant) {
     case 2:
       return replay_kernel<false, 16, 16, true>;
+    case 3:
+      return replay_kernel<false, 16, 16, false, true>;
     default:  // diagnostics are built for the <8,8> layout only
       return replay_kernel<false, 16, 16, false>;
   }

@@ -64,6 +64,7 @@ def lib():
         L.pdsim_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int32]
         L.pdsim_format_double.restype = C.c_int32
         L.pdsim_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.pdsim_gpu_set_search_mode.argtypes = [C.c_void_p, C.c_int]
         L.pdsim_gpu_profile_counters.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.pdsim_gpu_search_staged.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, P(abi.SearchOutput)]
         L.pdsim_synth_spec_default.argtypes = [P(abi.SynthSpec)]
@@ -361,6 +362,11 @@ class Context:
                                           C.byref(profile), seed, C.byref(out)))
         self._staged = (len(traces), len(settings))
         return SearchResult(out, att, ctr, st, cand, n)
+
+    def set_search_mode(self, mode):
+        """abi.SEARCH_FULL (default) or abi.SEARCH_ARGMAX (exact pruning:
+        same best_candidate / best_slo_ok, pruned candidates report -2)."""
+        self._check(lib().pdsim_gpu_set_search_mode(self._h, int(mode)))
 
     def set_profiling(self, enable):
         self._check(lib().pdsim_gpu_set_profiling(self._h, 1 if enable else 0))

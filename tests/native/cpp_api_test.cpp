@@ -168,6 +168,19 @@ int main() {
     }
   }
 
+  // SearchOptions::prune (argmax mode): same winner and count as the full search.
+  {
+    const std::vector<DeploymentPlan> cands = enumerate_plans({1, 2, 4}, 8);
+    const SearchResult full = plan_search({gen}, cands, p, SchedulerParams{}, 3);
+    SearchOptions so;
+    so.prune = true;
+    const SearchResult pr = plan_search({gen}, cands, p, SchedulerParams{}, 3, so);
+    CHECK(pr.best_candidate == full.best_candidate && pr.best_slo_ok == full.best_slo_ok);
+    for (size_t c = 0; c < cands.size(); ++c) {
+      CHECK(pr.candidate_slo_ok[c] == -2 || pr.candidate_slo_ok[c] == full.candidate_slo_ok[c]);
+    }
+  }
+
   // sweep() (pdsim sweep, pdsim.cpp:501-590): one launch over traces x
   // settings; each report equals build_report of run() under that setting.
   {

@@ -2,6 +2,8 @@
 alternates runs of the staged C2 search in fresh processes.
 
 usage: python tools/ab.py LIB_A LIB_B [rounds] [config] [pair_begin] [pair_end]
+LIB_x is a libpdsim_gpu.so, or a directory holding a whole package copy
+(paper_2602_14516_b200/ with its .so) when the Python bindings differ too.
 """
 import os
 import subprocess
@@ -25,8 +27,14 @@ def main(a, b, rounds=3, cfg="C2", pb="0", pe="-1"):
     res = {a: [], b: []}
     for _ in range(int(rounds)):
         for lib in (a, b):
-            env = dict(os.environ, PDSIM_LIB=os.path.abspath(lib))
-            out = subprocess.run([sys.executable, "-c", CHILD, cfg, pb, pe], cwd=root, env=env, capture_output=True, text=True)
+            if os.path.isdir(lib):
+                env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
+                cwd = os.path.abspath(lib)
+            else:
+                env = dict(os.environ, PDSIM_LIB=os.path.abspath(lib))
+                cwd = root
+            out = subprocess.run([sys.executable, "-c", CHILD, cfg, pb, pe], cwd=cwd, env=env, capture_output=True,
+                                 text=True)
             res[lib].append(float(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else None)
     for lib, v in res.items():
         print(cfg, lib, v, "min", min(x for x in v if x is not None))
