@@ -718,6 +718,7 @@ class EngineT {
     constexpr bool prof = kProf;
     int64_t tp = prof ? pdg_clock() : 0;
     int bucket = -1;
+    const int32_t n_sess = s_->T.S;
     while (!s_->failed_ && !s_->abort_) {
       warp_sync();  // re-converge once per event (handlers store uniform values)
       if (kPrune && ((++s_->prn_tick_ & 127u) == 0) && prune_check()) {
@@ -733,6 +734,9 @@ class EngineT {
         tp = now_c;
         bucket = kProfSelect;
       }
+      // Arrival cursor read ahead of the slot reduction (overlaps its latency).
+      const int32_t next_arr = s_->next_arr_;
+      const double next_arr_t = s_->next_arr_t_;
       // Next worker event: min over the slot table (lanes split the slots).
       double bt;
       uint64_t bk;
@@ -752,7 +756,7 @@ class EngineT {
       }
       // Arrivals carry kind 0 and seq = index: they precede every dynamic
       // event at an equal time (sim_engine.cpp:137-143).
-      if (s_->next_arr_ < s_->T.S && (src < 0 || s_->next_arr_t_ <= bt)) src = 2;
+      if (next_arr < n_sess && (src < 0 || next_arr_t <= bt)) src = 2;
       if (src < 0) {
         if (kLazy) catch_up(kInf, 0);  // drain silent steps (none remain)
         break;
@@ -1209,31 +1213,28 @@ class EngineT {
     if (lane + 32 < nslots) {
       const uint64_t t2 = dbits(s_->st_[lane + 32]);
       const uint64_t k2 = s_->sk_[lane + 32];
-      if (t2 < tb || (t2 == tb && k2 < kb)) {
-        tb = t2;
-        kb = k2;
-        id = lane + 32;
-      }
+      const bool take = (t2 < tb) | ((t2 == tb) & (k2 < kb));  // branch-free select
+      tb = take ? t2 : tb;
+      kb = take ? k2 : kb;
+      id = take ? lane + 32 : id;
     }
     static_assert(kSmallHeap <= 64, "two small-set entries per lane");
     const HEv* h = SHEAP();
     if (lane < hn) {
       const uint64_t t2 = dbits(h[lane].t);
       const uint64_t k2 = h[lane].key;
-      if (t2 < tb || (t2 == tb && k2 < kb)) {
-        tb = t2;
-        kb = k2;
-        id = kMaxSlots + lane;
-      }
+      const bool take = (t2 < tb) | ((t2 == tb) & (k2 < kb));  // branch-free select
+      tb = take ? t2 : tb;
+      kb = take ? k2 : kb;
+      id = take ? kMaxSlots + lane : id;
     }
     if (lane + 32 < hn) {
       const uint64_t t2 = dbits(h[lane + 32].t);
       const uint64_t k2 = h[lane + 32].key;
-      if (t2 < tb || (t2 == tb && k2 < kb)) {
-        tb = t2;
-        kb = k2;
-        id = kMaxSlots + lane + 32;
-      }
+      const bool take = (t2 < tb) | ((t2 == tb) & (k2 < kb));  // branch-free select
+      tb = take ? t2 : tb;
+      kb = take ? k2 : kb;
+      id = take ? kMaxSlots + lane + 32 : id;
     }
     const uint32_t hi = static_cast<uint32_t>(tb >> 32);
     const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
@@ -1732,7 +1733,8 @@ class EngineT {
   // smallest upper bound cannot win, and exact folds run only when two or
   // more candidates remain in contention.
   PDG_COLD void argmin_route(int d, int32_t ctx, int32_t incr, RouteOut* r) {
-    constexpr int kPer = (kMaxSlots + PDG_NL - 1) / PDG_NL;
+    // prefill candidates per lane: the compiled layout bounds P by kP
+    constexpr int kPer = ((kP > 0 ? kP : kMaxSlots) + PDG_NL - 1) / PDG_NL;
     const int n = s_->PL.P;
     const int lane = lane_id();
     double llo, lhi;
