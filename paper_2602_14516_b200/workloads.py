@@ -13,6 +13,10 @@ ReAct / mixed presets; this module is the repo's pinned mapping:
 All generation runs on the host through the product library's generators
 (bit-identical to the reference's, see tests/test_generators.py).
 """
+import ctypes as C
+
+import numpy as np
+
 from . import abi, native
 
 PROFILE_SEED = 7
@@ -133,6 +137,72 @@ def c5(model="llama3-8b", rates=None, seeds=4, sessions=1000, total_gpus=8):
                     f"{model}, {len(plans)} plans x {len(trs)} toolbench traces ({len(rates)} rates x {seeds} seeds)")
 
 
+class OwnedTrace:
+    """A host-built trace: numpy arrays kept alive, ``.view`` their pdsim_trace."""
+
+    def __init__(self, sid, arrival, round_offset, incr, dec, delay, ttft_thres, itl_thres):
+        self._arrays = [np.ascontiguousarray(sid, np.int64), np.ascontiguousarray(arrival, np.float64),
+                        np.ascontiguousarray(round_offset, np.int64), np.ascontiguousarray(incr, np.int64),
+                        np.ascontiguousarray(dec, np.int64), np.ascontiguousarray(delay, np.float64)]
+        a = self._arrays
+        ptr = lambda x, t: x.ctypes.data_as(C.POINTER(t))  # noqa: E731
+        self.view = abi.Trace(len(a[0]), len(a[3]), ptr(a[0], C.c_int64), ptr(a[1], C.c_double),
+                              ptr(a[2], C.c_int64), ptr(a[3], C.c_int64), ptr(a[4], C.c_int64),
+                              ptr(a[5], C.c_double), ttft_thres, itl_thres)
+
+
+def _arrays(v):
+    S, R = int(v.n_sessions), int(v.n_rounds)
+    get = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0)  # noqa: E731
+    return (get(v.session_id, S).astype(np.int64), get(v.arrival_time, S), get(v.round_offset, S + 1).astype(np.int64),
+            get(v.incr_input_len, R).astype(np.int64), get(v.decode_len, R).astype(np.int64),
+            get(v.interaction_delay, R))
+
+
+def merge_traces(a, b):
+    """C4's mixed agent + RAG trace: the sessions of two
+    traces merged by arrival time (stable: ties keep a's sessions first), ids
+    renumbered 0..S-1 in merged order, each session keeping its rounds. The
+    two presets share their SLO (workload.cpp:144, 156)."""
+    if (a.ttft_thres, a.itl_thres) != (b.ttft_thres, b.itl_thres):
+        raise ValueError("merge_traces: the traces' SLOs differ")
+    sa, aa, oa, ia, da, ya = _arrays(a)
+    sb, ab, ob, ib, db, yb = _arrays(b)
+    arr = np.concatenate([aa, ab])
+    order = np.argsort(arr, kind="stable")
+    starts = np.concatenate([oa[:-1], ob[:-1] + len(ia)])
+    lens = np.concatenate([np.diff(oa), np.diff(ob)])
+    inc, dec, dly = np.concatenate([ia, ib]), np.concatenate([da, db]), np.concatenate([ya, yb])
+    l_sorted = lens[order]
+    off = np.zeros(len(order) + 1, np.int64)
+    np.cumsum(l_sorted, out=off[1:])
+    # gather each session's round slice in merged order
+    idx = np.repeat(starts[order] - off[:-1], l_sorted) + np.arange(off[-1])
+    return OwnedTrace(np.arange(len(order)), arr[order], off, inc[idx], dec[idx], dly[idx], a.ttft_thres, a.itl_thres)
+
+
+C4_RATES = (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0, 8.0)
+
+
+def c4(rates=None, seeds=1, sessions=100000, total_gpus=8):
+    """C4: llama3-70b, mixed toolbench + hotpotqa traces (sessions/2 each at
+    rate/2 each, merged by arrival), an arrival-rate sweep x seeds. The full
+    grid is 8 rates x 64 seeds (512 traces x 169 plans = 86 528 pairs, ~5 GB
+    of host trace arrays); the default is its first seed."""
+    rates = list(rates or C4_RATES)
+    half = sessions // 2
+    jobs = [(r, s) for s in range(seeds) for r in rates]
+    tool = native.gen_traces(trace_stats("toolbench"), [r / 2 for r, _ in jobs], half,
+                             [1 + 2 * k for k in range(len(jobs))])
+    hot = native.gen_traces(trace_stats("hotpotqa"), [r / 2 for r, _ in jobs], sessions - half,
+                            [2 + 2 * k for k in range(len(jobs))])
+    trs = [merge_traces(t.view, h.view) for t, h in zip(tool, hot)]
+    plans = native.enumerate_plans(DEGREES, total_gpus)
+    return Workload("C4", "llama3-70b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
+                    f"llama3-70b, {len(plans)} plans x {len(trs)} mixed toolbench+hotpotqa traces of {sessions} "
+                    f"sessions ({len(rates)} rates x {seeds} seed(s))")
+
+
 def c2_small():
     """C2 with a 2000-session trace (profiling / quick checks only)."""
     wl = c2(sessions=2000)
@@ -140,4 +210,4 @@ def c2_small():
     return wl
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C5": c5}
+CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C4": c4, "C5": c5}
