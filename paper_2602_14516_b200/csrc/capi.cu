@@ -84,7 +84,7 @@ struct pdsim_gpu_ctx {
   std::vector<int8_t> cand_invalid;  // [n_candidates]: some pair of c is invalid (whole search)
   int64_t total_sessions = 0;        // sum of S over the staged traces
   int search_mode = 0;               // PDSIM_SEARCH_*
-  DevBuf d_pair_fail, d_best_key;    // argmax mode (pruning) state
+  DevBuf d_pair_fail, d_pair_ok, d_best_key;  // argmax mode (pruning) state
   // per-search buffers
   DevBuf d_ws, d_results, d_cand_sum, d_cand_bad, d_counter, d_best;
   // single-run records
@@ -372,12 +372,15 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   const bool prune = ctx->search_mode == PDSIM_SEARCH_ARGMAX && !with_rec0 && !ctx->profiling && n > 0;
   if (prune) {
     CU(ctx, ctx->d_pair_fail.reserve(4 * static_cast<size_t>(n)));
+    CU(ctx, ctx->d_pair_ok.reserve(4 * static_cast<size_t>(n)));
+    CU(ctx, cudaMemsetAsync(ctx->d_pair_ok.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
     CU(ctx, ctx->d_best_key.reserve(8));
     CU(ctx, cudaMemsetAsync(ctx->d_pair_fail.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
     CU(ctx, cudaMemsetAsync(ctx->d_best_key.p, 0, 8, ctx->stream));
     a.prune = 1;
     a.best_key = ctx->d_best_key.as<unsigned long long>();
     a.pair_fail = ctx->d_pair_fail.as<int32_t>();
+    a.pair_ok = ctx->d_pair_ok.as<int32_t>();
     a.cand_invalid = ctx->d_cand_inv.as<int8_t>();
     a.total_sessions = ctx->total_sessions;
   }

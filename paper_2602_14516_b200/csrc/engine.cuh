@@ -476,13 +476,14 @@ struct Records {
 struct Prune {
   unsigned long long* best;  // incumbent key ((lb + 1) << 32) | (0xffffffff - c); 0 = none; null = off
   int32_t* pair_fail;        // [pairs of the launch] failures seen per pair (max over attempts)
+  int32_t* pair_ok;          // [pairs of the launch] sessions attaining the SLO so far (max over attempts)
   int* cand_bad;             // [C] bit 1 = pruned (bit 0 = invalid)
   int64_t total_sessions;    // sum of S over all replicas
   int64_t self;              // this pair's index in pair_fail
   int64_t fail_base;         // index of (c, replica 0) in pair_fail (may be negative)
   int32_t c;                 // this pair's candidate
   int32_t r_lo, r_hi;        // replicas of c inside the launch
-  int32_t reserved;
+  int32_t c_invalid;         // some pair of c is invalid: c never becomes the incumbent
 };
 
 PDG_HD bool prune_dominated(int64_t ub, unsigned long long key, int32_t c) {
@@ -606,6 +607,7 @@ struct EngState {
   int32_t pruned_;    // the candidate can no longer be the argmax
   int32_t fails_;     // sessions of this attempt known to miss the SLO
   int32_t prn_pub_;   // fails_ last published to Prune::pair_fail
+  int32_t prn_ok_pub_;  // att_.slo_ok last published to Prune::pair_ok
   uint32_t prn_tick_;
 };
 
@@ -676,6 +678,7 @@ class EngineT {
     }
     s_->pruned_ = 0;
     s_->prn_pub_ = 0;
+    s_->prn_ok_pub_ = 0;
     s_->prn_tick_ = 0;
     warp_sync();
   }
@@ -986,21 +989,43 @@ class EngineT {
   PDG_COLD bool prune_check() {
     const Prune& p = s_->PRN;
     const int32_t f_own = s_->fails_;
+    const int32_t ok_own = static_cast<int32_t>(s_->att_.slo_ok);
 #if defined(__CUDA_ARCH__)
-    if (f_own > s_->prn_pub_ && lane_id() == 0) atomicMax(&p.pair_fail[p.self], f_own);
+    if (lane_id() == 0) {
+      if (f_own > s_->prn_pub_) atomicMax(&p.pair_fail[p.self], f_own);
+      if (ok_own > s_->prn_ok_pub_) atomicMax(&p.pair_ok[p.self], ok_own);
+    }
     warp_sync();
-    long long f = 0;
+    // Bounds of this candidate over its replicas in the launch: published
+    // values are real (max over attempts); this pair's own counts join by max.
+    long long f = 0, ok = 0;
     for (int32_t r = p.r_lo + lane_id(); r < p.r_hi; r += 32) {
       const int64_t j = p.fail_base + r;
-      const int32_t v = j == p.self ? f_own : *reinterpret_cast<volatile int32_t*>(&p.pair_fail[j]);
-      f += v > 0 ? v : 0;
+      int32_t vf = *reinterpret_cast<volatile int32_t*>(&p.pair_fail[j]);
+      int32_t vo = *reinterpret_cast<volatile int32_t*>(&p.pair_ok[j]);
+      if (j == p.self) {
+        vf = vf > f_own ? vf : f_own;
+        vo = vo > ok_own ? vo : ok_own;
+      }
+      f += vf > 0 ? vf : 0;
+      ok += vo > 0 ? vo : 0;
     }
-    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      f += __shfl_xor_sync(0xffffffffu, f, o);
+      ok += __shfl_xor_sync(0xffffffffu, ok, o);
+    }
+    // Sessions already attaining the SLO are final: a running candidate's
+    // partial count is a lower bound too (valid candidates only).
+    if (!p.c_invalid && ok > 0 && lane_id() == 0) {
+      atomicMax(p.best, (static_cast<unsigned long long>(ok + 1) << 32) | (0xffffffffull - static_cast<unsigned>(p.c)));
+    }
     const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(p.best);
     const bool dead = (*reinterpret_cast<volatile int*>(&p.cand_bad[p.c]) & 2) ||
                       prune_dominated(p.total_sessions - f, key, p.c);
     warp_sync();
-    if (f_own > s_->prn_pub_) s_->prn_pub_ = f_own;  // warp-uniform store
+    // warp-uniform stores
+    if (f_own > s_->prn_pub_) s_->prn_pub_ = f_own;
+    if (ok_own > s_->prn_ok_pub_) s_->prn_ok_pub_ = ok_own;
     if (dead && lane_id() == 0) atomicOr(&p.cand_bad[p.c], 2);
     return dead;
 #else

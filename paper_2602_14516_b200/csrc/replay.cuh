@@ -37,6 +37,7 @@ struct KernelArgs {
   int32_t prune;                       // search mode "argmax" (Prune, engine.cuh)
   unsigned long long* best_key;        // prune: incumbent key
   int32_t* pair_fail;                  // prune: [pair_end - pair_begin]
+  int32_t* pair_ok;                    // prune: [pair_end - pair_begin]
   const int8_t* cand_invalid;          // prune: [n_candidates] any pair of c invalid (whole search)
   int64_t total_sessions;              // prune: sum of S over the replicas
 };
@@ -97,6 +98,8 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       if (kPrune) {
         prn.best = a.best_key;
         prn.pair_fail = a.pair_fail;
+        prn.pair_ok = a.pair_ok;
+        prn.c_invalid = a.cand_invalid[c];
         prn.cand_bad = a.cand_bad;
         prn.total_sessions = a.total_sessions;
         prn.self = pair - a.pair_begin;
@@ -125,6 +128,11 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
         atomicOr(&a.cand_bad[c], 1);
       } else {
         const unsigned long long old = atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+        if (kPrune) {  // final counts join the replicas' bounds
+          atomicMax(&a.pair_ok[pair - a.pair_begin], static_cast<int32_t>(res.att.slo_ok));
+          atomicMax(&a.pair_fail[pair - a.pair_begin],
+                    static_cast<int32_t>(res.att.sessions_total - res.att.slo_ok));
+        }
         if (kPrune && !a.cand_invalid[c]) {  // completed replicas: a lower bound of c's count
           const unsigned long long lb = old + static_cast<unsigned long long>(res.att.slo_ok);
           atomicMax(a.best_key, ((lb + 1ull) << 32) | (0xffffffffull - static_cast<unsigned>(c)));
