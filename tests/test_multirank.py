@@ -88,3 +88,30 @@ def test_argmax_ties_and_invalid():
     t = torch.tensor([5, 7, -1, 7, 3])
     assert distributed.argmax(t) == (1, 7)
     assert distributed.argmax(torch.tensor([-1, -1])) == (-1, -1)
+
+
+def _pruned_worker(rank, world, port, q):
+    """Argmax-mode shards: each rank reports -2 for candidates its own bounds
+    pruned; the reduction excludes every negative (include/pdsim_gpu.h)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    local = [[-2, 5, 3, 7], [4, 6, -2, -1]][rank]
+    totals = distributed.reduce_counts(local)
+    q.put((rank, distributed.argmax(totals), totals.tolist()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_reduction_excludes_pruned_candidates():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_pruned_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, (best, cnt), totals in got:
+        assert totals == [-1, 11, -1, -1]
+        assert (best, cnt) == (1, 11)
