@@ -17,3 +17,11 @@ with native.Context(0) as ctx:
     st = native.preset_stats("toolbench")
     c = ctx.estimate_coefficients(st, [4.0, 8.0], [1, 2], prof, [1, 2, 4], 4)
     print("planner ok", [x[1] for x in c])
+    trs = [native.gen_trace(native.preset_stats("hotpotqa"), 20.0, 80, k) for k in (1, 2)]
+    ctx.set_search_mode(abi.SEARCH_ARGMAX)
+    a = ctx.plan_search([t.view for t in trs], plans, prof, abi.default_params(), 1)
+    ctx.set_search_mode(abi.SEARCH_FULL)
+    print("argmax ok", a.best_candidate, a.best_slo_ok)
+    settings = [abi.default_params(), abi.default_params(alpha=0.5, window=1), abi.default_params(reorder=0)]
+    w = ctx.sweep([t.view for t in trs], abi.make_plan({1: 1}, {1: 2}), prof, settings, 3)
+    print("sweep ok", [round(x.slo_attainment, 3) for x in w.reports])
