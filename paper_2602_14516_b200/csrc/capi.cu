@@ -369,7 +369,8 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   a.seed = seed;
   a.profile = ctx->profiling;
   const bool with_rec0 = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
-  const bool prune = ctx->search_mode == PDSIM_SEARCH_ARGMAX && !with_rec0 && !ctx->profiling && n > 0;
+  // (a single candidate is its own argmax: nothing to prune)
+  const bool prune = ctx->search_mode == PDSIM_SEARCH_ARGMAX && !with_rec0 && !ctx->profiling && n > 0 && C > 1;
   if (prune) {
     CU(ctx, ctx->d_pair_fail.reserve(4 * static_cast<size_t>(n)));
     CU(ctx, ctx->d_pair_ok.reserve(4 * static_cast<size_t>(n)));
