@@ -1,8 +1,9 @@
 // pdsim/metrics.hpp — drop-in Report types and build_report (reference
 // proj/include/pdsim/metrics.hpp:32-60, proj/src/metrics.cpp:108-190).
-// The CSV codecs and text/JSON formatting of the reference stay out of scope
-// (document I/O); the aggregation itself is here, and the batched search can
-// compute it per pair on the device (SearchOptions::report).
+// The raw-sample CSV writers of `pdsim simulate` are here too (byte-identical,
+// std::to_chars numbers); the CSV parsers and JSON/text report formatting stay
+// out of scope (document I/O). The batched search can compute the Report per
+// pair on the device (SearchOptions::report).
 #pragma once
 
 #include <cstdint>
@@ -37,6 +38,12 @@ struct Report {
 // Nearest-rank percentile: index ceil(q*n) on the 1-based sorted list; empty
 // input yields 0 (metrics.cpp:125-136). Throws DomainError for q outside (0, 1].
 double percentile_nearest_rank(std::vector<double> values, double q);
+
+// Raw-sample CSVs (metrics.cpp:350-474): header line, one row per record.
+std::string ttft_csv(const std::vector<TtftSample>& samples);
+std::string itl_csv(const std::vector<ItlSample>& samples);
+std::string sessions_csv(const std::vector<SessionOutcome>& sessions);
+std::string decisions_csv(const std::vector<DecisionRecord>& decisions);
 
 Report build_report(const SimResult& result);
 Report build_report_from_samples(const std::string& trace_name, std::int64_t sessions_total,

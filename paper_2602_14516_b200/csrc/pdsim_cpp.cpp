@@ -798,6 +798,56 @@ Report report_from_pod(const pdsim_report& p, const std::string& name) {
   return x;
 }
 
+// ---- raw-sample CSV writers (metrics.cpp:350-474) ----
+namespace {
+std::string num(double v) {
+  char buf[64];
+  const int32_t n = pdsim_format_double(v, buf, sizeof(buf));
+  return std::string(buf, static_cast<size_t>(std::max(n, 0)));
+}
+const char* flag(bool b) { return b ? "1" : "0"; }
+}  // namespace
+
+std::string ttft_csv(const std::vector<TtftSample>& samples) {
+  std::string out = "session_id,round,kind,local,created_time,completion_time,value\n";
+  for (const TtftSample& s : samples) {
+    out += std::to_string(s.session_id) + ',' + std::to_string(s.round) + ',' +
+           (s.kind == TaskKind::kInitial ? "initial" : "incremental") + ',' + flag(s.local) + ',' +
+           num(s.created_time) + ',' + num(s.completion_time) + ',' + num(s.value) + '\n';
+  }
+  return out;
+}
+
+std::string itl_csv(const std::vector<ItlSample>& samples) {
+  std::string out = "session_id,round,token_index,completion_time,value\n";
+  for (const ItlSample& s : samples) {
+    out += std::to_string(s.session_id) + ',' + std::to_string(s.round) + ',' + std::to_string(s.token_index) + ',' +
+           num(s.completion_time) + ',' + num(s.value) + '\n';
+  }
+  return out;
+}
+
+std::string sessions_csv(const std::vector<SessionOutcome>& sessions) {
+  std::string out = "session_id,arrival_time,completion_time,rounds,admission_wait,mean_itl,ttft_ok,itl_ok,slo_ok\n";
+  for (const SessionOutcome& s : sessions) {
+    out += std::to_string(s.session_id) + ',' + num(s.arrival_time) + ',' + num(s.completion_time) + ',' +
+           std::to_string(s.rounds) + ',' + num(s.admission_wait) + ',' + num(s.mean_itl) + ',' + flag(s.ttft_ok) +
+           ',' + flag(s.itl_ok) + ',' + flag(s.slo_ok) + '\n';
+  }
+  return out;
+}
+
+std::string decisions_csv(const std::vector<DecisionRecord>& decisions) {
+  std::string out = "time,session_id,round,local,worker,rationale,estimated_cost\n";
+  for (const DecisionRecord& d : decisions) {
+    out += num(d.time) + ',' + std::to_string(d.session_id) + ',' + std::to_string(d.round) + ',' + flag(d.local) +
+           ',' + std::to_string(d.worker) + ',' + to_string(d.rationale) + ',';
+    if (d.estimated_cost) out += num(*d.estimated_cost);
+    out += '\n';
+  }
+  return out;
+}
+
 // ---- sweep(): pdsim sweep as one batched GPU call ----
 std::vector<Report> sweep(const std::vector<Trace>& traces, const DeploymentPlan& plan, const PerfProfile& profile,
                           const std::vector<SchedulerParams>& settings, std::uint64_t seed,

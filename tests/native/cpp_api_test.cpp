@@ -28,6 +28,15 @@ static int failures = 0;
 
 static bool near(double a, double b) { return std::fabs(a - b) <= 1e-12 * std::max(1.0, std::fabs(b)); }
 
+static std::uint64_t fnv1a(const std::string& text) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : text) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
 static DeploymentPlan simple_plan(int prefill, int decode, int degree = 1) {
   DeploymentPlan plan;
   if (prefill > 0) plan.x[degree] = prefill;
@@ -166,6 +175,20 @@ int main() {
       CHECK(got.itl.mean == want.itl.mean && got.itl.p95 == want.itl.p95 && got.itl.count == want.itl.count);
       CHECK(got.e2e_mean == want.e2e_mean && got.local_fraction == want.local_fraction);
     }
+  }
+
+  // `pdsim simulate`'s raw-sample CSVs (metrics.cpp:350-474) of the survey
+  // fingerprint scenario: dureader 4000 sessions @16 seed
+  // 101, P:2x1 D:2x1, profile seed 7, engine seed 2 -> the reference's FNV-1a
+  // hashes of decisions / ttft / sessions / itl CSV text.
+  {
+    const PerfProfile fp = synth_profile(SynthProfileSpec{}, 7);
+    const Trace ft = gen_trace(preset_stats("dureader"), 16.0, 4000, 101);
+    const SimResult fr = run(ft, simple_plan(2, 2), fp, SchedulerParams{}, 2);
+    CHECK(fnv1a(decisions_csv(fr.decisions)) == 0x665772a5ffd1e99full);
+    CHECK(fnv1a(ttft_csv(fr.ttft_samples)) == 0xe4e6dd847853dbaeull);
+    CHECK(fnv1a(sessions_csv(fr.sessions)) == 0x2038a6a05715eebbull);
+    CHECK(fnv1a(itl_csv(fr.itl_samples)) == 0xbd3adf1d08563504ull);
   }
 
   // SearchOptions::prune (argmax mode): same winner and count as the full search.
