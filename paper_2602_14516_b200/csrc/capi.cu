@@ -378,7 +378,6 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     CU(ctx, ctx->d_best_key.reserve(8));
     CU(ctx, cudaMemsetAsync(ctx->d_pair_fail.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
     CU(ctx, cudaMemsetAsync(ctx->d_best_key.p, 0, 8, ctx->stream));
-    a.prune = 1;
     a.best_key = ctx->d_best_key.as<unsigned long long>();
     a.pair_fail = ctx->d_pair_fail.as<int32_t>();
     a.pair_ok = ctx->d_pair_ok.as<int32_t>();

@@ -34,7 +34,7 @@ struct KernelArgs {
   pdsim_report* reports;               // optional per-pair reports [pair_end - pair_begin]
   uint64_t seed;
   int32_t profile;                     // per-phase clock64 instrumentation
-  int32_t prune;                       // search mode "argmax" (Prune, engine.cuh)
+  int32_t reserved3;
   unsigned long long* best_key;        // prune: incumbent key
   int32_t* pair_fail;                  // prune: [pair_end - pair_begin]
   int32_t* pair_ok;                    // prune: [pair_end - pair_begin]
