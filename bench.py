@@ -206,9 +206,18 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
     from paper_2602_14516_b200 import abi, native, workloads
 
+    # PDSIM_BENCH_SHARED_GPU=1 (functional check of the N > 1 path on a
+    # one-GPU box only): ranks share the visible GPUs and reduce over gloo.
+    # Never used for a reported number: NCCL over one GPU per rank is the path.
+    shared = os.environ.get("PDSIM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # N > 1: weak scaling over trace replicas. The workload grows to N
     # replicas of the trace; rank r replays every candidate on replica r
     # (no data-path communication), and the per-candidate SLO counts are
