@@ -8,6 +8,8 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
              -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC)
 HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC)
+# nlohmann/json 3.11 (header-only; the copy cudnn_frontend vendors in the venv)
+JSON_DIR  ?= $(shell python3 -c "import sysconfig,os;print(os.path.join(sysconfig.get_paths()['purelib'],'include/cudnn_frontend/thirdparty/nlohmann'))" 2>/dev/null)
 HDRS      := include/pdsim_gpu.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp)
 CPPHDRS   := $(wildcard include/pdsim/*.hpp)
 
@@ -15,7 +17,7 @@ LIB       := $(PKG)/libpdsim_gpu.so
 HOSTSIM   := tests/native/libhostsim.so
 CPPTEST   := tests/native/cpp_api_test
 
-all: $(LIB) $(HOSTSIM) $(CPPTEST) oracle
+all: $(LIB) $(HOSTSIM) $(CPPTEST) oracle refsuites
 
 $(PKG)/build/capi.o: $(CSRC)/capi.cu $(HDRS)
 	@mkdir -p $(PKG)/build
@@ -37,7 +39,19 @@ $(PKG)/build/pdsim_cpp.o: $(CSRC)/pdsim_cpp.cpp $(HDRS) $(CPPHDRS)
 	@mkdir -p $(PKG)/build
 	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
 
-$(LIB): $(PKG)/build/capi.o $(PKG)/build/replay_l0.o $(PKG)/build/replay_l1.o $(PKG)/build/replay_l2.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o
+$(PKG)/build/policy_host.o: $(CSRC)/policy_host.cpp $(CPPHDRS)
+	@mkdir -p $(PKG)/build
+	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
+
+$(PKG)/build/metrics_io.o: $(CSRC)/metrics_io.cpp $(CPPHDRS)
+	@mkdir -p $(PKG)/build
+	$(CXX) $(HOSTFLAGS) -std=c++20 -I$(JSON_DIR) -c $< -o $@
+
+$(PKG)/build/doc_io.o: $(CSRC)/doc_io.cpp $(CPPHDRS)
+	@mkdir -p $(PKG)/build
+	$(CXX) $(HOSTFLAGS) -std=c++20 -I$(JSON_DIR) -c $< -o $@
+
+$(LIB): $(PKG)/build/capi.o $(PKG)/build/replay_l0.o $(PKG)/build/replay_l1.o $(PKG)/build/replay_l2.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o $(PKG)/build/policy_host.o $(PKG)/build/metrics_io.o $(PKG)/build/doc_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 # C++ drop-in API check program (links the product library; runs on a GPU box).
@@ -52,7 +66,27 @@ $(HOSTSIM): tests/native/hostsim.cpp $(HDRS)
 oracle:
 	$(MAKE) -C oracle all
 
+# TEST-ONLY: the reference's own unit and acceptance suites, UNMODIFIED,
+# compiled from where they lie under /root/reference against the drop-in
+# headers (include/pdsim) + libpdsim_gpu.so, with a doctest stand-in
+# (tests/native/doctest/doctest.h). Built only where the reference exists;
+# the binaries travel to the GPU box with the snapshot (git-ignored).
+REF_TESTS ?= /root/reference/proj/tests
+REFSUITES := perf_model_test workload_test planner_test coordinator_test reorder_test sim_engine_test \
+             metrics_test acceptance_test
+ifneq ($(wildcard $(REF_TESTS)/sim_engine_test.cpp),)
+refsuites: $(addprefix tests/native/ref_suites/,$(REFSUITES))
+
+tests/native/ref_suites/%: $(REF_TESTS)/%.cpp $(LIB) $(CPPHDRS) tests/native/doctest/doctest.h
+	@mkdir -p tests/native/ref_suites
+	$(CXX) -O2 -std=c++20 -Iinclude -Itests/native/doctest $< -o $@ -L$(PKG) -lpdsim_gpu \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
+else
+refsuites:
+	@echo "reference tests absent; using prebuilt tests/native/ref_suites/ if any"
+endif
+
 clean:
 	rm -rf $(PKG)/build $(LIB) $(HOSTSIM) $(CPPTEST)
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean refsuites

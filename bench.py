@@ -2,29 +2,42 @@
 """bench.py — candidate-plan replay search throughput on B200.
 
 One "step" = one full plan search over the workload: every (candidate,
-replica) pair replayed through the GPU engine, SLO counts reduced per
-candidate (NCCL all-reduce across ranks when N > 1), argmax taken.
+replica) pair replayed by the GPU engine, SLO counts reduced per candidate
+(in-library NCCL all-reduce across GPUs when N > 1), argmax taken.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Default workload: C3 (BASELINE.json configs[2], the largest configuration
+that fits one B200 and runs in seconds per search): qwen-32b cost model, all
+169 N=8 plans x 16 hotpotqa 8-round replicas of 50 000 sessions @2/s = 2704
+replays, 6.4 M request-rounds per replica-candidate sweep. At N > 1 the SAME
+search is sharded over the GPUs (strong scaling; pdsim_shard_pairs).
 
 Prints ONE JSON line (rank 0). `value` is whole-job request-rounds/s with
 inputs resident in HBM; `e2e` is the same metric through the host-buffer
-C-ABI call (H2D + kernels + D2H every step).
+C-ABI call (H2D + kernels + D2H every step). `cpu_baseline` is the unmodified
+reference (oracle/_ref) on all host threads over a fixed-seed stratified
+random sample of the pairs (one random replica per candidate), extrapolated
+to the whole search; the same sampled pairs are the line's parity check.
+`secondary.C2` repeats the measurement on C2 (configs[1]).
 """
 import argparse
 import json
 import os
+import random
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2602_14516_b200 import abi, specs  # noqa: E402  (plain data, no library load)
+
 METRIC = "candidate-plan trace replays/sec (request-rounds/sec); planner wall-time"
 UNIT = "request-rounds/s"
+SAMPLE_SEED = 20260217
 
 
 def parse():
@@ -32,26 +45,22 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample-seconds", type=float, default=12.0)
+    ap.add_argument("--secondary", default="C2", help="second config measured in the same line ('none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-argmax-mode", action="store_true")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 def peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(path) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
@@ -65,6 +74,7 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.out = ""
 
     def __enter__(self):
         try:
@@ -76,7 +86,6 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
-        self.out = ""
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -102,268 +111,351 @@ class ClockSampler:
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def shard(n_pairs, rank, world):
-    b = n_pairs * rank // world
-    e = n_pairs * (rank + 1) // world
-    return b, e
+# ---- sampling shared by both arms (plain Python, no library) -----------------
+
+def plan_workers(p):
+    x, y = abi.plan_dict(p)
+    return sum(x.values()) + sum(y.values())
 
 
-def cpu_baseline(wl, seconds, gpu_res=None):
-    """The reference's own CPU path (oracle/_ref, unmodified reference sources)
-    on all host threads over a bounded sample of the workload's pairs. When
-    the GPU result of the same search is given, the sampled pairs double as a
-    parity check of the timed run: per-pair attainment must be identical, and
-    when every pair was sampled, so must the argmax."""
+def heavy_first(pairs, traces, plans):
+    """Pool order for the reference's thread pool: the same cost heuristic as
+    the product's shard planner (rounds x (workers + 2)), heaviest first, so
+    the reference's wall time is not inflated by a long pair starting last."""
+    nt = len(traces)
+    return sorted(pairs, key=lambda p: (-int(traces[p % nt].n_rounds) * (plan_workers(plans[p // nt]) + 2), p))
+
+
+def stratified_sample(n_traces, n_cand, seed=SAMPLE_SEED):
+    """One uniformly random replica per candidate (every pair has inclusion
+    probability 1/n_traces; every candidate shape is covered). Single-replica
+    searches are sampled whole."""
+    if n_traces == 1:
+        return list(range(n_cand))
+    rng = random.Random(seed)
+    return [c * n_traces + rng.randrange(n_traces) for c in range(n_cand)]
+
+
+def rounds_of(wl, pairs):
+    nt = len(wl.traces)
+    return sum(int(wl.traces[p % nt].n_rounds) for p in pairs)
+
+
+def all_rounds(wl):
+    return sum(int(t.n_rounds) for t in wl.traces) * len(wl.plans)
+
+
+def cpu_baseline(wl, gpu_pairs=None):
+    """The reference's own CPU path (oracle/_ref: the unmodified reference
+    run() in a std::thread pool on all host threads) over the stratified
+    sample; extrapolated linearly to the whole search by request-rounds.
+    gpu_pairs (pair -> (status, attainment)) makes the sample the GPU run's
+    parity check: per-pair status and attainment must be identical."""
     from oracle import refbind
     if not refbind.available():
         return None, None
     n_threads = os.cpu_count() or 1
-    pairs = wl.n_pairs
-    t_total, rounds, done = 0.0, 0, 0
-    chunk = max(n_threads, 1)
-    mism = 0
-    sums = [0] * len(wl.plans)
-    bad = [False] * len(wl.plans)
-    while done < pairs and t_total < seconds:
-        e = min(pairs, done + chunk)
-        att, st, wall = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed,
-                                            n_threads=n_threads, pair_begin=done, pair_end=e)
-        if gpu_res is not None:
-            for k in range(e - done):
-                p = done + k
-                c = p // len(wl.traces)
-                g = gpu_res.pair_attainment[p]
-                same = gpu_res.pair_status[p] == st[k] and all(
-                    getattr(g, f) == getattr(att[k], f) for f in ("sessions_total", "sessions_completed", "slo_ok",
-                                                                  "ttft_ok", "itl_ok"))
-                mism += 0 if same else 1
-                if st[k] != 0:
-                    bad[c] = True
-                else:
-                    sums[c] += att[k].slo_ok
-        t_total += wall
-        rounds += wl.rounds_in(done, e)
-        done = e
-    base = {"value": rounds / t_total, "unit": UNIT, "cores": n_threads, "kind": "reference",
-            "sample": f"{done}/{pairs} pairs of {wl.name} (first {done} in enumeration order), "
-                      f"{t_total:.1f} s on {n_threads} threads, std::thread pool over pdsim::run",
-            "replays_per_s": done / t_total}
+    sample = heavy_first(stratified_sample(len(wl.traces), len(wl.plans)), wl.traces, wl.plans)
+    att, st, wall = refbind.plan_search_list(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, sample, n_threads)
+    r_sample, r_all = rounds_of(wl, sample), all_rounds(wl)
+    value = r_sample / wall
+    full = len(sample) == wl.n_pairs
+    base = {"value": value, "unit": UNIT, "cores": n_threads, "kind": "reference",
+            "sample": (f"{len(sample)}/{wl.n_pairs} pairs ({100.0 * len(sample) / wl.n_pairs:.2f} %), "
+                       + ("every pair" if full else f"stratified random: one uniformly random replica per candidate "
+                          f"(seed {SAMPLE_SEED}), all {len(wl.plans)} candidates")
+                       + f"; {wall:.1f} s wall on {n_threads} threads, std::thread pool over pdsim::run"),
+            "extrapolated": not full, "sample_wall_s": wall, "sample_pairs": len(sample),
+            "projected_full_search_s": wall * r_all / r_sample, "replays_per_s": len(sample) / wall}
     parity = None
-    if gpu_res is not None:
-        parity = {"pairs_checked": done, "pairs_total": pairs, "attainment_mismatches": mism,
+    if gpu_pairs is not None:
+        mism, cands = 0, set()
+        sums = [0] * len(wl.plans)
+        bad = [False] * len(wl.plans)
+        for k, p in enumerate(sample):
+            g_st, g = gpu_pairs(p)
+            same = g_st == st[k] and all(getattr(g, f) == getattr(att[k], f) for f in
+                                         ("sessions_total", "sessions_completed", "slo_ok", "ttft_ok", "itl_ok"))
+            mism += 0 if same else 1
+            c = p // len(wl.traces)
+            cands.add(c)
+            if st[k] != 0:
+                bad[c] = True
+            else:
+                sums[c] += att[k].slo_ok
+        parity = {"pairs_checked": len(sample), "pairs_total": wl.n_pairs, "candidates_covered": len(cands),
+                  "attainment_mismatches": mism, "sample": "the cpu_baseline sample",
                   "checker": "oracle/_ref (unmodified reference run())"}
-        if done == pairs:
+        if full:
             key = [(-1 if bad[c] else sums[c], -c) for c in range(len(wl.plans))]
-            ref_best = max(range(len(wl.plans)), key=lambda c: key[c])
-            parity["reference_best_candidate"] = ref_best
-            parity["argmax_identical"] = ref_best == gpu_res.best_candidate
+            parity["reference_best_candidate"] = max(range(len(wl.plans)), key=lambda c: key[c])
     return base, parity
 
 
+# ---- reference arm ------------------------------------------------------------
+
 def run_reference(args, rank, world):
+    """The unmodified reference's CPU plan search (oracle/_ref), inputs built
+    through the reference itself (oracle/ref_workloads.py: its gen_trace,
+    synth_profile and top_k) — no product code is loaded. Each step replays a
+    bounded random sample of the pairs (the next n_threads of a fixed-seed
+    permutation) on all host threads; value = request-rounds / wall."""
     if rank != 0:
         return
-    from paper_2602_14516_b200 import workloads
-    from oracle import refbind
-    # same workload as our arm: at N > 1 the C2 search grows to N replicas
-    wl = workloads.c2(replicas=world) if (args.config == "C2" and world > 1) else workloads.CONFIGS[args.config]()
+    from oracle import ref_workloads, refbind
+    spec = specs.SPECS[args.config]()
+    wl = ref_workloads.build(spec)
     n_threads = os.cpu_count() or 1
-    # each step = a bounded sample of the pairs (~10 s of CPU work at most)
-    probe_end = min(wl.n_pairs, n_threads)
-    _, _, w0 = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, n_threads, 0, probe_end)
-    per_pair = w0 / probe_end * n_threads
-    step_pairs = int(max(n_threads, min(wl.n_pairs, 8.0 * n_threads / max(per_pair, 1e-6))))
+    perm = list(range(wl.n_pairs))
+    random.Random(SAMPLE_SEED).shuffle(perm)
+    # three pairs per thread per step, heaviest first, so the pool's wall time
+    # is not one long pair with idle threads (a bias against the reference)
+    step_pairs = min(wl.n_pairs, 3 * n_threads) if wl.n_pairs > 4 * n_threads else wl.n_pairs
+    cursor = 0
+
+    def take(n):
+        nonlocal cursor
+        out = [perm[(cursor + k) % wl.n_pairs] for k in range(n)]
+        cursor += n
+        return heavy_first(out, wl.traces, wl.plans)
+
     for _ in range(args.warmup):
-        refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, n_threads, 0,
-                            min(step_pairs, n_threads))
-    total_t, total_rounds, cursor = 0.0, 0, 0
+        refbind.plan_search_list(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, take(min(step_pairs, n_threads)),
+                                 n_threads)
+    total_t, total_rounds, total_pairs = 0.0, 0, 0
     for _ in range(args.steps):
-        b = cursor % wl.n_pairs
-        e = min(wl.n_pairs, b + step_pairs)
-        _, _, wall = refbind.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, n_threads, b, e)
+        pairs = take(step_pairs)
+        _, _, wall = refbind.plan_search_list(wl.traces, wl.plans, wl.profile, wl.params, wl.seed, pairs, n_threads)
         total_t += wall
-        total_rounds += wl.rounds_in(b, e)
-        cursor = e
+        total_rounds += sum(wl.rounds_of_pair(p) for p in pairs)
+        total_pairs += len(pairs)
     v = total_rounds / total_t
+    full = step_pairs == wl.n_pairs
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference gen_trace presets, host RNG)",
-            "config": {"workload": wl.desc, "config": wl.name, "pairs": wl.n_pairs,
-                       "step_sample_pairs": step_pairs},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference gen_trace presets on the reference's own RNG; synth_profile seed 7)",
+            "config": specs.config_dict(spec),
+            "planner_wall_s_projected": total_t / total_rounds * (sum(int(t.n_rounds) for t in wl.traces) * len(wl.plans)),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": n_threads, "kind": "reference",
-                             "sample": f"{step_pairs} pairs per step of {wl.n_pairs}"},
+                             "sample": (f"{step_pairs} pairs per step" + (" (every pair)" if full else
+                                        f" of {wl.n_pairs}: consecutive slices of a fixed-seed random permutation "
+                                        f"({total_pairs} distinct-or-wrapped pairs timed, extrapolated)"))},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank, world, local):
+# ---- our arm ------------------------------------------------------------------
+
+def measure(ctx, wl, pairs, args, stream, flush, world, steps, warmup, clock_index=None):
+    """Warm-up, then `steps` timed searches of `pairs` with inputs resident;
+    L2 flushed before each. Returns (per-step ms list, kernel ms list,
+    launches, last result, clock summary)."""
     import torch
-    import torch.distributed as dist
-    from paper_2602_14516_b200 import abi, native, workloads
-
-    # PDSIM_BENCH_SHARED_GPU=1 (functional check of the N > 1 path on a
-    # one-GPU box only): ranks share the visible GPUs and reduce over gloo.
-    # Never used for a reported number: NCCL over one GPU per rank is the path.
-    shared = os.environ.get("PDSIM_BENCH_SHARED_GPU") == "1"
-    if shared:
-        local = local % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(local)
+    for _ in range(warmup):
+        ctx.search_staged_list(wl.seed, pairs)
     if world > 1:
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # N > 1: weak scaling over trace replicas. The workload grows to N
-    # replicas of the trace; rank r replays every candidate on replica r
-    # (no data-path communication), and the per-candidate SLO counts are
-    # summed over replicas by the one collective before the argmax.
-    if args.config == "C2" and world > 1:
-        wl = workloads.c2(replicas=world)
-    else:
-        wl = workloads.CONFIGS[args.config]()
-    n_pairs = wl.n_pairs
-    if len(wl.traces) == world and world > 1:
-        my_traces = [wl.traces[rank]]
-        b, e = 0, len(wl.plans)
-        my_bytes = (24 * wl.traces[rank].n_rounds + 16 * wl.traces[rank].n_sessions) * len(wl.plans)
-    else:
-        my_traces = wl.traces
-        b, e = shard(n_pairs, rank, world)
-        my_bytes = wl.input_bytes(b, e)
-    stream = torch.cuda.current_stream()
-    ctx = native.Context(local)
-    ctx.set_stream(stream.cuda_stream)
-    ctx.stage(my_traces, wl.plans, wl.profile, wl.params)
-    C = len(wl.plans)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
-
-    def step(staged=True):
-        res = ctx.search_staged(wl.seed, b, e) if staged else ctx.plan_search(
-            my_traces, wl.plans, wl.profile, wl.params, wl.seed, b, e)
-        if world == 1:  # the library's own device argmax (argmax_kernel)
-            return res, res.best_candidate, res.best_slo_ok
-        cand = torch.tensor([res.candidate_slo_ok[c] for c in range(C)], dtype=torch.int64, device="cuda")
-        bad = (cand < 0).to(torch.int64)
-        cnt = torch.clamp(cand, min=0)
-        if world > 1:  # the one collective: per-candidate counts over NVLink
-            dist.all_reduce(cnt)
-            dist.all_reduce(bad, op=dist.ReduceOp.MAX)
-        key = torch.where(bad > 0, torch.full_like(cnt, -1), cnt)
-        best = int(torch.argmax(key).item())  # first max = smallest index
-        return res, best, int(key[best].item())
-
-    for _ in range(args.warmup):
-        step()
-    if world > 1:
+        import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    times, kernel_ms, launches = [], [], 0
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+    times, kernel_ms, launches, res = [], [], 0, None
+    sampler = ClockSampler(clock_index) if clock_index is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        for _ in range(steps):
             flush.zero_()
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            res, best, best_cnt = step()
+            res = ctx.search_staged_list(wl.seed, pairs)
             ev1.record(stream)
             torch.cuda.synchronize()
             times.append(ev0.elapsed_time(ev1))
             kernel_ms.append(res.kernel_ms)
             launches += res.kernel_launches
-    my_ms = sum(times)
-    t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    rounds_all = wl.rounds_in(0, n_pairs)
-    value = rounds_all * args.steps / (total_ms / 1e3)
+    finally:
+        if sampler:
+            sampler.__exit__()
+    return times, kernel_ms, launches, res, (sampler.summary() if sampler else None)
 
-    # e2e: host buffers through the public C-ABI call (H2D + kernels + D2H)
+
+def max_over_ranks(x, world):
+    import torch
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2602_14516_b200 import native, workloads
+
+    # PDSIM_BENCH_SHARED_GPU=1 (functional check of the N > 1 path on a
+    # one-GPU box only): ranks share the visible GPU; never a reported number.
+    shared = os.environ.get("PDSIM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo" if shared else "nccl", device_id=None if shared else torch.device("cuda", local))
+    spec = specs.SPECS[args.config]()
+    wl = workloads.build(spec)
+    stream = torch.cuda.current_stream()
+    ctx = native.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.stage(wl.traces, wl.plans, wl.profile, wl.params)
+    if world > 1:
+        # the one collective: per-candidate counts all-reduced over NCCL by
+        # the library itself, at the end of every search (pdsim_gpu_comm_init)
+        obj = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(world, rank, obj[0])
+        ctx.set_global_sessions(sum(int(t.n_sessions) for t in wl.traces))
+    # this GPU's shard of the SAME search, heaviest pairs first
+    pairs = native.shard_pairs(wl.traces, wl.plans, world, rank)
+    C = len(wl.plans)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    times, kernel_ms, launches, res, clocks = measure(ctx, wl, pairs, args, stream, flush, world, args.steps,
+                                                      args.warmup, clock_index=local)
+    total_ms = max_over_ranks(sum(times), world)
+    rounds_all = all_rounds(wl)
+    value = rounds_all * args.steps / (total_ms / 1e3)
+    best, best_cnt = res.best_candidate, res.best_slo_ok
+
+    # e2e: host buffers through the public C-ABI call every step — stage
+    # (pack + H2D) + replay + reduction + D2H.
     e2e_ms, h2d, d2h = [], 0, 0
-    for _ in range(max(2, min(args.steps, 3))):
+    for _ in range(2):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res_e, _, _ = step(staged=False)
+        if world == 1:
+            r_e = ctx.plan_search(wl.traces, wl.plans, wl.profile, wl.params, wl.seed)
+            h2d = r_e.h2d_bytes
+        else:
+            ctx.stage(wl.traces, wl.plans, wl.profile, wl.params)
+            r_e = ctx.search_staged_list(wl.seed, pairs)
+            # packed trace arrays staged per rank (pack.hpp: f64 arrival, i32
+            # round offsets, i32 incr / decode, f64 delay, i64 id, i32 ranks)
+            # + the pair list
+            h2d = sum(28 * int(t.n_sessions) + 4 + 16 * int(t.n_rounds) for t in wl.traces) + r_e.h2d_bytes
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        h2d, d2h = res_e.h2d_bytes, res_e.d2h_bytes
-    te = torch.tensor([statistics.median(e2e_ms)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = rounds_all / (float(te.item()) / 1e3)
+        d2h = r_e.d2h_bytes
+        assert r_e.best_candidate == best and r_e.best_slo_ok == best_cnt
+    te = max_over_ranks(statistics.median(e2e_ms), world)
+    e2e_value = rounds_all / (te / 1e3)
 
-    # Search mode ARGMAX (exact pruning, include/pdsim_gpu.h): same plan and
-    # count, fewer replays; reported beside the full-replay headline, which
-    # alone defines `value`.
+    # Search mode ARGMAX (exact pruning): same plan and count, fewer replays;
+    # reported beside the full-replay headline, which alone defines `value`.
     arg = None
-    if world == 1:
+    if world == 1 and not args.no_argmax_mode and C > 1:
         ctx.set_search_mode(abi.SEARCH_ARGMAX)
         am = []
-        for _ in range(max(2, min(args.steps, 3))):
+        for _ in range(2):
             flush.zero_()
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
-            res_a = ctx.search_staged(wl.seed, b, e)
+            res_a = ctx.search_staged_list(wl.seed, pairs)
             ev1.record(stream)
             torch.cuda.synchronize()
             am.append(ev0.elapsed_time(ev1))
         ctx.set_search_mode(abi.SEARCH_FULL)
         arg = {"planner_wall_ms": statistics.median(am), "best_candidate": res_a.best_candidate,
-               "best_slo_ok": res_a.best_slo_ok, "same_plan_as_full": res_a.best_candidate == best and
-               res_a.best_slo_ok == best_cnt,
+               "best_slo_ok": res_a.best_slo_ok,
+               "same_plan_as_full": res_a.best_candidate == best and res_a.best_slo_ok == best_cnt,
                "pruned_candidates": sum(1 for c in range(C) if res_a.candidate_slo_ok[c] == -2)}
 
-    # roofline of the dominant kernel (replay_kernel): algorithmic input bytes
-    # per launch (24 B/round + 16 B/session per pair of this shard) / its
-    # average CUDA-event duration.
+    # Roofline of the dominant kernel (replay_kernel): algorithmic input bytes
+    # per launch (24 B/round + 16 B/session for every pair of this shard,
+    # SURVEY.md §8(d)) / its average CUDA-event duration.
     peak, peak_src = peaks()
-    bytes_launch = my_bytes
+    nt = len(wl.traces)
+    bytes_launch = sum(24 * int(wl.traces[p % nt].n_rounds) + 16 * int(wl.traces[p % nt].n_sessions) for p in pairs)
     avg_k = statistics.mean(kernel_ms)
     achieved = bytes_launch / (avg_k / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{wl.name}.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1:
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            t = json.load(open(tp))
+            if t.get("config_desc") == spec.desc:
+                traffic = t.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
+    pos = {p: k for k, p in enumerate(pairs)}
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, parity = cpu_baseline(wl, args.cpu_sample_seconds, gpu_res=res)
+        cpu, parity = cpu_baseline(wl, lambda p: (res.pair_status[pos[p]], res.pair_attainment[pos[p]]))
+        if parity is not None and "reference_best_candidate" in parity:
+            parity["argmax_identical"] = parity["reference_best_candidate"] == best
+
+    secondary = {}
+    if world == 1 and args.secondary and args.secondary.lower() != "none" and args.secondary != args.config:
+        s_spec = specs.SPECS[args.secondary]()
+        swl = workloads.build(s_spec)
+        ctx.stage(swl.traces, swl.plans, swl.profile, swl.params)
+        spairs = native.shard_pairs(swl.traces, swl.plans, 1, 0)
+        s_times, s_kms, s_launches, s_res, _ = measure(ctx, swl, spairs, args, stream, flush, 1, 3, 1)
+        s_rounds = all_rounds(swl)
+        se = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r_se = ctx.plan_search(swl.traces, swl.plans, swl.profile, swl.params, swl.seed)
+            torch.cuda.synchronize()
+            se.append((time.perf_counter() - t0) * 1e3)
+        entry = {"config": specs.config_dict(s_spec), "value": s_rounds * len(s_times) / (sum(s_times) / 1e3),
+                 "unit": UNIT, "ms_per_step": statistics.mean(s_times), "kernel_ms": statistics.mean(s_kms),
+                 "e2e": {"value": s_rounds / (statistics.median(se) / 1e3), "unit": UNIT,
+                         "h2d_bytes_per_step": r_se.h2d_bytes, "d2h_bytes_per_step": r_se.d2h_bytes},
+                 "best_candidate": s_res.best_candidate, "best_slo_ok": s_res.best_slo_ok, "steps": len(s_times)}
+        if not args.no_cpu_baseline:
+            spos = {p: k for k, p in enumerate(spairs)}
+            scpu, spar = cpu_baseline(swl, lambda p: (s_res.pair_status[spos[p]], s_res.pair_attainment[spos[p]]))
+            if scpu:
+                entry["cpu_baseline"] = scpu
+            if spar:
+                if "reference_best_candidate" in spar:
+                    spar["argmax_identical"] = spar["reference_best_candidate"] == s_res.best_candidate
+                entry["parity"] = spar
+        secondary[args.secondary] = entry
+        launches_secondary = s_launches  # noqa: F841  (not part of the headline's timed region)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": ("weak" if len(wl.traces) == world else "strong") if world > 1 else "strong",
-            "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference gen_trace presets on the host RNG; synth_profile seed 7)",
-            "config": {"workload": wl.desc, "config": wl.name, "model_cost": wl.model, "pairs": n_pairs,
-                       "candidates": C, "replicas": len(wl.traces),
-                       "sessions": [int(x.n_sessions) for x in wl.traces][:4],
-                       "parallelism": (f"one trace replica per GPU ({world} GPUs), counts all-reduced"
-                                       if len(wl.traces) == world and world > 1
-                                       else f"pairs sharded over {world} GPU(s)"),
-                       "l2": "flushed between timed steps (256 MiB write)"},
-            "replays_per_s": n_pairs * args.steps / (total_ms / 1e3),
+            "config": specs.config_dict(spec),
+            "parallelism": (f"the same search sharded over {world} GPUs (cost-aware LPT split, pdsim_shard_pairs); "
+                            "per-candidate counts all-reduced in-library over NCCL" if world > 1 else
+                            "1 GPU, pairs in cost order (persistent kernel, atomic queue)"),
+            "replays_per_s": wl.n_pairs * args.steps / (total_ms / 1e3),
             "planner_wall_ms": total_ms / args.steps,
             "kernel_ms": avg_k,
             "best_candidate": best, "best_slo_ok": best_cnt,
+            "best_plan": abi.format_plan(wl.plans[best]) if best >= 0 else None,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_launch": bytes_launch, "kernel": "replay_kernel"},
+                         "bytes_per_launch": bytes_launch, "kernel": "replay_kernel",
+                         "note": "latency-bound serial DES per pair; see DESIGN.md §5 for issue/stall figures"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": float(te.item())},
-            "clocks": clk.summary(),
+                    "ms_per_step": te},
+            "clocks": clocks,
         }
         if arg:
             line["argmax_mode"] = arg
@@ -371,9 +463,12 @@ def run_ours(args, rank, world, local):
             line["cpu_baseline"] = cpu
         if parity:
             line["parity"] = parity
+        if secondary:
+            line["secondary"] = secondary
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

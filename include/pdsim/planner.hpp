@@ -69,4 +69,10 @@ std::vector<DeploymentPlan> top_k(const LatencyCoefficients& coeffs, int total_g
 
 std::string format_plan(const DeploymentPlan& plan);  // "P:<TP=4, DP=2>, D:<TP=8, DP=1>"
 
+// plan_v1 JSON (planner.hpp:108-113). Canonical: plan_to_json(plan_from_json(
+// plan_to_json(p))) == plan_to_json(p). plan_from_json throws ParseError.
+std::string plan_to_json(const DeploymentPlan& plan);
+DeploymentPlan plan_from_json(const std::string& text);
+std::string coefficients_to_json(const LatencyCoefficients& coeffs);
+
 }  // namespace pdsim

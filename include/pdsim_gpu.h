@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PDSIM_ABI_VERSION 2
+#define PDSIM_ABI_VERSION 3
 
 #define PDSIM_MAX_DEGREES 8     /* profile degree set size */
 #define PDSIM_MAX_BREAKPOINTS 7 /* per piecewise curve; segments = bps + 1 */
@@ -370,9 +370,60 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
  * pairs report PDSIM_PAIR_PRUNED and pruned candidates candidate_slo_ok = -2.
  * Record/report searches always run FULL. Sharded callers reduce
  * candidate_slo_ok with the same rule as invalid candidates (any negative
- * excludes the candidate): the global argmax is never pruned on any shard. */
+ * excludes the candidate): the global argmax is never pruned on any shard,
+ * PROVIDED the upper bound counts the sessions of the whole search — a shard
+ * that stages only some replicas must declare the global total with
+ * pdsim_gpu_set_global_sessions(), or it would prune a candidate that merely
+ * loses on its own replicas. */
 enum { PDSIM_SEARCH_FULL = 0, PDSIM_SEARCH_ARGMAX = 1 };
 int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode);
+/* Sessions of every replica of the search this context is a shard of (0 =
+ * the staged replicas are the whole search). Used only by ARGMAX bounds. */
+int pdsim_gpu_set_global_sessions(pdsim_gpu_ctx* ctx, int64_t total_sessions);
+
+/* ---- multi-GPU (replaces the reference's serial sweep
+ * loop pdsim.cpp:547-586 over run() calls, sim_engine.cpp:676-681) -------- */
+
+/* Cost-aware shard of the pairs c * n_traces + r over `world` GPUs: pair cost
+ * rounds(r) x (workers(c) + 2), longest first, each to the least-loaded rank
+ * (deterministic; every rank computes the same split without communicating).
+ * Writes rank's pairs in queue order (heaviest first) to out[0..capacity) and
+ * returns their count (-1 on bad arguments). */
+int64_t pdsim_shard_pairs(int32_t n_traces, const int64_t* trace_rounds,
+                          int32_t n_candidates, const pdsim_plan* candidates,
+                          int32_t world, int32_t rank, int64_t* out,
+                          int64_t capacity);
+
+/* Replays the staged pairs listed in `pairs` (global indices, no duplicates)
+ * in list order: the persistent kernel's queue hands them out in that order.
+ * Per-pair outputs follow the list; per-candidate outputs cover the pairs
+ * replayed (or, with a communicator, the whole sharded search). */
+int pdsim_gpu_search_staged_list(pdsim_gpu_ctx* ctx, const int64_t* pairs,
+                                 int64_t n_pairs, uint64_t seed,
+                                 pdsim_search_output* out);
+
+/* NCCL (loaded at first use from the process's libnccl.so.2). One process per
+ * GPU: rank 0 calls pdsim_nccl_unique_id(), the caller broadcasts the 128
+ * bytes, every rank calls pdsim_gpu_comm_init(). From then on every search
+ * of the context ends with the only collective of the path: an in-place
+ * ncclAllReduce of the per-candidate counts (sum, uint64) and flags (max)
+ * on the search's stream, then the argmax — candidate_slo_ok, best_candidate
+ * and best_slo_ok describe the whole sharded search on every rank. */
+int pdsim_nccl_unique_id(uint8_t id[128]);
+int pdsim_gpu_comm_init(pdsim_gpu_ctx* ctx, int32_t world, int32_t rank,
+                        const uint8_t id[128]);
+
+/* One host thread driving several GPUs of this process: stages the whole
+ * search on every device, shards it with pdsim_shard_pairs, replays the
+ * shards concurrently and all-reduces the counts over a communicator made by
+ * ncclCommInitAll. Outputs are indexed by global pair like
+ * pdsim_gpu_plan_search (the pair range must be the whole search);
+ * kernel_ms / device_ms are the maximum over devices. */
+int pdsim_multi_plan_search(int32_t n_devices, const int32_t* devices,
+                            const pdsim_search_input* in,
+                            const pdsim_profile* profile,
+                            const pdsim_sched_params* params, uint64_t seed,
+                            int32_t search_mode, pdsim_search_output* out);
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable);
 int pdsim_gpu_profile_counters(const pdsim_gpu_ctx* ctx, int64_t* cycles, int64_t* counts,
                                int64_t* replayed);

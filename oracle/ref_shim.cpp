@@ -259,6 +259,41 @@ int ref_synth_profile(const pdsim_synth_spec* spec, uint64_t seed, pdsim_profile
   });
 }
 
+// The reference's default SynthProfileSpec (perf_model.hpp:110-139) as POD.
+int ref_synth_spec_default(pdsim_synth_spec* out) {
+  return guarded([&] {
+    const pdsim::SynthProfileSpec s;
+    std::memset(out, 0, sizeof(*out));
+    if (s.degrees.size() > PDSIM_MAX_DEGREES || s.prefill_breakpoints.size() > PDSIM_MAX_BREAKPOINTS ||
+        s.decode_breakpoints.size() > PDSIM_MAX_BREAKPOINTS) {
+      throw pdsim::ConfigError("synth spec default exceeds the POD capacity");
+    }
+    out->n_degrees = static_cast<int32_t>(s.degrees.size());
+    for (std::size_t i = 0; i < s.degrees.size(); ++i) out->degrees[i] = s.degrees[i];
+    out->prefill_alpha_min = s.prefill_alpha_min;
+    out->prefill_alpha_max = s.prefill_alpha_max;
+    out->prefill_beta_min = s.prefill_beta_min;
+    out->prefill_beta_max = s.prefill_beta_max;
+    out->n_prefill_breakpoints = static_cast<int32_t>(s.prefill_breakpoints.size());
+    for (std::size_t i = 0; i < s.prefill_breakpoints.size(); ++i) out->prefill_breakpoints[i] = s.prefill_breakpoints[i];
+    out->decode_alpha_min = s.decode_alpha_min;
+    out->decode_alpha_max = s.decode_alpha_max;
+    out->decode_beta_min = s.decode_beta_min;
+    out->decode_beta_max = s.decode_beta_max;
+    out->n_decode_breakpoints = static_cast<int32_t>(s.decode_breakpoints.size());
+    for (std::size_t i = 0; i < s.decode_breakpoints.size(); ++i) out->decode_breakpoints[i] = s.decode_breakpoints[i];
+    out->segment_growth_min = s.segment_growth_min;
+    out->segment_growth_max = s.segment_growth_max;
+    out->scaling_exponent = s.scaling_exponent;
+    out->kv_bandwidth_bytes_per_sec = s.kv_bandwidth_bytes_per_sec;
+    out->kv_latency_seconds = s.kv_latency_seconds;
+    out->kv_reshard_penalty = s.kv_reshard_penalty;
+    out->kv_bytes_per_token = s.kv_bytes_per_token;
+    out->gpu_memory_capacity = s.gpu_memory_capacity;
+    out->history_weight = s.history_weight;
+  });
+}
+
 uint64_t ref_profile_hash(const pdsim_profile* p) {
   try {
     return fnv1a(pdsim::save_profile(profile_from_pod(*p)));
@@ -424,9 +459,12 @@ int ref_run(const pdsim_trace* tr, const pdsim_plan* plan, const pdsim_profile* 
 // n_traces + r) from an atomic counter and calls pdsim::run on each. Traces,
 // plans and the profile are converted to reference types before the clock
 // starts; *wall_s covers the pool only. A ConfigError marks the pair invalid.
-int ref_plan_search(const pdsim_search_input* in, const pdsim_profile* prof,
-                    const pdsim_sched_params* params, uint64_t seed, int32_t n_threads,
-                    pdsim_attainment* pair_att, int8_t* pair_status, double* wall_s) {
+// Pair k of the pool is pairs[k] when `pairs` is given (a sample of the
+// search, outputs indexed by k), else pair_begin + k.
+static int plan_search_impl(const pdsim_search_input* in, const pdsim_profile* prof,
+                            const pdsim_sched_params* params, uint64_t seed, int32_t n_threads,
+                            const int64_t* pairs, int64_t n_pairs, pdsim_attainment* pair_att,
+                            int8_t* pair_status, double* wall_s) {
   return guarded([&] {
     std::vector<pdsim::Trace> traces;
     for (int i = 0; i < in->n_traces; ++i) traces.push_back(trace_from_pod(in->traces[i]));
@@ -435,13 +473,14 @@ int ref_plan_search(const pdsim_search_input* in, const pdsim_profile* prof,
     const pdsim::PerfProfile profile = profile_from_pod(*prof);
     const pdsim::SchedulerParams sp = params_from_pod(*params);
     const int64_t total = static_cast<int64_t>(in->n_traces) * in->n_candidates;
-    const int64_t b = in->pair_begin;
-    const int64_t e = in->pair_end < 0 ? total : in->pair_end;
+    const int64_t b = pairs ? 0 : in->pair_begin;
+    const int64_t e = pairs ? n_pairs : (in->pair_end < 0 ? total : in->pair_end);
     std::atomic<int64_t> next{b};
     auto worker = [&] {
       for (;;) {
-        const int64_t p = next.fetch_add(1);
-        if (p >= e) return;
+        const int64_t k = next.fetch_add(1);
+        if (k >= e) return;
+        const int64_t p = pairs ? pairs[k] : k;
         const int c = static_cast<int>(p / in->n_traces);
         const int r = static_cast<int>(p % in->n_traces);
         pdsim_attainment a{};
@@ -454,8 +493,8 @@ int ref_plan_search(const pdsim_search_input* in, const pdsim_profile* prof,
         } catch (...) {
           st = PDSIM_PAIR_ERROR;
         }
-        if (pair_att) pair_att[p - b] = a;
-        if (pair_status) pair_status[p - b] = st;
+        if (pair_att) pair_att[k - b] = a;
+        if (pair_status) pair_status[k - b] = st;
       }
     };
     const int nt = n_threads > 0 ? n_threads
@@ -467,6 +506,21 @@ int ref_plan_search(const pdsim_search_input* in, const pdsim_profile* prof,
     const auto t1 = std::chrono::steady_clock::now();
     if (wall_s) *wall_s = std::chrono::duration<double>(t1 - t0).count();
   });
+}
+
+int ref_plan_search(const pdsim_search_input* in, const pdsim_profile* prof,
+                    const pdsim_sched_params* params, uint64_t seed, int32_t n_threads,
+                    pdsim_attainment* pair_att, int8_t* pair_status, double* wall_s) {
+  return plan_search_impl(in, prof, params, seed, n_threads, nullptr, 0, pair_att, pair_status, wall_s);
+}
+
+// The same pool over an explicit list of pairs (bench.py's sampled CPU
+// baseline); the pool pulls them in list order.
+int ref_plan_search_list(const pdsim_search_input* in, const pdsim_profile* prof,
+                         const pdsim_sched_params* params, uint64_t seed, int32_t n_threads,
+                         const int64_t* pairs, int64_t n_pairs, pdsim_attainment* pair_att,
+                         int8_t* pair_status, double* wall_s) {
+  return plan_search_impl(in, prof, params, seed, n_threads, pairs, n_pairs, pair_att, pair_status, wall_s);
 }
 
 // Every plan top_k ranks (k = capacity), in plan_ranks_before order — used to

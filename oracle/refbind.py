@@ -45,6 +45,9 @@ def lib():
                               P(C.c_double), P(C.c_int64)]
         L.ref_plan_search.argtypes = [P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams), C.c_uint64,
                                       C.c_int32, P(abi.Attainment), P(C.c_int8), P(C.c_double)]
+        L.ref_plan_search_list.argtypes = [P(abi.SearchInput), P(abi.Profile), P(abi.SchedParams), C.c_uint64,
+                                           C.c_int32, P(C.c_int64), C.c_int64, P(abi.Attainment), P(C.c_int8),
+                                           P(C.c_double)]
         L.ref_top_k_plans.argtypes = [P(C.c_int32), C.c_int32, C.c_int32, P(abi.Plan), C.c_int64]
         L.ref_top_k_plans.restype = C.c_int64
         L.ref_phase_sims.argtypes = [P(abi.Trace), P(abi.Profile), C.c_int32, P(abi.PhaseResult),
@@ -162,6 +165,22 @@ def plan_search(traces, plans, profile, params, seed, n_threads=0, pair_begin=0,
     wall = C.c_double(0)
     _check(lib().ref_plan_search(C.byref(inp), C.byref(profile), C.byref(params), seed, n_threads, att, st,
                                  C.byref(wall)))
+    return att, st, wall.value
+
+
+def plan_search_list(traces, plans, profile, params, seed, pairs, n_threads=0):
+    """The reference pool over an explicit pair list (pulled in list order).
+    Returns (att, status, wall_s) indexed like `pairs`."""
+    tarr = (abi.Trace * len(traces))(*traces)
+    parr = (abi.Plan * len(plans))(*plans)
+    inp = abi.SearchInput(len(traces), len(plans), tarr, parr, 0, -1)
+    n = len(pairs)
+    pl = (C.c_int64 * max(n, 1))(*pairs)
+    att = (abi.Attainment * max(n, 1))()
+    st = (C.c_int8 * max(n, 1))()
+    wall = C.c_double(0)
+    _check(lib().ref_plan_search_list(C.byref(inp), C.byref(profile), C.byref(params), seed, n_threads, pl, n,
+                                      att, st, C.byref(wall)))
     return att, st, wall.value
 
 

@@ -16,15 +16,20 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.cuh"
+#include "nccl_dl.hpp"
 #include "pack.hpp"
+#include "shard.hpp"
 #include "planner.cuh"
 #include "replay.cuh"
 #include "pdsim_gpu.h"
@@ -83,6 +88,10 @@ struct pdsim_gpu_ctx {
   DevBuf d_trace_data, d_traces, d_plans, d_invalid, d_cand_params, d_cand_inv;
   std::vector<int8_t> cand_invalid;  // [n_candidates]: some pair of c is invalid (whole search)
   int64_t total_sessions = 0;        // sum of S over the staged traces
+  int64_t global_sessions = 0;       // > 0: sum of S over every replica of a sharded search (argmax bounds)
+  DevBuf d_pair_list;                // launch pair list (sharded / cost-ordered searches)
+  ncclComm_t comm = nullptr;         // set: every search all-reduces its candidate counts over it
+  int32_t comm_world = 1, comm_rank = 0;
   int search_mode = 0;               // PDSIM_SEARCH_*
   DevBuf d_pair_fail, d_pair_ok, d_best_key;  // argmax mode (pruning) state
   // per-search buffers
@@ -142,6 +151,81 @@ __global__ void argmax_kernel(const unsigned long long* cand_sum, const int* can
     unsigned long long k = 0;
     for (int w = 0; w < static_cast<int>((blockDim.x + 31) / 32); ++w) k = warp_best[w] > k ? warp_best[w] : k;
     *best = k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The cost model lives in one __constant__ bank per module (engine.cuh
+// c_profile): every context on a device shares it. A context uploads its
+// profile and launches under a per-device lease; leases on the same profile
+// run concurrently, a different profile waits until the device's running
+// searches have finished, then replaces the bank. The lease ends after the
+// search's stream synchronisation, so a kernel never sees another context's
+// cost model.
+struct ProfileGate {
+  std::mutex m;
+  std::condition_variable cv;
+  bool loaded = false;
+  pdsim_profile cur{};
+  int active = 0;
+};
+
+ProfileGate& profile_gate(int device) {
+  static ProfileGate gates[64];
+  return gates[device & 63];
+}
+
+class ProfileLease {
+ public:
+  explicit ProfileLease(pdsim_gpu_ctx* ctx) : ctx_(ctx) {}
+  ProfileLease(const ProfileLease&) = delete;
+  ProfileLease& operator=(const ProfileLease&) = delete;
+  cudaError_t acquire();
+  ~ProfileLease();
+
+ private:
+  pdsim_gpu_ctx* ctx_;
+  bool held_ = false;
+};
+
+cudaError_t ProfileLease::acquire() {
+  ProfileGate& g = profile_gate(ctx_->device);
+  std::unique_lock<std::mutex> lk(g.m);
+  auto same = [&] { return g.loaded && memcmp(&g.cur, &ctx_->profile, sizeof(pdsim_profile)) == 0; };
+  g.cv.wait(lk, [&] { return g.active == 0 || same(); });
+  if (!same()) {
+    cudaError_t e = pdg::replay_set_profile(&ctx_->profile, ctx_->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx_->stream);
+    if (e != cudaSuccess) {
+      g.loaded = false;
+      return e;
+    }
+    g.cur = ctx_->profile;
+    g.loaded = true;
+  }
+  ++g.active;
+  held_ = true;
+  return cudaSuccess;
+}
+
+ProfileLease::~ProfileLease() {
+  if (!held_) return;
+  cudaStreamSynchronize(ctx_->stream);  // error paths: the kernel must be done before the bank may change
+  ProfileGate& g = profile_gate(ctx_->device);
+  {
+    std::lock_guard<std::mutex> lk(g.m);
+    --g.active;
+  }
+  g.cv.notify_all();
+}
+
+// Candidate flags before the cross-GPU max-reduction: bit 0 = invalid on
+// this GPU, bit 1 = pruned here. Invalid anywhere must win over pruned, so
+// invalid becomes 3 (both bits): max() then keeps bit 0 whenever any rank
+// saw the candidate invalid, and bit 1 alone means pruned somewhere.
+__global__ void flags_for_max_kernel(int* cand_bad, int n) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    if (cand_bad[c] & 1) cand_bad[c] = 3;
   }
 }
 
@@ -218,6 +302,10 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
       ctx->cand_invalid[static_cast<size_t>(c)] |= ctx->pair_invalid[static_cast<size_t>(c) * in->n_traces + r];
   ctx->total_sessions = 0;
   for (const auto& t : ctx->packed) ctx->total_sessions += t.S;
+  // Argmax / pruning keys pack (count + 1) into 32 bits (argmax_kernel).
+  if (ctx->total_sessions >= static_cast<int64_t>(0xfffffffeLL)) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "search: the replicas hold 2^32-2 or more sessions (argmax key range)");
+  }
 
   std::vector<const pdg::PackedTrace*> tp;
   for (auto& t : ctx->packed) tp.push_back(&t);
@@ -290,7 +378,6 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
     CU(ctx, cudaMemcpyAsync(ctx->d_cand_params.p, ctx->cand_params.data(),
                             sizeof(pdg::DevParams) * ctx->cand_params.size(), cudaMemcpyHostToDevice, ctx->stream));
   }
-  CU(ctx, pdg::replay_set_profile(profile, ctx->stream));
   CU(ctx, cudaStreamSynchronize(ctx->stream));
   if (h2d_bytes) {
     *h2d_bytes = static_cast<int64_t>(off + sizeof(pdg::DevTrace) * dt.size() +
@@ -302,12 +389,25 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
 }
 
 // Replays pairs [b, e) of the staged inputs; results land in host buffers.
+// With `list` (n_list entries), the launch replays those pairs in list order
+// instead of the range; per-pair outputs follow the list.
 int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_search_output* out,
-                pdg::Records rec, pdg::PairResult* single_result) {
+                pdg::Records rec, pdg::PairResult* single_result, const int64_t* list = nullptr,
+                int64_t n_list = 0) {
   if (!ctx->staged) return set_err(ctx, PDSIM_ERR_CONFIG, "search: nothing staged");
   const int64_t total = static_cast<int64_t>(ctx->n_traces) * ctx->n_candidates;
+  if (list) {
+    if (n_list < 0) return set_err(ctx, PDSIM_ERR_CONFIG, "search: negative pair-list length");
+    std::vector<uint8_t> seen(static_cast<size_t>(total), 0);
+    for (int64_t k = 0; k < n_list; ++k) {
+      if (list[k] < 0 || list[k] >= total) return set_err(ctx, PDSIM_ERR_CONFIG, "search: pair index out of range");
+      if (seen[static_cast<size_t>(list[k])]++) return set_err(ctx, PDSIM_ERR_CONFIG, "search: duplicate pair in list");
+    }
+    b = 0;
+    e = n_list;
+  }
   if (e < 0) e = total;
-  if (b < 0 || b > e || e > total) return set_err(ctx, PDSIM_ERR_CONFIG, "search: bad pair range");
+  if (b < 0 || b > e || (!list && e > total)) return set_err(ctx, PDSIM_ERR_CONFIG, "search: bad pair range");
   const int64_t n = e - b;
   const int C = ctx->n_candidates;
   // Report mode widens the global workspace layout (the shared-memory layout
@@ -318,7 +418,15 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     int32_t max_r = 1;
     for (const auto& t : ctx->packed) max_r = std::max(max_r, t.R);
     caps.rep_r = max_r;
-    caps.rep_gapcap = 1 << 16;
+    // Distinct ITL gaps <= decode steps <= decode tokens: 2x the largest
+    // trace's token count (load factor <= 1/2) guarantees room; capped at
+    // 2^24 entries (256 MiB per slot). Beyond the cap a full table is a loud
+    // PDSIM_PAIR_ERROR, never a silent miscount.
+    int64_t max_tok = 1;
+    for (const auto& t : ctx->packed) max_tok = std::max<int64_t>(max_tok, t.total_decode);
+    int32_t cap = 1 << 12;
+    while (cap < (1 << 24) && static_cast<int64_t>(cap) < 2 * max_tok) cap <<= 1;
+    caps.rep_gapcap = cap;
   }
   const size_t slot_bytes = pdg::global_slot_bytes(caps, nullptr, nullptr);
 
@@ -371,20 +479,33 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   const bool with_rec0 = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
   // (a single candidate is its own argmax: nothing to prune)
   const bool prune = ctx->search_mode == PDSIM_SEARCH_ARGMAX && !with_rec0 && !ctx->profiling && n > 0 && C > 1;
+  if (list && n > 0) {
+    CU(ctx, ctx->d_pair_list.reserve(8 * static_cast<size_t>(n)));
+    CU(ctx, cudaMemcpyAsync(ctx->d_pair_list.p, list, 8 * static_cast<size_t>(n), cudaMemcpyHostToDevice, ctx->stream));
+    a.pair_list = ctx->d_pair_list.as<int64_t>();
+  }
   if (prune) {
-    CU(ctx, ctx->d_pair_fail.reserve(4 * static_cast<size_t>(n)));
-    CU(ctx, ctx->d_pair_ok.reserve(4 * static_cast<size_t>(n)));
-    CU(ctx, cudaMemsetAsync(ctx->d_pair_ok.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
+    // bounds are indexed by global pair (every replica of a candidate)
+    const size_t nb = 4 * static_cast<size_t>(total);
+    CU(ctx, ctx->d_pair_fail.reserve(nb));
+    CU(ctx, ctx->d_pair_ok.reserve(nb));
+    CU(ctx, cudaMemsetAsync(ctx->d_pair_ok.p, 0, nb, ctx->stream));
     CU(ctx, ctx->d_best_key.reserve(8));
-    CU(ctx, cudaMemsetAsync(ctx->d_pair_fail.p, 0, 4 * static_cast<size_t>(n), ctx->stream));
+    CU(ctx, cudaMemsetAsync(ctx->d_pair_fail.p, 0, nb, ctx->stream));
     CU(ctx, cudaMemsetAsync(ctx->d_best_key.p, 0, 8, ctx->stream));
     a.best_key = ctx->d_best_key.as<unsigned long long>();
     a.pair_fail = ctx->d_pair_fail.as<int32_t>();
     a.pair_ok = ctx->d_pair_ok.as<int32_t>();
     a.cand_invalid = ctx->d_cand_inv.as<int8_t>();
-    a.total_sessions = ctx->total_sessions;
+    // A shard of a larger search (replicas staged on other GPUs) bounds
+    // candidates by the sessions of the WHOLE search (set_global_sessions):
+    // the local staged total would prune a candidate that merely loses on
+    // this GPU's replicas.
+    a.total_sessions = ctx->global_sessions > 0 ? ctx->global_sessions : ctx->total_sessions;
   }
   int64_t launches = 0;
+  ProfileLease lease(ctx);  // held until this search's stream synchronisation
+  CU(ctx, lease.acquire());
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
     // The diagnostics build (per-phase clock64 counters) is a separate
@@ -403,6 +524,27 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     CU(ctx, cudaGetLastError());
   }
   CU(ctx, cudaEventRecord(ctx->ev[2], ctx->stream));
+  if (ctx->comm) {
+    // The one collective of a sharded search: per-candidate
+    // counts summed and flags max-reduced over every GPU's shard, in place,
+    // on this search's stream; the argmax below then sees the whole search.
+    flags_for_max_kernel<<<1, 256, 0, ctx->stream>>>(ctx->d_cand_bad.as<int>(), C);
+    ++launches;
+    CU(ctx, cudaGetLastError());
+    const pdg::NcclApi& nc = pdg::nccl();
+    ncclResult_t r = nc.GroupStart();
+    if (r == ncclSuccess) {
+      r = nc.AllReduce(ctx->d_cand_sum.p, ctx->d_cand_sum.p, static_cast<size_t>(C), ncclUint64, ncclSum, ctx->comm,
+                       ctx->stream);
+    }
+    if (r == ncclSuccess) {
+      r = nc.AllReduce(ctx->d_cand_bad.p, ctx->d_cand_bad.p, static_cast<size_t>(C), ncclInt32, ncclMax, ctx->comm,
+                       ctx->stream);
+    }
+    const ncclResult_t r2 = nc.GroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) return set_err(ctx, PDSIM_ERR_CUDA, "ncclAllReduce: " + pdg::nccl_error(r));
+  }
   argmax_kernel<<<1, 256, 0, ctx->stream>>>(ctx->d_cand_sum.as<unsigned long long>(), ctx->d_cand_bad.as<int>(), C,
                                           ctx->d_best.as<unsigned long long>());
   ++launches;
@@ -614,6 +756,7 @@ void pdsim_gpu_destroy(pdsim_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) pdg::nccl().CommDestroy(ctx->comm);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -677,6 +820,202 @@ int pdsim_gpu_plan_search(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, cons
   return rc;
 }
 
+int pdsim_gpu_search_staged_list(pdsim_gpu_ctx* ctx, const int64_t* pairs, int64_t n_pairs, uint64_t seed,
+                                 pdsim_search_output* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!pairs && n_pairs > 0) return set_err(ctx, PDSIM_ERR_CONFIG, "search: null pair list");
+  static const int64_t kNone = 0;
+  pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  const int rc = search_impl(ctx, 0, 0, seed, out, rec, nullptr, pairs ? pairs : &kNone, n_pairs);
+  if (out && rc == PDSIM_OK) out->h2d_bytes = 8 * n_pairs;
+  return rc;
+}
+
+int pdsim_gpu_set_global_sessions(pdsim_gpu_ctx* ctx, int64_t total_sessions) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (total_sessions < 0 || total_sessions >= static_cast<int64_t>(0xfffffffeLL)) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "search: global session total out of range");
+  }
+  ctx->global_sessions = total_sessions;
+  return PDSIM_OK;
+}
+
+int64_t pdsim_shard_pairs(int32_t n_traces, const int64_t* trace_rounds, int32_t n_candidates,
+                          const pdsim_plan* candidates, int32_t world, int32_t rank, int64_t* out,
+                          int64_t capacity) {
+  if (n_traces < 0 || n_candidates < 0 || (n_traces > 0 && !trace_rounds) || (n_candidates > 0 && !candidates) ||
+      world < 1 || rank < 0 || rank >= world) {
+    set_err(nullptr, PDSIM_ERR_CONFIG, "shard_pairs: bad arguments");
+    return -1;
+  }
+  const std::vector<int64_t> mine = pdg::shard_pairs(n_traces, trace_rounds, n_candidates, candidates, world, rank);
+  if (out) {
+    for (size_t k = 0; k < mine.size() && static_cast<int64_t>(k) < capacity; ++k) out[k] = mine[k];
+  }
+  return static_cast<int64_t>(mine.size());
+}
+
+int pdsim_nccl_unique_id(uint8_t id[128]) {
+  const pdg::NcclApi& nc = pdg::nccl();
+  if (!nc.error.empty()) return set_err(nullptr, PDSIM_ERR_CUDA, nc.error);
+  ncclUniqueId u;
+  const ncclResult_t r = nc.GetUniqueId(&u);
+  if (r != ncclSuccess) return set_err(nullptr, PDSIM_ERR_CUDA, "ncclGetUniqueId: " + pdg::nccl_error(r));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  memcpy(id, &u, sizeof(u));
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_comm_init(pdsim_gpu_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128]) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (world < 1 || rank < 0 || rank >= world || !id) return set_err(ctx, PDSIM_ERR_CONFIG, "comm_init: bad arguments");
+  const pdg::NcclApi& nc = pdg::nccl();
+  if (!nc.error.empty()) return set_err(ctx, PDSIM_ERR_CUDA, nc.error);
+  if (ctx->comm) {
+    nc.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = nc.CommInitRank(&ctx->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    ctx->comm = nullptr;
+    return set_err(ctx, PDSIM_ERR_CUDA, "ncclCommInitRank: " + pdg::nccl_error(r));
+  }
+  ctx->comm_world = world;
+  ctx->comm_rank = rank;
+  return PDSIM_OK;
+}
+
+int pdsim_multi_plan_search(int32_t n_devices, const int32_t* devices, const pdsim_search_input* in,
+                            const pdsim_profile* profile, const pdsim_sched_params* params, uint64_t seed,
+                            int32_t search_mode, pdsim_search_output* out) {
+  if (n_devices < 1 || !devices || !in || !profile || !params) {
+    return set_err(nullptr, PDSIM_ERR_CONFIG, "multi_plan_search: bad arguments");
+  }
+  if (in->n_traces < 1 || in->n_candidates < 1 || !in->traces || !in->candidates) {
+    return set_err(nullptr, PDSIM_ERR_CONFIG, "search: need at least one trace and one candidate");
+  }
+  const int64_t total = static_cast<int64_t>(in->n_traces) * in->n_candidates;
+  if (in->pair_begin != 0 || (in->pair_end >= 0 && in->pair_end != total)) {
+    return set_err(nullptr, PDSIM_ERR_CONFIG, "multi_plan_search: shards the whole search (pair range must be all)");
+  }
+  const pdg::NcclApi& nc = pdg::nccl();
+  if (!nc.error.empty()) return set_err(nullptr, PDSIM_ERR_CUDA, nc.error);
+  std::vector<pdsim_gpu_ctx*> ctxs(static_cast<size_t>(n_devices), nullptr);
+  auto cleanup = [&]() {
+    for (auto* c : ctxs) pdsim_gpu_destroy(c);
+  };
+  for (int32_t k = 0; k < n_devices; ++k) {
+    if (int rc = pdsim_gpu_create(devices[k], &ctxs[static_cast<size_t>(k)])) {
+      cleanup();
+      return rc;
+    }
+  }
+  std::vector<ncclComm_t> comms(static_cast<size_t>(n_devices), nullptr);
+  const ncclResult_t r = nc.CommInitAll(comms.data(), n_devices, devices);
+  if (r != ncclSuccess) {
+    cleanup();
+    return set_err(nullptr, PDSIM_ERR_CUDA, "ncclCommInitAll: " + pdg::nccl_error(r));
+  }
+  std::vector<int64_t> rounds(static_cast<size_t>(in->n_traces));
+  int64_t sessions = 0;
+  for (int32_t t = 0; t < in->n_traces; ++t) {
+    rounds[static_cast<size_t>(t)] = in->traces[t].n_rounds;
+    sessions += in->traces[t].n_sessions;
+  }
+  const int C = in->n_candidates;
+  std::vector<std::vector<int64_t>> lists(static_cast<size_t>(n_devices));
+  std::vector<int> rcs(static_cast<size_t>(n_devices), PDSIM_OK);
+  std::vector<pdsim_search_output> outs(static_cast<size_t>(n_devices));
+  std::vector<std::vector<pdsim_attainment>> att(static_cast<size_t>(n_devices));
+  std::vector<std::vector<pdsim_counters>> ctr(static_cast<size_t>(n_devices));
+  std::vector<std::vector<int8_t>> st(static_cast<size_t>(n_devices));
+  std::vector<std::vector<int64_t>> ev(static_cast<size_t>(n_devices)), cy(static_cast<size_t>(n_devices));
+  std::vector<std::vector<int64_t>> cand(static_cast<size_t>(n_devices), std::vector<int64_t>(static_cast<size_t>(C)));
+  std::vector<int64_t> h2d(static_cast<size_t>(n_devices), 0);
+  std::vector<std::thread> th;
+  for (int32_t k = 0; k < n_devices; ++k) {
+    th.emplace_back([&, k]() {
+      const size_t K = static_cast<size_t>(k);
+      pdsim_gpu_ctx* c = ctxs[K];
+      c->comm = comms[K];
+      c->comm_world = n_devices;
+      c->comm_rank = k;
+      lists[K] = pdg::shard_pairs(in->n_traces, rounds.data(), C, in->candidates, n_devices, k);
+      const size_t m = std::max<size_t>(lists[K].size(), 1);
+      att[K].resize(m);
+      ctr[K].resize(m);
+      st[K].resize(m);
+      ev[K].resize(m);
+      cy[K].resize(m);
+      pdsim_search_output& o = outs[K];
+      memset(&o, 0, sizeof(o));
+      o.pair_attainment = att[K].data();
+      o.pair_counters = ctr[K].data();
+      o.pair_status = st[K].data();
+      o.pair_events = ev[K].data();
+      o.pair_cycles = cy[K].data();
+      o.candidate_slo_ok = cand[K].data();
+      int rc = check_ctx(c);
+      if (rc == PDSIM_OK) rc = stage_impl(c, in, profile, params, &h2d[K]);
+      if (rc == PDSIM_OK) rc = pdsim_gpu_set_global_sessions(c, sessions);
+      if (rc == PDSIM_OK) rc = pdsim_gpu_set_search_mode(c, search_mode);
+      pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+      static const int64_t kNone = 0;
+      // every rank reaches the collective inside search_impl, even with an
+      // empty shard; a rank that failed before it would hang the others,
+      // so staging errors are validated identically on every rank first.
+      if (rc == PDSIM_OK) {
+        rc = search_impl(c, 0, 0, seed, &o, rec, nullptr, lists[K].empty() ? &kNone : lists[K].data(),
+                         static_cast<int64_t>(lists[K].size()));
+      }
+      rcs[K] = rc;
+    });
+  }
+  for (auto& t : th) t.join();
+  int rc = PDSIM_OK;
+  std::string msg;
+  for (int32_t k = 0; k < n_devices && rc == PDSIM_OK; ++k) {
+    if (rcs[static_cast<size_t>(k)] != PDSIM_OK) {
+      rc = rcs[static_cast<size_t>(k)];
+      msg = ctxs[static_cast<size_t>(k)]->err;
+    }
+  }
+  if (rc == PDSIM_OK && out) {
+    const pdsim_search_output& o0 = outs[0];
+    double kms = 0, dms = 0;
+    int64_t launches = 0, d2h = 0, h2d_all = 0;
+    for (int32_t k = 0; k < n_devices; ++k) {
+      const size_t K = static_cast<size_t>(k);
+      for (size_t j = 0; j < lists[K].size(); ++j) {
+        const int64_t p = lists[K][j];
+        if (out->pair_attainment) out->pair_attainment[p] = att[K][j];
+        if (out->pair_counters) out->pair_counters[p] = ctr[K][j];
+        if (out->pair_status) out->pair_status[p] = st[K][j];
+        if (out->pair_events) out->pair_events[p] = ev[K][j];
+        if (out->pair_cycles) out->pair_cycles[p] = cy[K][j];
+      }
+      kms = std::max(kms, outs[K].kernel_ms);
+      dms = std::max(dms, outs[K].device_ms);
+      launches += outs[K].kernel_launches;
+      d2h += outs[K].d2h_bytes;
+      h2d_all += h2d[K];
+    }
+    if (out->candidate_slo_ok) memcpy(out->candidate_slo_ok, cand[0].data(), 8 * static_cast<size_t>(C));
+    out->best_candidate = o0.best_candidate;
+    out->best_slo_ok = o0.best_slo_ok;
+    out->kernel_ms = kms;
+    out->device_ms = dms;
+    out->kernel_launches = launches;
+    out->d2h_bytes = d2h;
+    out->h2d_bytes = h2d_all;
+  }
+  cleanup();  // destroys the communicators with the contexts
+  if (rc != PDSIM_OK) return set_err(nullptr, rc, msg);
+  return PDSIM_OK;
+}
+
 int pdsim_gpu_sweep(pdsim_gpu_ctx* ctx, int32_t n_traces, const pdsim_trace* traces, const pdsim_plan* plan,
                     int32_t n_settings, const pdsim_sched_params* settings, const pdsim_profile* profile,
                     uint64_t seed, pdsim_search_output* out) {
@@ -694,6 +1033,16 @@ int pdsim_gpu_sweep(pdsim_gpu_ctx* ctx, int32_t n_traces, const pdsim_trace* tra
   in.pair_end = -1;
   int64_t h2d = 0;
   if (int rc = stage_impl(ctx, &in, profile, &settings[0], &h2d, settings)) return rc;
+  // The reference sweep replays rate-major (pdsim.cpp:547-586) and run()'s
+  // precheck throws at the first trace with an oversized first round; the
+  // plan is the same for every setting, so that trace fails them all.
+  for (int32_t r = 0; r < n_traces; ++r) {
+    if (ctx->pair_invalid[static_cast<size_t>(r)]) {
+      ctx->staged = false;
+      const int64_t i = pdg::precheck_violator(ctx->packed[static_cast<size_t>(r)], ctx->plans[0], ctx->profile);
+      return set_err(ctx, PDSIM_ERR_CONFIG, pdg::precheck_message(ctx->packed[static_cast<size_t>(r)], i));
+    }
+  }
   pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const int rc = search_impl(ctx, 0, -1, seed, out, rec, nullptr);
   // The settings stay staged: pdsim_gpu_search_staged() re-runs the sweep
@@ -717,7 +1066,8 @@ int pdsim_gpu_run(pdsim_gpu_ctx* ctx, const pdsim_trace* trace, const pdsim_plan
   in.pair_end = 1;
   if (int rc = stage_impl(ctx, &in, profile, params, nullptr)) return rc;
   if (ctx->pair_invalid[0]) {
-    return set_err(ctx, PDSIM_ERR_CONFIG, "trace: a session's first-round KV exceeds every decode worker's capacity");
+    const int64_t i = pdg::precheck_violator(ctx->packed[0], ctx->plans[0], ctx->profile);
+    return set_err(ctx, PDSIM_ERR_CONFIG, pdg::precheck_message(ctx->packed[0], i));
   }
   const pdg::PackedTrace& t = ctx->packed[0];
   pdg::Records rec{nullptr, nullptr, nullptr, nullptr, nullptr, 0};

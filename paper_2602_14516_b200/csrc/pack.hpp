@@ -295,6 +295,25 @@ inline bool precheck(const PackedTrace& t, const DevPlan& plan, const pdsim_prof
   return true;
 }
 
+// Index of the first session (trace order) precheck_sessions would reject,
+// -1 when none; and the reference's ConfigError text for it
+// (sim_engine.cpp:217-231).
+inline int64_t precheck_violator(const PackedTrace& t, const DevPlan& plan, const pdsim_profile& prof) {
+  int64_t max_cap = 0;
+  for (int d = 0; d < plan.D; ++d) {
+    max_cap = std::max<int64_t>(max_cap, static_cast<int64_t>(prof.degrees[plan.ddeg[d]]) * prof.gpu_memory_capacity);
+  }
+  for (size_t i = 0; i < t.first_round_incr.size(); ++i) {
+    if (t.first_round_incr[i] * prof.kv_bytes_per_token > max_cap) return static_cast<int64_t>(i);
+  }
+  return -1;
+}
+
+inline std::string precheck_message(const PackedTrace& t, int64_t i) {
+  return "trace: session " + std::to_string(t.sid[static_cast<size_t>(i)]) +
+         " first-round KV exceeds every decode worker's capacity";
+}
+
 inline DevParams to_dev_params(const pdsim_sched_params& s) {
   DevParams d;
   d.routing = s.routing;

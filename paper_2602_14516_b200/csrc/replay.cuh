@@ -27,7 +27,7 @@ struct KernelArgs {
   size_t slot_bytes;
   size_t smem_bytes;
   unsigned long long* next_pair;
-  PairResult* results;            // [pair_end - pair_begin]
+  PairResult* results;            // [pair_end - pair_begin], by launch item
   unsigned long long* cand_sum;        // [n_candidates]
   int* cand_bad;                       // [n_candidates]
   Records rec;                    // single-run records (one pair only)
@@ -36,10 +36,11 @@ struct KernelArgs {
   int32_t profile;                     // per-phase clock64 instrumentation
   int32_t reserved3;
   unsigned long long* best_key;        // prune: incumbent key
-  int32_t* pair_fail;                  // prune: [pair_end - pair_begin]
-  int32_t* pair_ok;                    // prune: [pair_end - pair_begin]
+  int32_t* pair_fail;                  // prune: [n_candidates * n_traces], by global pair
+  int32_t* pair_ok;                    // prune: [n_candidates * n_traces], by global pair
   const int8_t* cand_invalid;          // prune: [n_candidates] any pair of c invalid (whole search)
-  int64_t total_sessions;              // prune: sum of S over the replicas
+  int64_t total_sessions;              // prune: sum of S over ALL replicas of the search (every shard)
+  const int64_t* pair_list;            // optional: the launch replays pair_list[0 .. pair_end - pair_begin)
 };
 
 // One warp per block; the warp replays pairs pulled from an atomic queue.
@@ -64,8 +65,12 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     unsigned long long ticket = 0;
     if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    const int64_t pair = static_cast<int64_t>(ticket) + a.pair_begin;
-    if (pair >= a.pair_end) break;
+    // Item `idx` of the launch: pair_begin + idx, or pair_list[idx] (a shard
+    // of the search in cost order, pdsim_shard_pairs). Per-pair outputs are
+    // indexed by item; argmax-mode bounds by global pair (c * n_traces + r).
+    const int64_t idx = static_cast<int64_t>(ticket);
+    if (idx >= a.pair_end - a.pair_begin) break;
+    const int64_t pair = a.pair_list ? a.pair_list[idx] : a.pair_begin + idx;
     const int32_t c = static_cast<int32_t>(pair / a.n_traces);
     const int32_t r = static_cast<int32_t>(pair % a.n_traces);
     PairResult res;
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
         memset(&rep, 0, sizeof(rep));
         rep.sessions_total = a.traces[r].S;
         rep.empty = 1;
-        a.reports[pair - a.pair_begin] = rep;
+        a.reports[idx] = rep;
       }
     } else {
       const DevTrace tr = a.traces[r];
@@ -102,12 +107,14 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
         prn.c_invalid = a.cand_invalid[c];
         prn.cand_bad = a.cand_bad;
         prn.total_sessions = a.total_sessions;
-        prn.self = pair - a.pair_begin;
-        prn.fail_base = static_cast<int64_t>(c) * a.n_traces - a.pair_begin;
-        const int64_t lo = a.pair_begin - static_cast<int64_t>(c) * a.n_traces;
-        const int64_t hi = a.pair_end - static_cast<int64_t>(c) * a.n_traces;
-        prn.r_lo = static_cast<int32_t>(lo < 0 ? 0 : lo);
-        prn.r_hi = static_cast<int32_t>(hi > a.n_traces ? a.n_traces : hi);
+        // Bounds over every replica of c: replicas outside this launch (or
+        // on another GPU) read as 0 failures / 0 attained, which keeps the
+        // upper bound (total_sessions of the whole search - failures) and
+        // the lower bound (attained so far) valid for the global argmax.
+        prn.self = pair;
+        prn.fail_base = static_cast<int64_t>(c) * a.n_traces;
+        prn.r_lo = 0;
+        prn.r_hi = a.n_traces;
         prn.c = c;
       }
       EngineT<kProf, kD, kP, kRec, true, kPrune> eng(sslot.es, tr, pl, prm, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0,
@@ -117,11 +124,11 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       if (kRec && a.reports) {
         pdsim_report rep;
         eng.build_report(&rep);
-        if (lane == 0) a.reports[pair - a.pair_begin] = rep;
+        if (lane == 0) a.reports[idx] = rep;
       }
     }
     if (lane == 0) {
-      a.results[pair - a.pair_begin] = res;
+      a.results[idx] = res;
       if (res.status == PDSIM_PAIR_PRUNED) {
         atomicOr(&a.cand_bad[c], 2);
       } else if (res.status != PDSIM_PAIR_OK) {
@@ -129,8 +136,8 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       } else {
         const unsigned long long old = atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
         if (kPrune) {  // final counts join the replicas' bounds
-          atomicMax(&a.pair_ok[pair - a.pair_begin], static_cast<int32_t>(res.att.slo_ok));
-          atomicMax(&a.pair_fail[pair - a.pair_begin],
+          atomicMax(&a.pair_ok[pair], static_cast<int32_t>(res.att.slo_ok));
+          atomicMax(&a.pair_fail[pair],
                     static_cast<int32_t>(res.att.sessions_total - res.att.slo_ok));
         }
         if (kPrune && !a.cand_invalid[c]) {  // completed replicas: a lower bound of c's count

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDSIM_LIB") or os.path.join(HERE, "libpdsim_gpu.so")
 
 _lib = None
-ABI_VERSION = 2  # include/pdsim_gpu.h PDSIM_ABI_VERSION
+ABI_VERSION = 3  # include/pdsim_gpu.h PDSIM_ABI_VERSION
 
 
 class PdsimError(RuntimeError):
@@ -91,6 +91,16 @@ def lib():
         L.pdsim_top_k.argtypes = [P(abi.Coefficients), C.c_int32, C.c_int32, P(abi.Plan), P(C.c_double),
                                   P(C.c_int32)]
         L.pdsim_top_k.restype = C.c_int64
+        L.pdsim_gpu_set_global_sessions.argtypes = [C.c_void_p, C.c_int64]
+        L.pdsim_shard_pairs.argtypes = [C.c_int32, P(C.c_int64), C.c_int32, P(abi.Plan), C.c_int32, C.c_int32,
+                                        P(C.c_int64), C.c_int64]
+        L.pdsim_shard_pairs.restype = C.c_int64
+        L.pdsim_gpu_search_staged_list.argtypes = [C.c_void_p, P(C.c_int64), C.c_int64, C.c_uint64,
+                                                   P(abi.SearchOutput)]
+        L.pdsim_nccl_unique_id.argtypes = [P(C.c_uint8)]
+        L.pdsim_gpu_comm_init.argtypes = [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint8)]
+        L.pdsim_multi_plan_search.argtypes = [C.c_int32, P(C.c_int32), P(abi.SearchInput), P(abi.Profile),
+                                              P(abi.SchedParams), C.c_uint64, C.c_int32, P(abi.SearchOutput)]
         if L.pdsim_abi_version() != ABI_VERSION:
             raise PdsimError(abi.ERR_INTERNAL, "ABI version mismatch")
         _lib = L
@@ -363,6 +373,24 @@ class Context:
         self._staged = (len(traces), len(settings))
         return SearchResult(out, att, ctr, st, cand, n)
 
+    def search_staged_list(self, seed, pairs, report=False):
+        """Replays the staged pairs in `pairs` (global indices) in list order;
+        per-pair outputs follow the list (include/pdsim_gpu.h)."""
+        nt, nc = self._staged
+        arr = (C.c_int64 * max(len(pairs), 1))(*pairs)
+        out, att, ctr, st, cand = self._outputs(len(pairs), nc, report)
+        self._check(lib().pdsim_gpu_search_staged_list(self._h, arr, len(pairs), seed, C.byref(out)))
+        return SearchResult(out, att, ctr, st, cand, len(pairs))
+
+    def set_global_sessions(self, total):
+        """Sessions of the whole search this context is a shard of (ARGMAX bounds)."""
+        self._check(lib().pdsim_gpu_set_global_sessions(self._h, int(total)))
+
+    def comm_init(self, world, rank, unique_id):
+        """Joins the NCCL communicator of a sharded search (one process per GPU)."""
+        buf = (C.c_uint8 * 128)(*unique_id)
+        self._check(lib().pdsim_gpu_comm_init(self._h, world, rank, buf))
+
     def set_search_mode(self, mode):
         """abi.SEARCH_FULL (default) or abi.SEARCH_ARGMAX (exact pruning:
         same best_candidate / best_slo_ok, pruned candidates report -2)."""
@@ -392,6 +420,37 @@ class Context:
         out, att, ctr, st, cand = self._outputs(n, nc, report)
         self._check(lib().pdsim_gpu_search_staged(self._h, pair_begin, pair_end, seed, C.byref(out)))
         return SearchResult(out, att, ctr, st, cand, n)
+
+
+def shard_pairs(traces, plans, world, rank):
+    """This rank's pairs (global index c * len(traces) + r) in queue order:
+    the library's cost-aware LPT split (pdsim_shard_pairs)."""
+    rounds = (C.c_int64 * max(len(traces), 1))(*[int(t.n_rounds) for t in traces])
+    pv = (abi.Plan * max(len(plans), 1))(*plans)
+    n = lib().pdsim_shard_pairs(len(traces), rounds, len(plans), pv, world, rank, None, 0)
+    if n < 0:
+        _check(abi.ERR_CONFIG)
+    out = (C.c_int64 * max(n, 1))()
+    lib().pdsim_shard_pairs(len(traces), rounds, len(plans), pv, world, rank, out, n)
+    return list(out)[:n]
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    _check(lib().pdsim_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def multi_plan_search(devices, traces, plans, profile, params, seed, mode=abi.SEARCH_FULL):
+    """One host thread, several GPUs (pdsim_multi_plan_search): shards, replays,
+    all-reduces over NCCL; outputs indexed by global pair."""
+    inp = search_input(traces, plans)
+    n = len(traces) * len(plans)
+    dv = (C.c_int32 * len(devices))(*devices)
+    out, att, ctr, st, cand = Context._outputs(None, n, len(plans), False)
+    _check(lib().pdsim_multi_plan_search(len(devices), dv, C.byref(inp), C.byref(profile), C.byref(params), seed,
+                                         int(mode), C.byref(out)))
+    return SearchResult(out, att, ctr, st, cand, n)
 
 
 def format_double(x):

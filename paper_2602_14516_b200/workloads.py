@@ -17,28 +17,12 @@ import ctypes as C
 
 import numpy as np
 
-from . import abi, native
-
-PROFILE_SEED = 7
-ENGINE_SEED = 1
-DEGREES = (1, 2, 4, 8)
-
-MODEL_PRESETS = {
-    "llama3-8b": dict(scale=1.0, kv_bytes_per_token=131072),
-    "qwen-32b": dict(scale=4.0, kv_bytes_per_token=262144),
-    "llama3-70b": dict(scale=8.75, kv_bytes_per_token=327680),
-}
+from . import abi, native, specs
+from .specs import DEGREES, ENGINE_SEED, MODEL_PRESETS, PROFILE_SEED  # noqa: F401
 
 
 def model_spec(name):
-    p = MODEL_PRESETS[name]
-    s = native.default_synth_spec()
-    k = p["scale"]
-    for f in ("prefill_alpha_min", "prefill_alpha_max", "prefill_beta_min", "prefill_beta_max",
-              "decode_alpha_min", "decode_alpha_max", "decode_beta_min", "decode_beta_max"):
-        setattr(s, f, getattr(s, f) * k)
-    s.kv_bytes_per_token = p["kv_bytes_per_token"]
-    return s
+    return specs.apply_model(native.default_synth_spec(), name)
 
 
 def model_profile(name):
@@ -48,17 +32,7 @@ def model_profile(name):
 def trace_stats(kind):
     """toolbench / gaia / hotpotqa / dureader presets, plus the two
     fixed-round variants the configs name."""
-    if kind == "toolbench-4fixed":  # C1: ReAct-style 4 fixed rounds
-        st = native.preset_stats("toolbench")
-        st.mean_rounds = 4.0
-        st.fixed_rounds = 1
-        return st
-    if kind == "hotpotqa-8fixed":  # C3: iterative RAG, 8 fixed rounds
-        st = native.preset_stats("hotpotqa")
-        st.mean_rounds = 8.0
-        st.fixed_rounds = 1
-        return st
-    return native.preset_stats(kind)
+    return specs.apply_stats(native.preset_stats(specs.STATS[kind][0]), kind)
 
 
 class Workload:
@@ -98,43 +72,55 @@ class Workload:
         return sum(self.traces[p % nt].n_rounds for p in range(pair_begin, end))
 
 
+def build_trace(job):
+    """A spec TraceJob through the product generators (merged jobs: C4)."""
+    tr = native.gen_trace(trace_stats(job.kind), job.rate, job.sessions, job.seed)
+    if job.merge_with is None:
+        return tr
+    other = build_trace(job.merge_with)
+    return merge_traces(tr.view, other.view)
+
+
+def build(spec):
+    """Workload of a specs.Spec: traces (all host threads for plain jobs),
+    cost model, candidates (the reference's enumeration order)."""
+    plain = all(j.merge_with is None for j in spec.jobs)
+    if plain and len(spec.jobs) > 1 and len({j.kind for j in spec.jobs}) == 1 and len({j.sessions for j in spec.jobs}) == 1:
+        trs = native.gen_traces(trace_stats(spec.jobs[0].kind), [j.rate for j in spec.jobs], spec.jobs[0].sessions,
+                                [j.seed for j in spec.jobs])
+    else:
+        trs = [build_trace(j) for j in spec.jobs]
+    if spec.fixed_plan:
+        plans = [abi.make_plan(*spec.fixed_plan)]
+    else:
+        plans = native.enumerate_plans(spec.degrees, spec.total_gpus)
+    wl = Workload(spec.name, spec.model, trs, plans, abi.default_params(), spec.engine_seed, spec.total_gpus, spec.desc)
+    wl.spec = spec
+    return wl
+
+
 def c1():
-    st = trace_stats("toolbench-4fixed")
-    tr = native.gen_trace(st, 8.0, 1000, 1)
-    plan = abi.make_plan({1: 2}, {1: 2})
-    return Workload("C1", "llama3-8b", [tr], [plan], abi.default_params(), ENGINE_SEED, 4,
-                    "llama3-8b, fixed P:2x1 D:2x1, toolbench 1k sessions x 4 fixed rounds @8/s, 1 replay")
+    return build(specs.c1())
 
 
 def c2(sessions=10000, rate=16.0, seed=5, total_gpus=8, replicas=1):
-    """C2; with replicas > 1 (the multi-GPU weak-scaling form) trace replica
-    k uses gen seed seed + k."""
-    st = trace_stats("toolbench")
-    trs = [native.gen_trace(st, rate, sessions, seed + k) for k in range(replicas)]
-    plans = native.enumerate_plans(DEGREES, total_gpus)
-    rep = "" if replicas == 1 else f" x {replicas} replicas (seeds {seed}..{seed + replicas - 1})"
-    return Workload("C2", "llama3-8b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
-                    f"llama3-8b, all {len(plans)} N={total_gpus} P/D plans over degrees {{1,2,4,8}}, "
-                    f"toolbench {sessions} sessions @{rate}/s{rep}")
+    """C2; with replicas > 1 trace replica k uses gen seed seed + k."""
+    s = specs.c2(sessions, rate, seed, replicas)
+    s.total_gpus = total_gpus
+    return build(s)
 
 
-def c3(sessions=50000, rate=20.0, replicas=16, total_gpus=8):
-    st = trace_stats("hotpotqa-8fixed")
-    trs = native.gen_traces(st, [rate] * replicas, sessions, list(range(1, replicas + 1)))
-    plans = native.enumerate_plans(DEGREES, total_gpus)
-    return Workload("C3", "qwen-32b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
-                    f"qwen-32b, {len(plans)} plans x {replicas} hotpotqa-8-round replicas of {sessions} sessions")
+def c3(sessions=50000, rate=specs.C3_RATE, replicas=16, total_gpus=8):
+    s = specs.c3(sessions, rate, replicas)
+    s.total_gpus = total_gpus
+    return build(s)
 
 
 def c5(model="llama3-8b", rates=None, seeds=4, sessions=1000, total_gpus=8):
     """One model slice of C5: toolbench 1k-session traces over rates x seeds."""
-    rates = rates or [1.0 + 0.5 * k for k in range(32)]
-    st = trace_stats("toolbench")
-    rs = [r for r in rates for _ in range(seeds)]
-    trs = native.gen_traces(st, rs, sessions, [1000 + s for _ in rates for s in range(seeds)])
-    plans = native.enumerate_plans(DEGREES, total_gpus)
-    return Workload("C5", model, trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
-                    f"{model}, {len(plans)} plans x {len(trs)} toolbench traces ({len(rates)} rates x {seeds} seeds)")
+    s = specs.c5(model, rates, seeds, sessions)
+    s.total_gpus = total_gpus
+    return build(s)
 
 
 class OwnedTrace:
@@ -181,7 +167,7 @@ def merge_traces(a, b):
     return OwnedTrace(np.arange(len(order)), arr[order], off, inc[idx], dec[idx], dly[idx], a.ttft_thres, a.itl_thres)
 
 
-C4_RATES = (0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0, 8.0)
+C4_RATES = specs.C4_RATES
 
 
 def c4(rates=None, seeds=1, sessions=100000, total_gpus=8):
@@ -189,25 +175,14 @@ def c4(rates=None, seeds=1, sessions=100000, total_gpus=8):
     rate/2 each, merged by arrival), an arrival-rate sweep x seeds. The full
     grid is 8 rates x 64 seeds (512 traces x 169 plans = 86 528 pairs, ~5 GB
     of host trace arrays); the default is its first seed."""
-    rates = list(rates or C4_RATES)
-    half = sessions // 2
-    jobs = [(r, s) for s in range(seeds) for r in rates]
-    tool = native.gen_traces(trace_stats("toolbench"), [r / 2 for r, _ in jobs], half,
-                             [1 + 2 * k for k in range(len(jobs))])
-    hot = native.gen_traces(trace_stats("hotpotqa"), [r / 2 for r, _ in jobs], sessions - half,
-                            [2 + 2 * k for k in range(len(jobs))])
-    trs = [merge_traces(t.view, h.view) for t, h in zip(tool, hot)]
-    plans = native.enumerate_plans(DEGREES, total_gpus)
-    return Workload("C4", "llama3-70b", trs, plans, abi.default_params(), ENGINE_SEED, total_gpus,
-                    f"llama3-70b, {len(plans)} plans x {len(trs)} mixed toolbench+hotpotqa traces of {sessions} "
-                    f"sessions ({len(rates)} rates x {seeds} seed(s))")
+    s = specs.c4(rates, seeds, sessions)
+    s.total_gpus = total_gpus
+    return build(s)
 
 
 def c2_small():
     """C2 with a 2000-session trace (profiling / quick checks only)."""
-    wl = c2(sessions=2000)
-    wl.name = "C2s"
-    return wl
+    return build(specs.c2_small())
 
 
 CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C4": c4, "C5": c5}

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     lib = native.lib()
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.pdsim_abi_version() == native.ABI_VERSION == 2
+    assert lib.pdsim_abi_version() == native.ABI_VERSION == 3
 
 
 def test_struct_layouts_match_ctypes():

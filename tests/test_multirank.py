@@ -1,6 +1,9 @@
-"""World-size-2 gloo test of the sharded search host logic: two ranks each
-replay half of the pairs (with the CPU checker standing in for the GPU
-engine) and the all-reduced argmax equals the single-process search."""
+"""World-size-2 gloo tests of the sharded search host logic. Each rank takes
+its pairs from the library's cost-aware shard planner (C-ABI
+pdsim_shard_pairs), replays them (the CPU checker stands in for the GPU
+engine here; tests/test_gpu_multi.py runs the engine), the counts are
+all-reduced with the flags rule of the NCCL path, and the C-ABI argmax
+(pdsim_argmax_candidates) equals the single-process search."""
 import os
 import socket
 
@@ -27,12 +30,12 @@ def _inputs():
     return prof, traces, plans
 
 
-def _shard_counts(b, e, prof, traces, plans):
+def _shard_counts(pairs, prof, traces, plans):
     """CPU checker for one shard: per-candidate slo_ok (-1 invalid)."""
     from tests import parity
     nt = len(traces)
     out = [0] * len(plans)
-    for p in range(b, e):
+    for p in pairs:
         c, r = divmod(p, nt)
         try:
             run = parity.oracle_run(traces[r].view, plans[c], prof, abi.default_params(), 1)
@@ -48,17 +51,18 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     prof, traces, plans = _inputs()
-    n_pairs = len(traces) * len(plans)
+    views = [t.view for t in traces]
+    mine = distributed.shard(views, plans, rank, world)
     best, cnt, totals = distributed.sharded_search(
-        lambda b, e: _shard_counts(b, e, prof, traces, plans), n_pairs, rank, world)
-    q.put((rank, best, cnt, totals.tolist()))
+        lambda pairs: _shard_counts(pairs, prof, traces, plans), views, plans, rank, world)
+    q.put((rank, best, cnt, totals.tolist(), mine))
     dist.destroy_process_group()
 
 
 def test_two_rank_sharded_argmax_matches_single_process():
     prof, traces, plans = _inputs()
     n_pairs = len(traces) * len(plans)
-    full = _shard_counts(0, n_pairs, prof, traces, plans)
+    full = _shard_counts(range(n_pairs), prof, traces, plans)
     want_best = max(range(len(full)), key=lambda c: (full[c], -c))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -70,10 +74,13 @@ def test_two_rank_sharded_argmax_matches_single_process():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, best, cnt, totals in res:
+    shards = {}
+    for rank, best, cnt, totals, mine in res:
         assert totals == full
         assert best == want_best
         assert cnt == full[want_best]
+        shards[rank] = mine
+    assert sorted(shards[0] + shards[1]) == list(range(n_pairs))  # a partition of the pairs
 
 
 def test_shard_ranges_partition_the_pairs():
@@ -113,5 +120,32 @@ def test_two_rank_reduction_excludes_pruned_candidates():
     for p in procs:
         p.join(timeout=60)
     for rank, (best, cnt), totals in got:
-        assert totals == [-1, 11, -1, -1]
+        assert totals == [-2, 11, -2, -1]  # invalid anywhere wins over pruned
         assert (best, cnt) == (1, 11)
+
+
+def test_shard_planner_is_a_balanced_lpt_partition():
+    """pdsim_shard_pairs: every pair on exactly one rank; each rank's queue
+    in non-increasing cost; the split equals LPT list scheduling restated
+    here (cost = rounds x (workers + 2), ties to the lower pair / rank)."""
+    prof, traces, plans = _inputs()
+    views = [t.view for t in traces] + [native.gen_trace(native.preset_stats("gaia"), 3.0, 60, 9).view]
+    nt = len(views)
+
+    def cost(p):
+        c, r = divmod(p, nt)
+        x, y = abi.plan_dict(plans[c])
+        return max(int(views[r].n_rounds), 1) * (sum(x.values()) + sum(y.values()) + 2)
+
+    n = nt * len(plans)
+    for world in (1, 2, 3, 8):
+        order = sorted(range(n), key=lambda p: (-cost(p), p))
+        load, want = [0] * world, [[] for _ in range(world)]
+        for p in order:
+            k = min(range(world), key=lambda j: (load[j], j))
+            load[k] += cost(p)
+            want[k].append(p)
+        got = [distributed.shard(views, plans, r, world) for r in range(world)]
+        assert got == want
+        assert sorted(sum(got, [])) == list(range(n))
+        assert max(load) - min(load) <= max(cost(p) for p in range(n))

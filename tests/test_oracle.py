@@ -58,3 +58,29 @@ def test_c_oracle_config_errors():
         cbind.run(tr.view, abi.make_plan({1: 1}, {16: 1}), prof, abi.default_params(), 1)
     with pytest.raises(cbind.OracleError):
         cbind.run(tr.view, abi.make_plan({1: 1}, {1: 1}), prof, abi.default_params(window=9), 1)
+
+
+def test_reference_arm_builds_identical_inputs():
+    """bench.py's reference arm builds its inputs through the reference alone
+    (oracle/ref_workloads.py); they must be byte-identical to the product
+    arm's: traces, cost model, candidate order (SURVEY.md §8(d) pinning)."""
+    import numpy as np
+    from oracle import ref_workloads, refbind
+    from paper_2602_14516_b200 import specs, workloads
+    if not refbind.available():
+        pytest.skip("reference library not built")
+
+    def arrays(v):
+        return [np.ctypeslib.as_array(getattr(v, f), shape=(n,)).tobytes() for f, n in
+                [("session_id", v.n_sessions), ("arrival_time", v.n_sessions), ("round_offset", v.n_sessions + 1),
+                 ("incr_input_len", v.n_rounds), ("decode_len", v.n_rounds), ("interaction_delay", v.n_rounds)]]
+
+    for sp in (specs.c1(), specs.c2(sessions=400), specs.c3(sessions=200, replicas=2),
+               specs.c4(rates=[2.0, 6.0], sessions=500), specs.c5(rates=[4.0], seeds=2, sessions=100)):
+        a, b = workloads.build(sp), ref_workloads.build(sp)
+        assert bytes(a.profile) == bytes(b.profile), sp.name
+        assert [bytes(x) for x in a.plans] == [bytes(x) for x in b.plans], sp.name
+        assert len(a.traces) == len(b.traces)
+        for x, y in zip(a.traces, b.traces):
+            assert arrays(x) == arrays(y) and (x.ttft_thres, x.itl_thres) == (y.ttft_thres, y.itl_thres), sp.name
+        assert specs.config_dict(sp)["pairs"] == a.n_pairs == b.n_pairs

@@ -123,3 +123,57 @@ def test_sweep_rejects_bad_setting(ctx):
         ctx.sweep([tr.view], plan, prof, [abi.default_params(), abi.default_params(window=9)], 1)
     with pytest.raises(native.ConfigError):  # SchedulerParams::validate (sim_engine.cpp:653-666)
         ctx.sweep([tr.view], plan, prof, [abi.default_params(alpha=-1.0)], 1)
+
+
+@pytest.mark.gpu
+def test_sweep_precheck_failure_is_config_error(ctx):
+    """A trace whose first round cannot fit any decode worker makes the
+    reference's run() throw inside the sweep loop (sim_engine.cpp:217-231,
+    pdsim.cpp:567-570): the batched sweep raises the same ConfigError text,
+    naming the first offending session of the first failing trace."""
+    import numpy as np
+    from oracle import refbind
+    prof = native.synth_profile(native.default_synth_spec(), 7)
+    plan = abi.make_plan({1: 1}, {1: 1})
+    trs = [native.gen_trace(native.preset_stats("toolbench"), 4.0, 200, s) for s in (1, 2)]
+
+    def first_rounds(v):
+        off = np.ctypeslib.as_array(v.round_offset, shape=(v.n_sessions + 1,))
+        return np.ctypeslib.as_array(v.incr_input_len, shape=(v.n_rounds,))[off[:-1]]
+
+    m0, m1 = int(first_rounds(trs[0].view).max()), int(first_rounds(trs[1].view).max())
+    assert m0 != m1
+    lo, hi = sorted((m0, m1))
+    prof.gpu_memory_capacity = (lo + hi) // 2 * prof.kv_bytes_per_token  # degree 1: one worker's capacity
+    bad = 0 if m0 > m1 else 1
+    settings = [abi.default_params(), abi.default_params(alpha=0.5)]
+    with pytest.raises(native.ConfigError) as ei:
+        ctx.sweep([t.view for t in trs], plan, prof, settings, 1)
+    if refbind.available():
+        with pytest.raises(refbind.RefError) as er:
+            refbind.run(trs[bad].view, plan, prof, settings[0], 1)
+        assert str(er.value).split("] ", 1)[1] in str(ei.value)
+    sid = np.ctypeslib.as_array(trs[bad].view.session_id, shape=(trs[bad].view.n_sessions,))
+    first = int(np.argmax(first_rounds(trs[bad].view) * prof.kv_bytes_per_token > prof.gpu_memory_capacity))
+    assert f"session {int(sid[first])} first-round KV" in str(ei.value)
+    # nothing stays staged after the failure
+    ctx._staged = (len(trs), len(settings))
+    with pytest.raises(native.ConfigError):
+        ctx.search_staged(1)
+
+
+@pytest.mark.gpu
+def test_report_on_10k_session_trace(ctx):
+    """Report mode on a trace with ~2M decode tokens: the ITL-gap histogram is
+    sized from the staged traces (2x the decode tokens), so a long replay
+    never overflows it, and every report equals the reference's."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    from paper_2602_14516_b200 import workloads
+    prof = workloads.model_profile("llama3-8b")
+    tr = native.gen_trace(native.preset_stats("toolbench"), 16.0, 10000, 5)
+    plans = [abi.make_plan({4: 1}, {4: 1}), abi.make_plan({1: 2}, {2: 3})]
+    res = ctx.plan_search([tr.view], plans, prof, abi.default_params(), 1, report=True)
+    for c, plan in enumerate(plans):
+        assert res.reports[c].as_tuple() == refbind.report(tr.view, plan, prof, abi.default_params(), 1).as_tuple(), c
