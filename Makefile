@@ -5,53 +5,56 @@ CXX       ?= g++
 PKG       := paper_2602_14516_b200
 CSRC      := $(PKG)/csrc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
+# EXTRA: defines for an A/B variant build (tools/build_variant.sh), e.g. -DPDG_ARRWIN=0
+EXTRA     ?=
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
-             -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC)
-HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC)
+             -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA)
+HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC) $(EXTRA)
 # nlohmann/json 3.11 (header-only; the copy cudnn_frontend vendors in the venv)
 JSON_DIR  ?= $(shell python3 -c "import sysconfig,os;print(os.path.join(sysconfig.get_paths()['purelib'],'include/cudnn_frontend/thirdparty/nlohmann'))" 2>/dev/null)
 HDRS      := include/pdsim_gpu.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp)
 CPPHDRS   := $(wildcard include/pdsim/*.hpp)
 
-LIB       := $(PKG)/libpdsim_gpu.so
+BUILD     ?= $(PKG)/build
+LIB       ?= $(PKG)/libpdsim_gpu.so
 HOSTSIM   := tests/native/libhostsim.so
 CPPTEST   := tests/native/cpp_api_test
 
 all: $(LIB) $(HOSTSIM) $(CPPTEST) oracle refsuites
 
-$(PKG)/build/capi.o: $(CSRC)/capi.cu $(HDRS)
-	@mkdir -p $(PKG)/build
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(PKG)/build/ptxas.log || (cat $(PKG)/build/ptxas.log; false)
+$(BUILD)/capi.o: $(CSRC)/capi.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas.log || (cat $(BUILD)/ptxas.log; false)
 
-$(PKG)/build/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
-	@mkdir -p $(PKG)/build
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(PKG)/build/ptxas_l$*.log || (cat $(PKG)/build/ptxas_l$*.log; false)
+$(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_l$*.log || (cat $(BUILD)/ptxas_l$*.log; false)
 
-$(PKG)/build/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 
-$(PKG)/build/planner_host.o: $(CSRC)/planner_host.cpp $(HDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/planner_host.o: $(CSRC)/planner_host.cpp $(HDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 
-$(PKG)/build/pdsim_cpp.o: $(CSRC)/pdsim_cpp.cpp $(HDRS) $(CPPHDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/pdsim_cpp.o: $(CSRC)/pdsim_cpp.cpp $(HDRS) $(CPPHDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
 
-$(PKG)/build/policy_host.o: $(CSRC)/policy_host.cpp $(CPPHDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/policy_host.o: $(CSRC)/policy_host.cpp $(CPPHDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -std=c++20 -c $< -o $@
 
-$(PKG)/build/metrics_io.o: $(CSRC)/metrics_io.cpp $(CPPHDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/metrics_io.o: $(CSRC)/metrics_io.cpp $(CPPHDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -std=c++20 -I$(JSON_DIR) -c $< -o $@
 
-$(PKG)/build/doc_io.o: $(CSRC)/doc_io.cpp $(CPPHDRS)
-	@mkdir -p $(PKG)/build
+$(BUILD)/doc_io.o: $(CSRC)/doc_io.cpp $(CPPHDRS)
+	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -std=c++20 -I$(JSON_DIR) -c $< -o $@
 
-$(LIB): $(PKG)/build/capi.o $(PKG)/build/replay_l0.o $(PKG)/build/replay_l1.o $(PKG)/build/replay_l2.o $(PKG)/build/host_gen.o $(PKG)/build/planner_host.o $(PKG)/build/pdsim_cpp.o $(PKG)/build/policy_host.o $(PKG)/build/metrics_io.o $(PKG)/build/doc_io.o
+$(LIB): $(BUILD)/capi.o $(BUILD)/replay_l0.o $(BUILD)/replay_l1.o $(BUILD)/replay_l2.o $(BUILD)/host_gen.o $(BUILD)/planner_host.o $(BUILD)/pdsim_cpp.o $(BUILD)/policy_host.o $(BUILD)/metrics_io.o $(BUILD)/doc_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 # C++ drop-in API check program (links the product library; runs on a GPU box).
@@ -87,6 +90,6 @@ refsuites:
 endif
 
 clean:
-	rm -rf $(PKG)/build $(LIB) $(HOSTSIM) $(CPPTEST)
+	rm -rf $(BUILD) $(LIB) $(HOSTSIM) $(CPPTEST)
 
 .PHONY: all oracle clean refsuites

@@ -351,13 +351,9 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
     d.reserved = 0;
     d.ttft_thres = t.ttft_thres;
     d.itl_thres = t.itl_thres;
-    d.arrival = static_cast<const double*>(put(t.arrival.data(), t.arrival.size() * 8));
-    d.round_off = static_cast<const int32_t*>(put(t.round_off.data(), t.round_off.size() * 4));
-    d.incr = static_cast<const int32_t*>(put(t.incr.data(), t.incr.size() * 4));
-    d.dec = static_cast<const int32_t*>(put(t.dec.data(), t.dec.size() * 4));
-    d.delay = static_cast<const double*>(put(t.delay.data(), t.delay.size() * 8));
+    d.ss = static_cast<const pdg::SessTr*>(put(t.stab.data(), t.stab.size() * sizeof(pdg::SessTr)));
+    d.rr = static_cast<const pdg::RoundTr*>(put(t.rtab.data(), t.rtab.size() * sizeof(pdg::RoundTr)));
     d.sid = static_cast<const int64_t*>(put(t.sid.data(), t.sid.size() * 8));
-    d.rank = static_cast<const int32_t*>(put(t.rank.data(), t.rank.size() * 4));
     d.by_rank = static_cast<const int32_t*>(put(t.by_rank.data(), t.by_rank.size() * 4));
   }
   CU(ctx, cudaMemcpyAsync(ctx->d_trace_data.p, host.data(), off, cudaMemcpyHostToDevice, ctx->stream));

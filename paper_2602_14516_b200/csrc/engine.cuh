@@ -184,6 +184,25 @@ struct HEv {
   uint32_t b;
 };
 
+// Trace records, one 128-bit load each (workload.hpp:28-39 re-laid for the
+// device). Per session: arrival time, offset of its first round, rank of its
+// id among all ids. Per round: the Round's three fields.
+struct alignas(16) SessTr {
+  double arrival;
+  int32_t round_off;
+  int32_t rank;
+};
+struct alignas(16) RoundTr {
+  int32_t incr;
+  int32_t dec;
+  double delay;
+};
+static_assert(sizeof(SessTr) == 16 && sizeof(RoundTr) == 16, "trace records are one 128-bit load");
+
+// Session-table length: S + 1 entries (entry S holds the round count as its
+// round_off, so session i's rounds are [ss[i].round_off, ss[i+1].round_off)).
+PDG_HD int64_t sess_table_len(int64_t S) { return S + 1; }
+
 // Packed read-only trace (one per replica, shared by all candidates).
 struct DevTrace {
   int32_t S;
@@ -192,14 +211,10 @@ struct DevTrace {
   int32_t reserved;
   double ttft_thres;
   double itl_thres;
-  const double* arrival;     // [S]
-  const int32_t* round_off;  // [S+1]
-  const int32_t* incr;       // [R]
-  const int32_t* dec;        // [R]
-  const double* delay;       // [R]
+  const SessTr* ss;          // [sess_table_len(S)]; entry S: round_off = R
+  const RoundTr* rr;         // [R]
   const int64_t* sid;        // [S]
-  const int32_t* rank;       // [S] rank of session_id among all ids
-  const int32_t* by_rank;    // [S] inverse of rank
+  const int32_t* by_rank;    // [S] session of each id rank
 };
 
 // Worker layout of a candidate (sim_engine.cpp:175-203): prefill workers
@@ -238,8 +253,11 @@ struct SessRt {
   int8_t bound;      // decode worker index
   int8_t postpone;   // PrefillTask::postpone_count
   int8_t ttft_bad;   // some TTFT > threshold
-  int8_t reserved[7];
+  int8_t reserved;
+  int16_t nround;    // the session's round count (cached at admission)
+  int32_t roff;      // index of its first round in the round table (cached at admission)
 };
+static_assert(sizeof(SessRt) == 80, "SessRt layout");
 
 // A worker's task queue (global ring) + exact sum of the queued costs.
 struct TaskQueue {
@@ -381,14 +399,13 @@ struct SmemOff {
   size_t dw, pw, mt, order, heap;
 };
 PDG_HD constexpr SmemOff smem_off(size_t dres, size_t pres) {
-  return SmemOff{smem_a16(kEngStateBytes), smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres),
-                 smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) + sizeof(PrefillW) * pres),
-                 smem_a16(smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) + sizeof(PrefillW) * pres) +
-                          8 * 312),
-                 smem_a16(smem_a16(smem_a16(smem_a16(smem_a16(kEngStateBytes) + sizeof(DecodeW) * dres) +
-                                             sizeof(PrefillW) * pres) +
-                                    8 * 312) +
-                          4 * kMaxSlots)};
+  return SmemOff{smem_a16(kEngStateBytes),
+                 smem_a16(kEngStateBytes) + smem_a16(sizeof(DecodeW) * dres),
+                 smem_a16(kEngStateBytes) + smem_a16(sizeof(DecodeW) * dres) + smem_a16(sizeof(PrefillW) * pres),
+                 smem_a16(kEngStateBytes) + smem_a16(sizeof(DecodeW) * dres) + smem_a16(sizeof(PrefillW) * pres) +
+                     smem_a16(8 * 312),
+                 smem_a16(kEngStateBytes) + smem_a16(sizeof(DecodeW) * dres) + smem_a16(sizeof(PrefillW) * pres) +
+                     smem_a16(8 * 312) + smem_a16(4 * kMaxSlots)};
 }
 
 PDG_HD size_t smem_slot_bytes(const Caps& c, SmemSlot* s, char* base) {
@@ -567,6 +584,8 @@ struct EngState {
   double now_;
   double next_arr_t_;
   uint64_t seq_;
+  int32_t next_arr_roff_;  // round offset of the next arrival
+  int32_t next_arr_pad_;
   int32_t hn_;
   int32_t heap_spilled_;
   int32_t hsmall_;  // session events form an unordered set of <= kSmallHeap entries in shared memory
@@ -625,6 +644,8 @@ inline const pdsim_profile*& host_profile() {  // host (test) builds only
 #endif
 
 static_assert(sizeof(EngState) <= kEngStateBytes, "EngState outgrew its shared-memory reservation");
+
+
 static_assert(kEngStateBytes % 16 == 0, "slot layout alignment");
 
 #if defined(__CUDA_ARCH__)
@@ -765,13 +786,19 @@ class EngineT {
         break;
       }
       if (src == 2) {
-        const int32_t i = s_->next_arr_++;
-        const double t = s_->next_arr_t_;
-        if (s_->next_arr_ < s_->T.S) s_->next_arr_t_ = GLP(s_->T.arrival)[s_->next_arr_];
+        const int32_t i = next_arr;
+        const double t = next_arr_t;
+        const int32_t roff = s_->next_arr_roff_;
+        // the next cursor entry (one 128-bit load): its round offset also
+        // ends session i's round range
+        const SessTr nx = sess_tr(i + 1);
+        s_->next_arr_ = i + 1;
+        s_->next_arr_t_ = nx.arrival;
+        s_->next_arr_roff_ = nx.round_off;
         s_->cur_kind_ = kArrival;
         if (prof) prof_switch(&tp, &bucket, kProfArrival);
         advance_to(t);
-        on_arrival(i);
+        on_arrival(i, roff, nx.round_off - roff);
         continue;
       }
       const uint32_t kind = static_cast<uint32_t>(bk >> 58);
@@ -957,23 +984,32 @@ class EngineT {
     *bucket = next;
   }
 
+  // Writes this pair's result to *out (global memory on the device; lane 0
+  // stores, the warp re-converges after).
   PDG_HD void finish_result(PairResult* out) {
-    for (int d = 0; d < s_->PL.D; ++d) s_->ctr_.kv_bytes_residual += DW(d).kv_used;
-    out->att = s_->att_;
-    out->att.sessions_total = s_->T.S;
-    out->ctr = s_->ctr_;
-    out->n_decisions = s_->n_dec_;
-    out->n_ttft = s_->n_ttft_;
-    out->n_steps = s_->n_steps_;
-    out->n_spans = s_->n_spans_;
-    out->events = s_->events_;
-    out->exact_folds = s_->folds_;
-    out->status = s_->failed_ ? PDSIM_PAIR_ERROR : s_->pruned_ ? PDSIM_PAIR_PRUNED : PDSIM_PAIR_OK;
-    out->attempts = s_->attempts_;
-    for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
-      out->prof_cycles[j] = s_->prof_c_[j];
-      out->prof_count[j] = s_->prof_n_[j];
+    int64_t kv_res = s_->ctr_.kv_bytes_residual;
+    for (int d = 0; d < s_->PL.D; ++d) kv_res += DW(d).kv_used;
+    warp_sync();
+    if (lane_id() == 0) {
+      out->att = s_->att_;
+      out->att.sessions_total = s_->T.S;
+      out->ctr = s_->ctr_;
+      out->ctr.kv_bytes_residual = kv_res;
+      out->n_decisions = s_->n_dec_;
+      out->n_ttft = s_->n_ttft_;
+      out->n_steps = s_->n_steps_;
+      out->n_spans = s_->n_spans_;
+      out->events = s_->events_;
+      out->exact_folds = s_->folds_;
+      out->status = s_->failed_ ? PDSIM_PAIR_ERROR : s_->pruned_ ? PDSIM_PAIR_PRUNED : PDSIM_PAIR_OK;
+      out->attempts = s_->attempts_;
+      out->cycles = 0;
+      for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) {
+        out->prof_cycles[j] = kProf ? s_->prof_c_[j] : 0;
+        out->prof_count[j] = kProf ? s_->prof_n_[j] : 0;
+      }
     }
+    warp_sync();
   }
 
  private:
@@ -1049,6 +1085,37 @@ class EngineT {
   HEv* SHEAP() const { return s_->SM.heap; }
 #endif
 
+  // ---- trace records (one 128-bit read-only load each) ----
+  PDG_HD static SessTr ld_sess(const SessTr* p) {
+#if defined(__CUDA_ARCH__)
+    const int4 v = __ldg(reinterpret_cast<const int4*>(p));
+    SessTr r;
+    r.arrival = __hiloint2double(v.y, v.x);
+    r.round_off = v.z;
+    r.rank = v.w;
+    return r;
+#else
+    return *p;
+#endif
+  }
+  PDG_HD static RoundTr ld_round(const RoundTr* p) {
+#if defined(__CUDA_ARCH__)
+    const int4 v = __ldg(reinterpret_cast<const int4*>(p));
+    RoundTr r;
+    r.incr = v.x;
+    r.dec = v.y;
+    r.delay = __hiloint2double(v.w, v.z);
+    return r;
+#else
+    return *p;
+#endif
+  }
+  PDG_HD SessTr sess_tr(int32_t i) const { return ld_sess(GLP(s_->T.ss) + i); }
+  PDG_HD RoundTr round_tr(int32_t ridx) const { return ld_round(GLP(s_->T.rr) + ridx); }
+  // Round `round` (1-based) of admitted session i (its round offset is cached in SessRt).
+  PDG_HD RoundTr round_of(int32_t i, int round) const { return round_tr(GLP(s_->G.sess)[i].roff + round - 1); }
+
+
   PDG_HD void advance_to(double t) {
     if (t < s_->now_) s_->ctr_.events_in_order = 0;  // sim_engine.cpp:148-150
     s_->now_ = t;
@@ -1061,7 +1128,11 @@ class EngineT {
     s_->heap_spilled_ = false;
     s_->hsmall_ = 1;
     s_->next_arr_ = 0;
-    s_->next_arr_t_ = s_->T.S > 0 ? GLP(s_->T.arrival)[0] : 0.0;
+    {
+      const SessTr e0 = sess_tr(0);
+      s_->next_arr_t_ = s_->T.S > 0 ? e0.arrival : 0.0;
+      s_->next_arr_roff_ = e0.round_off;
+    }
     s_->adm_head_ = 0;
     s_->rr_next_ = 0;
     s_->ctr_.events_in_order = 1;
@@ -1161,9 +1232,9 @@ class EngineT {
     return curve_eval(PDG_PROF.kv[src][dst], static_cast<double>(l));
   }
 
-  PDG_HD int32_t l_incr_of(int32_t i) const { return GLP(s_->T.incr)[GLP(s_->T.round_off)[i] + GLP(s_->G.sess)[i].round - 1]; }
-  PDG_HD double created_of(int32_t i) const {
-    return GLP(s_->G.sess)[i].round == 1 ? GLP(s_->T.arrival)[i] : GLP(s_->G.sess)[i].t_enq;  // sim_engine.cpp:258, 283, 588
+  PDG_HD int32_t l_incr_of(int32_t i) const {
+    const SessRt& s = GLP(s_->G.sess)[i];
+    return round_tr(s.roff + s.round - 1).incr;
   }
 
   // ---- RNG (coordinator.cpp:124-130): std::mt19937_64 in shared memory ----
@@ -1453,9 +1524,9 @@ class EngineT {
   }
 
   // ---- admission (sim_engine.cpp:240-267; bind_session coordinator.cpp:60-72) ----
-  PDG_HD void on_arrival(int32_t i) {
+  PDG_HD void on_arrival(int32_t i, int32_t roff, int32_t nround) {
     if (s_->adm_head_ < i) return;  // queue non-empty: park behind the head
-    if (!try_admit(i)) return;  // parked: s_->adm_head_ == i
+    if (!try_admit(i, roff, nround)) return;  // parked: s_->adm_head_ == i
     s_->adm_head_ = i + 1;
   }
 
@@ -1554,14 +1625,17 @@ class EngineT {
     return total;
   }
 
-  PDG_COLD bool try_admit(int32_t i) {
+  PDG_COLD bool try_admit(int32_t i, int32_t roff, int32_t nround) {
     int64_t kv_best;
+    const RoundTr r1 = round_tr(roff);
     const int best = bind_session(&kv_best);
     const DecodeW& w = DW(best);
-    const int64_t first = static_cast<int64_t>(GLP(s_->T.incr)[GLP(s_->T.round_off)[i]]) * PDG_PROF.kv_bytes_per_token;
+    const int64_t first = static_cast<int64_t>(r1.incr) * PDG_PROF.kv_bytes_per_token;
     if (kv_best + first > w.kv_cap) return false;
     SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
+      s.roff = roff;
+      s.nround = static_cast<int16_t>(nround);
       s.bound = static_cast<int8_t>(best);
       s.bind_time = s_->now_;
       s.round = 1;
@@ -1574,23 +1648,27 @@ class EngineT {
       s.postpone = 0;
       s.ttft_bad = 0;
     }
-    start_round(i, 1, best, 0);
+    start_round(i, 1, best, 0, r1.incr);
     return true;
   }
 
   PDG_HD void admit_waiting() {
-    while (s_->adm_head_ < s_->next_arr_ && try_admit(s_->adm_head_)) ++s_->adm_head_;
+    while (s_->adm_head_ < s_->next_arr_) {
+      const int32_t i = s_->adm_head_;
+      const int32_t roff = sess_tr(i).round_off;
+      if (!try_admit(i, roff, sess_tr(i + 1).round_off - roff)) break;
+      ++s_->adm_head_;
+    }
   }
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
-  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx) {
+  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx, int32_t incr) {
     SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.t_enq = s_->now_;
       s.postpone = 0;
     }
     ++s_->ctr_.tasks_created;
-    const int32_t incr = GLP(s_->T.incr)[GLP(s_->T.round_off)[i] + round - 1];
     const int64_t tr0 = pb();
     const RouteOut r = decide(i, bound, ctx, incr);
     pe(kProfRoute, tr0);
@@ -1637,12 +1715,15 @@ class EngineT {
       r.rationale = PDSIM_RATIONALE_FORCED_REMOTE;
       return r;
     }
-    route(bound, ctx, incr, &r);
-    return r;
+    return route(bound, ctx, incr);
   }
 
   // Coordinator::route (coordinator.cpp:115-171).
-  PDG_COLD void route(int bound, int32_t ctx, int32_t incr, RouteOut* r) {
+  // Returns the decision by value (registers across the call: no stack).
+  PDG_COLD RouteOut route(int bound, int32_t ctx, int32_t incr) {
+    RouteOut r;
+    r.has_est = 0;
+    r.est = 0.0;
     const int n = s_->PL.P;
     if (n > 0) {
 #if defined(__CUDA_ARCH__)
@@ -1691,21 +1772,22 @@ class EngineT {
       for (int k = 0; k < n; ++k) {
         const int p = packed ? static_cast<int>((perm >> (4 * k)) & 15u) : order[k];
         if (ttft_has_slack(p, thr)) {
-          r->local = 0;
-          r->p = p;
-          r->rationale = PDSIM_RATIONALE_SLACK_REMOTE;
-          return;
+          r.local = 0;
+          r.p = p;
+          r.rationale = PDSIM_RATIONALE_SLACK_REMOTE;
+          return r;
         }
       }
     }
     if (itl_has_slack(bound, dmul(s_->PR.beta, s_->T.itl_thres))) {
-      r->local = 1;
-      r->p = -1;
-      r->rationale = PDSIM_RATIONALE_SLACK_LOCAL;
-      return;
+      r.local = 1;
+      r.p = -1;
+      r.rationale = PDSIM_RATIONALE_SLACK_LOCAL;
+      return r;
     }
-    r->rationale = PDSIM_RATIONALE_ARGMIN;
-    argmin_route(bound, ctx, incr, r);
+    r = argmin_route(bound, ctx, incr);
+    r.rationale = PDSIM_RATIONALE_ARGMIN;
+    return r;
   }
 
   // ---- routing estimates (coordinator.cpp:74-100) ----
@@ -1757,7 +1839,7 @@ class EngineT {
   // candidates in parallel; a candidate whose bracket starts above the
   // smallest upper bound cannot win, and exact folds run only when two or
   // more candidates remain in contention.
-  PDG_COLD void argmin_route(int d, int32_t ctx, int32_t incr, RouteOut* r) {
+  PDG_COLD RouteOut argmin_route(int d, int32_t ctx, int32_t incr) {
     // prefill candidates per lane: the compiled layout bounds P by kP
     constexpr int kPer = ((kP > 0 ? kP : kMaxSlots) + PDG_NL - 1) / PDG_NL;
     const int n = s_->PL.P;
@@ -1838,10 +1920,13 @@ class EngineT {
       estimate(d, ctx, incr, winner, true, &a, &b, &e);
       est = a;
     }
-    r->local = winner < 0 ? 1 : 0;
-    r->p = winner < 0 ? -1 : winner;
-    r->has_est = 1;
-    r->est = est;
+    RouteOut r;
+    r.local = winner < 0 ? 1 : 0;
+    r.p = winner < 0 ? -1 : winner;
+    r.rationale = PDSIM_RATIONALE_ARGMIN;
+    r.has_est = 1;
+    r.est = est;
+    return r;
   }
 
   // ---- windowed statistics (coordinator.cpp:27-47) ----
@@ -2475,7 +2560,9 @@ class EngineT {
   PDG_HD void complete_task_(int32_t i, bool local, int p, int d) {
     SessRt& s = GLP(s_->G.sess)[i];
     const int round = s.round;
-    const double created = round == 1 ? GLP(s_->T.arrival)[i] : s.t_enq;
+    const SessTr st = sess_tr(i);
+    const RoundTr rt = round_tr(s.roff + round - 1);
+    const double created = round == 1 ? st.arrival : s.t_enq;
     const double value = dsub(s_->now_, created);
     if (!local) ttft_add(p, value);  // decode workers' TTFT windows are never queried
     if (kRec && s_->REC.ttft && lane_id() == 0) {
@@ -2502,14 +2589,13 @@ class EngineT {
       if (local) ++s_->rep_n_local_;
     }
     ++s_->n_ttft_;
-    const int32_t ridx = GLP(s_->T.round_off)[i] + round - 1;
-    const int32_t incr = GLP(s_->T.incr)[ridx];
-    const int32_t dec = GLP(s_->T.dec)[ridx];
+    const int32_t incr = rt.incr;
+    const int32_t dec = rt.dec;
     DecodeW& w = DW(d);
     interrupt_run(d);
     const int32_t join = w.steps;  // first token in the next step started
     const uint64_t key =
-        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(GLP(s_->T.rank)[i]);
+        (static_cast<uint64_t>(static_cast<uint32_t>(join + dec - 1)) << 32) | static_cast<uint32_t>(st.rank);
     warp_sync();
     const int32_t hint = w.seg_end;
     if (kPrune) {
@@ -2778,8 +2864,8 @@ class EngineT {
       fh_pop(d);
       const int32_t i = GLP(s_->T.by_rank)[rank];
       SessRt& s = GLP(s_->G.sess)[i];
-      const int32_t ridx = GLP(s_->T.round_off)[i] + s.round - 1;
-      const int32_t dec = GLP(s_->T.dec)[ridx];
+      const RoundTr rt = round_tr(s.roff + s.round - 1);
+      const int32_t dec = rt.dec;
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
       double sum = s.itl_sum;
       double ilo = s.itl_lo, ihi = s.itl_hi;
@@ -2808,7 +2894,7 @@ class EngineT {
         }
         s_->n_spans_ = nsp + 1;  // warp-uniform store
       }
-      const bool last = s.round == GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
+      const bool last = s.round == s.nround;
       {  // warp-uniform stores (every lane writes the same values)
         s.itl_sum = sum;
         s.itl_lo = ilo;
@@ -2821,7 +2907,7 @@ class EngineT {
         terminate_session(i, d);
         any_terminated = true;
       } else {
-        heap_push(dadd(s_->now_, GLP(s_->T.delay)[ridx]), kInteractionDone, static_cast<uint32_t>(i), 0u);
+        heap_push(dadd(s_->now_, rt.delay), kInteractionDone, static_cast<uint32_t>(i), 0u);
       }
       pe(kProfFinisher, tf0);
     }
@@ -2834,8 +2920,9 @@ class EngineT {
     const int round = s.round + 1;
     const int bound = s.bound;
     const int32_t ctx = s.ctx;
+    const int32_t incr = round_tr(s.roff + round - 1).incr;
     s.round = static_cast<int16_t>(round);  // warp-uniform store
-    start_round(i, round, bound, ctx);
+    start_round(i, round, bound, ctx, incr);
   }
 
   // terminate_session + slo_verdict (sim_engine.cpp:591-607, 668-674).
@@ -2861,16 +2948,18 @@ class EngineT {
     {  // warp-uniform stores (every lane writes the same values)
       DW(d).kv_used -= static_cast<int64_t>(ctx) * PDG_PROF.kv_bytes_per_token;
       if (kRec && s_->C.rep_gapcap > 0 && lane_id() == 0) {
-        GLP(s_->G.rep_e2e)[GLP(s_->T.rank)[i]] = dsub(s_->now_, GLP(s_->T.arrival)[i]);
+        const SessTr st = sess_tr(i);
+        GLP(s_->G.rep_e2e)[st.rank] = dsub(s_->now_, st.arrival);
       }
       if (kRec && s_->REC.sessions) {
         pdsim_session_outcome& o = s_->REC.sessions[s_->att_.sessions_completed];
+        const double arrival = sess_tr(i).arrival;
         o.session_id = GLP(s_->T.sid)[i];
-        o.arrival_time = GLP(s_->T.arrival)[i];
+        o.arrival_time = arrival;
         o.completion_time = s_->now_;
-        o.admission_wait = dsub(s.bind_time, GLP(s_->T.arrival)[i]);
+        o.admission_wait = dsub(s.bind_time, arrival);
         o.mean_itl = mean_itl;
-        o.rounds = GLP(s_->T.round_off)[i + 1] - GLP(s_->T.round_off)[i];
+        o.rounds = s.nround;
         o.ttft_ok = ttft_ok;
         o.itl_ok = itl_ok;
         o.slo_ok = slo_ok;

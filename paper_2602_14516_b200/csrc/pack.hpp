@@ -139,9 +139,11 @@ struct PackedTrace {
   std::vector<int32_t> round_off, incr, dec, rank, by_rank;
   std::vector<int64_t> sid;
   std::vector<int64_t> first_round_incr;  // for the KV precheck
-  size_t device_bytes() const {
-    return arrival.size() * 8 + delay.size() * 8 + round_off.size() * 4 + incr.size() * 4 +
-           dec.size() * 4 + rank.size() * 4 + by_rank.size() * 4 + sid.size() * 8;
+  // the replay engine's record tables (engine.cuh SessTr / RoundTr)
+  std::vector<SessTr> stab;   // [sess_table_len(S)]
+  std::vector<RoundTr> rtab;  // [R]
+  size_t device_bytes() const {  // what the replay engine reads from HBM
+    return stab.size() * sizeof(SessTr) + rtab.size() * sizeof(RoundTr) + by_rank.size() * 4 + sid.size() * 8;
   }
 };
 
@@ -221,6 +223,16 @@ inline bool pack_trace(const pdsim_trace& t, PackedTrace* out, HostError* err) {
             [&](int32_t a, int32_t b) { return t.session_id[a] < t.session_id[b]; });
   out->rank.resize(static_cast<size_t>(S));
   for (int32_t k = 0; k < static_cast<int32_t>(S); ++k) out->rank[static_cast<size_t>(out->by_rank[k])] = k;
+  out->stab.assign(static_cast<size_t>(sess_table_len(S)), SessTr{0.0, static_cast<int32_t>(R), 0});
+  for (int64_t i = 0; i < S; ++i) {
+    out->stab[static_cast<size_t>(i)] = SessTr{out->arrival[static_cast<size_t>(i)], out->round_off[static_cast<size_t>(i)],
+                                              out->rank[static_cast<size_t>(i)]};
+  }
+  out->rtab.resize(static_cast<size_t>(R));
+  for (int64_t r = 0; r < R; ++r) {
+    out->rtab[static_cast<size_t>(r)] = RoundTr{out->incr[static_cast<size_t>(r)], out->dec[static_cast<size_t>(r)],
+                                               out->delay[static_cast<size_t>(r)]};
+  }
   return true;
 }
 

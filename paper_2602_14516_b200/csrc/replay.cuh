@@ -43,6 +43,25 @@ struct KernelArgs {
   const int64_t* pair_list;            // optional: the launch replays pair_list[0 .. pair_end - pair_begin)
 };
 
+// Result of a pair that is not replayed (pruned / invalid), field by field.
+__device__ __forceinline__ void write_empty_result(PairResult* out, int32_t status, int64_t sessions) {
+  out->att.sessions_total = sessions;
+  out->att.sessions_completed = out->att.slo_ok = out->att.ttft_ok = out->att.itl_ok = 0;
+  out->ctr.tasks_created = out->ctr.tasks_completed = out->ctr.tokens_decoded = out->ctr.kv_bytes_residual = 0;
+  out->ctr.max_postpone_observed = out->ctr.events_in_order = 0;
+  out->n_decisions = out->n_ttft = out->n_steps = out->n_spans = out->events = out->cycles = out->exact_folds = 0;
+  out->status = status;
+  out->attempts = 0;
+  for (int j = 0; j < PDSIM_PROF_BUCKETS; ++j) out->prof_cycles[j] = out->prof_count[j] = 0;
+}
+__device__ __forceinline__ void write_empty_report(pdsim_report* rep, int64_t sessions) {
+  pdsim_report z;
+  memset(&z, 0, sizeof(z));
+  z.sessions_total = sessions;
+  z.empty = 1;
+  *rep = z;
+}
+
 // One warp per block; the warp replays pairs pulled from an atomic queue.
 // kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
 // addresses slot state at compile-time offsets (engine.cuh smem_off).
@@ -73,25 +92,20 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
     const int64_t pair = a.pair_list ? a.pair_list[idx] : a.pair_begin + idx;
     const int32_t c = static_cast<int32_t>(pair / a.n_traces);
     const int32_t r = static_cast<int32_t>(pair % a.n_traces);
-    PairResult res;
-    memset(&res, 0, sizeof(res));
-    bool skip = false;
+    // Per-pair result: written straight to a.results[idx] by lane 0 (no
+    // local copy); the counters the reduction needs are read back after.
+    PairResult* out = a.results + idx;
     if (kPrune) {  // a dead candidate's remaining replicas are not replayed
       const unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(a.best_key);
-      skip = (*reinterpret_cast<volatile int*>(&a.cand_bad[c]) & 2) || prune_dominated(a.total_sessions, key, c);
+      if ((*reinterpret_cast<volatile int*>(&a.cand_bad[c]) & 2) || prune_dominated(a.total_sessions, key, c)) {
+        if (lane == 0) write_empty_result(out, PDSIM_PAIR_PRUNED, a.traces[r].S);
+        goto reduce;
+      }
     }
-    if (skip) {
-      res.status = PDSIM_PAIR_PRUNED;
-      res.att.sessions_total = a.traces[r].S;
-    } else if (a.pair_invalid[pair]) {
-      res.status = PDSIM_PAIR_INVALID;
-      res.att.sessions_total = a.traces[r].S;
-      if (a.reports && lane == 0) {
-        pdsim_report rep;
-        memset(&rep, 0, sizeof(rep));
-        rep.sessions_total = a.traces[r].S;
-        rep.empty = 1;
-        a.reports[idx] = rep;
+    if (a.pair_invalid[pair]) {
+      if (lane == 0) {
+        write_empty_result(out, PDSIM_PAIR_INVALID, a.traces[r].S);
+        if (a.reports) write_empty_report(a.reports + idx, a.traces[r].S);
       }
     } else {
       const DevTrace tr = a.traces[r];
@@ -119,29 +133,31 @@ __global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
       }
       EngineT<kProf, kD, kP, kRec, true, kPrune> eng(sslot.es, tr, pl, prm, a.caps, sslot, gslot, a.rec, a.seed, kProf ? 1 : 0,
                                        &prn);
-      eng.run(&res);
-      res.cycles = clock64() - t0;
+      eng.run(out);
+      if (lane == 0) out->cycles = clock64() - t0;
       if (kRec && a.reports) {
         pdsim_report rep;
         eng.build_report(&rep);
         if (lane == 0) a.reports[idx] = rep;
       }
     }
+  reduce:
+    __syncwarp();
     if (lane == 0) {
-      a.results[idx] = res;
-      if (res.status == PDSIM_PAIR_PRUNED) {
+      const int32_t status = out->status;
+      const int64_t slo_ok = out->att.slo_ok, total = out->att.sessions_total;
+      if (status == PDSIM_PAIR_PRUNED) {
         atomicOr(&a.cand_bad[c], 2);
-      } else if (res.status != PDSIM_PAIR_OK) {
+      } else if (status != PDSIM_PAIR_OK) {
         atomicOr(&a.cand_bad[c], 1);
       } else {
-        const unsigned long long old = atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(res.att.slo_ok));
+        const unsigned long long old = atomicAdd(&a.cand_sum[c], static_cast<unsigned long long>(slo_ok));
         if (kPrune) {  // final counts join the replicas' bounds
-          atomicMax(&a.pair_ok[pair], static_cast<int32_t>(res.att.slo_ok));
-          atomicMax(&a.pair_fail[pair],
-                    static_cast<int32_t>(res.att.sessions_total - res.att.slo_ok));
+          atomicMax(&a.pair_ok[pair], static_cast<int32_t>(slo_ok));
+          atomicMax(&a.pair_fail[pair], static_cast<int32_t>(total - slo_ok));
         }
         if (kPrune && !a.cand_invalid[c]) {  // completed replicas: a lower bound of c's count
-          const unsigned long long lb = old + static_cast<unsigned long long>(res.att.slo_ok);
+          const unsigned long long lb = old + static_cast<unsigned long long>(slo_ok);
           atomicMax(a.best_key, ((lb + 1ull) << 32) | (0xffffffffull - static_cast<unsigned>(c)));
         }
       }

@@ -185,4 +185,10 @@ def c2_small():
     return build(specs.c2_small())
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C4": c4, "C5": c5}
+def c3_small():
+    """C3 with 10 000-session replicas: the same 2704 pairs and per-SM
+    concurrency, a fifth of the events (profiling only)."""
+    return c3(sessions=10000)
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C2s": c2_small, "C3": c3, "C3s": c3_small, "C4": c4, "C5": c5}

@@ -66,13 +66,9 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   dt.reserved = 0;
   dt.ttft_thres = t.ttft_thres;
   dt.itl_thres = t.itl_thres;
-  dt.arrival = t.arrival.data();
-  dt.round_off = t.round_off.data();
-  dt.incr = t.incr.data();
-  dt.dec = t.dec.data();
-  dt.delay = t.delay.data();
+  dt.ss = t.stab.data();
+  dt.rr = t.rtab.data();
   dt.sid = t.sid.data();
-  dt.rank = t.rank.data();
   dt.by_rank = t.by_rank.data();
   const pdg::DevParams dprm = pdg::to_dev_params(*params);
   pdg::Records rec{out->decisions, out->ttft_samples, out->sessions, nullptr, nullptr, 0};

@@ -1,7 +1,7 @@
-"""A/B kernel timing of two builds of libpdsim_gpu.so on the same box:
-alternates runs of the staged C2 search in fresh processes.
+"""A/B kernel timing of several builds of libpdsim_gpu.so on the same box:
+alternates runs of a staged search in fresh processes.
 
-usage: python tools/ab.py LIB_A LIB_B [rounds] [config] [pair_begin] [pair_end]
+usage: python tools/ab.py CONFIG ROUNDS LIB [LIB ...]
 LIB_x is a libpdsim_gpu.so, or a directory holding a whole package copy
 (paper_2602_14516_b200/ with its .so) when the Python bindings differ too.
 """
@@ -22,11 +22,11 @@ print(min(ms))
 '''
 
 
-def main(a, b, rounds=3, cfg="C2", pb="0", pe="-1"):
+def main(libs, rounds=3, cfg="C2", pb="0", pe="-1"):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {a: [], b: []}
+    res = {lib: [] for lib in libs}
     for _ in range(int(rounds)):
-        for lib in (a, b):
+        for lib in libs:
             if os.path.isdir(lib):
                 env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
                 cwd = os.path.abspath(lib)
@@ -36,9 +36,13 @@ def main(a, b, rounds=3, cfg="C2", pb="0", pe="-1"):
             out = subprocess.run([sys.executable, "-c", CHILD, cfg, pb, pe], cwd=cwd, env=env, capture_output=True,
                                  text=True)
             res[lib].append(float(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else None)
+            if out.returncode != 0:
+                print(out.stderr[-2000:], file=sys.stderr)
     for lib, v in res.items():
-        print(cfg, lib, v, "min", min(x for x in v if x is not None))
+        ok = [x for x in v if x is not None]
+        print(cfg, lib, v, "min", min(ok) if ok else None, flush=True)
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    # usage: ab.py CONFIG ROUNDS LIB [LIB ...]
+    main(sys.argv[3:], rounds=sys.argv[2], cfg=sys.argv[1])
