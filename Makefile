@@ -7,8 +7,10 @@ CSRC      := $(PKG)/csrc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 # EXTRA: defines for an A/B variant build (tools/build_variant.sh), e.g. -DPDG_ARRWIN=0
 EXTRA     ?=
+# NVEXTRA: nvcc-only flags of a variant build (e.g. -Xptxas -O2)
+NVEXTRA   ?=
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
-             -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA)
+             -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA) $(NVEXTRA)
 HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC) $(EXTRA)
 # nlohmann/json 3.11 (header-only; the copy cudnn_frontend vendors in the venv)
 JSON_DIR  ?= $(shell python3 -c "import sysconfig,os;print(os.path.join(sysconfig.get_paths()['purelib'],'include/cudnn_frontend/thirdparty/nlohmann'))" 2>/dev/null)
@@ -29,6 +31,13 @@ $(BUILD)/capi.o: $(CSRC)/capi.cu $(HDRS)
 $(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_l$*.log || (cat $(BUILD)/ptxas_l$*.log; false)
+
+# Throughput build of the search kernels: the same sources
+# with the shared hot subroutines kept out of line (smaller I-cache footprint
+# when many warps share an SM), in their own namespace pdg_tp.
+$(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=20 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
 
 $(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(BUILD)
@@ -54,7 +63,7 @@ $(BUILD)/doc_io.o: $(CSRC)/doc_io.cpp $(CPPHDRS)
 	@mkdir -p $(BUILD)
 	$(CXX) $(HOSTFLAGS) -std=c++20 -I$(JSON_DIR) -c $< -o $@
 
-$(LIB): $(BUILD)/capi.o $(BUILD)/replay_l0.o $(BUILD)/replay_l1.o $(BUILD)/replay_l2.o $(BUILD)/host_gen.o $(BUILD)/planner_host.o $(BUILD)/pdsim_cpp.o $(BUILD)/policy_host.o $(BUILD)/metrics_io.o $(BUILD)/doc_io.o
+$(LIB): $(BUILD)/capi.o $(BUILD)/replay_l0.o $(BUILD)/replay_l1.o $(BUILD)/replay_l2.o $(BUILD)/replay_tp_l0.o $(BUILD)/replay_tp_l1.o $(BUILD)/replay_tp_l2.o $(BUILD)/host_gen.o $(BUILD)/planner_host.o $(BUILD)/pdsim_cpp.o $(BUILD)/policy_host.o $(BUILD)/metrics_io.o $(BUILD)/doc_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 # C++ drop-in API check program (links the product library; runs on a GPU box).

@@ -326,6 +326,8 @@ def run_ours(args, rank, world, local):
 
     times, kernel_ms, launches, res, clocks = measure(ctx, wl, pairs, args, stream, flush, world, args.steps,
                                                       args.warmup, clock_index=local)
+    build = {abi.BUILD_LATENCY: "latency (hot subroutines inlined)",
+             abi.BUILD_THROUGHPUT: "throughput (shared hot subroutines out of line)"}.get(ctx.last_kernel_build())
     total_ms = max_over_ranks(sum(times), world)
     rounds_all = all_rounds(wl)
     value = rounds_all * args.steps / (total_ms / 1e3)
@@ -451,7 +453,7 @@ def run_ours(args, rank, world, local):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_launch": bytes_launch, "kernel": "replay_kernel",
+                         "bytes_per_launch": bytes_launch, "kernel": "replay_kernel", "kernel_build": build,
                          "note": "latency-bound serial DES per pair; see DESIGN.md §5 for issue/stall figures"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": te},

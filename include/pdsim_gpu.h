@@ -377,6 +377,17 @@ int pdsim_gpu_search_staged(pdsim_gpu_ctx* ctx, int64_t pair_begin,
  * loses on its own replicas. */
 enum { PDSIM_SEARCH_FULL = 0, PDSIM_SEARCH_ARGMAX = 1 };
 int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode);
+/* Kernel build of attainment-only searches (both builds compile the same
+ * engine source and return identical results). LATENCY inlines every hot
+ * subroutine (fewest instructions per event: few pairs per SM); THROUGHPUT
+ * keeps the subroutines shared by several handlers out of line (smaller
+ * instruction footprint: many warps per SM, where instruction fetch binds,
+ * DESIGN.md §3.1). AUTO (default): THROUGHPUT when a launch replays more than
+ * 8 pairs per SM. Record, report and diagnostics searches use LATENCY. */
+enum { PDSIM_BUILD_AUTO = 0, PDSIM_BUILD_LATENCY = 1, PDSIM_BUILD_THROUGHPUT = 2 };
+int pdsim_gpu_set_kernel_build(pdsim_gpu_ctx* ctx, int build);
+/* Build the context's last replay launch used (LATENCY or THROUGHPUT; 0 before any). */
+int pdsim_gpu_last_kernel_build(const pdsim_gpu_ctx* ctx);
 /* Sessions of every replica of the search this context is a shard of (0 =
  * the staged replicas are the whole search). Used only by ARGMAX bounds. */
 int pdsim_gpu_set_global_sessions(pdsim_gpu_ctx* ctx, int64_t total_sessions);

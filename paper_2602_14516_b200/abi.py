@@ -17,6 +17,7 @@ ROUTING_ADAPTIVE, ROUTING_ALWAYS_REMOTE, ROUTING_ALWAYS_LOCAL = 0, 1, 2
 RATIONALES = ("slack_remote", "slack_local", "argmin", "forced_remote", "forced_local")
 PAIR_OK, PAIR_INVALID, PAIR_ERROR, PAIR_PRUNED = 0, 1, 2, 3
 SEARCH_FULL, SEARCH_ARGMAX = 0, 1
+BUILD_AUTO, BUILD_LATENCY, BUILD_THROUGHPUT = 0, 1, 2  # pdsim_gpu_set_kernel_build
 
 
 class Curve(C.Structure):

@@ -34,6 +34,18 @@
 #include "replay.cuh"
 #include "pdsim_gpu.h"
 
+// Throughput build of the search kernels (replay_tp_l*.o, Makefile): the same
+// sources compiled in namespace pdg_tp with the shared hot subroutines kept
+// out of line — a smaller instruction footprint when many warps share an SM
+// (DESIGN.md §3.1). Its KernelArgs is pdg::KernelArgs (same source, same
+// layout); only the search variants (0, 3) exist there.
+namespace pdg_tp {
+struct KernelArgs;
+using ReplayKernel = void (*)(KernelArgs);
+ReplayKernel replay_kernel_for(int layout, int variant);
+cudaError_t replay_set_profile(const pdsim_profile* profile, cudaStream_t stream);
+}  // namespace pdg_tp
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -68,6 +80,8 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 struct pdsim_gpu_ctx {
   int device = 0;
   int sm_count = 0;
+  int kernel_build = PDSIM_BUILD_AUTO;
+  int last_build = 0;  // build of the last replay launch
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   std::string err;
@@ -195,6 +209,7 @@ cudaError_t ProfileLease::acquire() {
   g.cv.wait(lk, [&] { return g.active == 0 || same(); });
   if (!same()) {
     cudaError_t e = pdg::replay_set_profile(&ctx_->profile, ctx_->stream);
+    if (e == cudaSuccess) e = pdg_tp::replay_set_profile(&ctx_->profile, ctx_->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx_->stream);
     if (e != cudaSuccess) {
       g.loaded = false;
@@ -514,6 +529,13 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     // 3: attainment-only search in argmax mode (Prune, engine.cuh).
     const int variant = with_rec ? 2 : ctx->profiling ? 1 : prune ? 3 : 0;
     pdg::ReplayKernel kern = pdg::replay_kernel_for(ctx->layout, variant);
+    // Many warps per SM (more than 8 pairs per SM in this launch): the
+    // throughput build. Few pairs: the inlined build (lowest latency per event).
+    const bool search_only = variant == 0 || variant == 3;
+    const bool tp = search_only && (ctx->kernel_build == PDSIM_BUILD_THROUGHPUT ||
+                                    (ctx->kernel_build == PDSIM_BUILD_AUTO && n > 8 * static_cast<int64_t>(ctx->sm_count)));
+    if (tp) kern = reinterpret_cast<pdg::ReplayKernel>(pdg_tp::replay_kernel_for(ctx->layout, variant));
+    ctx->last_build = tp ? PDSIM_BUILD_THROUGHPUT : PDSIM_BUILD_LATENCY;
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
     kern<<<static_cast<unsigned>(slots), 32, ctx->smem_bytes, ctx->stream>>>(a);
     ++launches;
@@ -773,6 +795,17 @@ int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode) {
   ctx->search_mode = mode;
   return PDSIM_OK;
 }
+
+int pdsim_gpu_set_kernel_build(pdsim_gpu_ctx* ctx, int build) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (build != PDSIM_BUILD_AUTO && build != PDSIM_BUILD_LATENCY && build != PDSIM_BUILD_THROUGHPUT) {
+    return set_err(ctx, PDSIM_ERR_CONFIG, "unknown kernel build");
+  }
+  ctx->kernel_build = build;
+  return PDSIM_OK;
+}
+
+int pdsim_gpu_last_kernel_build(const pdsim_gpu_ctx* ctx) { return ctx ? ctx->last_build : 0; }
 
 int pdsim_gpu_set_profiling(pdsim_gpu_ctx* ctx, int enable) {
   if (int rc = check_ctx(ctx)) return rc;

@@ -80,6 +80,65 @@ inline T* GLP(T* p) {
 }
 #endif
 
+// Shared-or-inlined hot subroutines (I-cache footprint): a
+// routine inlined at several call sites occupies instruction-cache lines once
+// per copy; a PDG_SHARE_<NAME> build keeps one out-of-line copy instead.
+#if defined(PDG_SHARE_SEG_APPEND) || defined(PDG_SHARE_ALL)
+#define PDG_A_SEG_APPEND PDG_COLD
+#else
+#define PDG_A_SEG_APPEND PDG_HD
+#endif
+#if defined(PDG_SHARE_CATCH_UP_WORKER) || defined(PDG_SHARE_ALL)
+#define PDG_A_CATCH_UP_WORKER PDG_COLD
+#else
+#define PDG_A_CATCH_UP_WORKER PDG_HD
+#endif
+#if defined(PDG_SHARE_TRY_STAGE) || defined(PDG_SHARE_ALL)
+#define PDG_A_TRY_STAGE PDG_COLD
+#else
+#define PDG_A_TRY_STAGE PDG_HD
+#endif
+#if defined(PDG_SHARE_COMPLETE_TASK) || defined(PDG_SHARE_ALL)
+#define PDG_A_COMPLETE_TASK PDG_COLD
+#else
+#define PDG_A_COMPLETE_TASK PDG_HD
+#endif
+#if defined(PDG_SHARE_HEAP_PUSH) || defined(PDG_SHARE_ALL)
+#define PDG_A_HEAP_PUSH PDG_COLD
+#else
+#define PDG_A_HEAP_PUSH PDG_HD
+#endif
+#if defined(PDG_SHARE_SELECT_NEXT) || defined(PDG_SHARE_ALL)
+#define PDG_A_SELECT_NEXT PDG_COLD
+#else
+#define PDG_A_SELECT_NEXT PDG_HD
+#endif
+#if defined(PDG_SHARE_FH_PUSH) || defined(PDG_SHARE_ALL)
+#define PDG_A_FH_PUSH PDG_COLD
+#else
+#define PDG_A_FH_PUSH PDG_HD
+#endif
+#if defined(PDG_SHARE_FH_POP) || defined(PDG_SHARE_ALL)
+#define PDG_A_FH_POP PDG_COLD
+#else
+#define PDG_A_FH_POP PDG_HD
+#endif
+#if defined(PDG_SHARE_ADVANCE_DECODE) || defined(PDG_SHARE_ALL)
+#define PDG_A_ADVANCE_DECODE PDG_COLD
+#else
+#define PDG_A_ADVANCE_DECODE PDG_HD
+#endif
+#if defined(PDG_SHARE_START_ROUND) || defined(PDG_SHARE_ALL)
+#define PDG_A_START_ROUND PDG_COLD
+#else
+#define PDG_A_START_ROUND PDG_HD
+#endif
+#if defined(PDG_SHARE_TTFT_HAS_SLACK) || defined(PDG_SHARE_ALL)
+#define PDG_A_TTFT_HAS_SLACK PDG_COLD
+#else
+#define PDG_A_TTFT_HAS_SLACK PDG_HD
+#endif
+
 constexpr int kMaxSlots = 64;
 constexpr int32_t kSmallHeap = 64;
 constexpr int32_t kShortBulk = 16;  // silent stretches up to this long are stepped with plain fp64 adds  // session events kept unordered (lanes scan them) up to this count
@@ -1401,7 +1460,7 @@ class EngineT {
     }
   }
 
-  PDG_HD void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
+  PDG_A_HEAP_PUSH void heap_push(double t, uint32_t kind, uint32_t a, uint32_t b) {
     const int64_t t0 = pb();
     heap_push_(t, kind, a, b);
     pe(kProfHeap, t0);
@@ -1662,7 +1721,7 @@ class EngineT {
   }
 
   // ---- task creation and routing (sim_engine.cpp:271-333) ----
-  PDG_HD void start_round(int32_t i, int round, int bound, int32_t ctx, int32_t incr) {
+  PDG_A_START_ROUND void start_round(int32_t i, int round, int bound, int32_t ctx, int32_t incr) {
     SessRt& s = GLP(s_->G.sess)[i];
     {  // warp-uniform stores (every lane writes the same values)
       s.t_enq = s_->now_;
@@ -1983,7 +2042,7 @@ class EngineT {
   }
 
   // query(now) <= thr with the sequential windowed mean's semantics.
-    PDG_HD bool ttft_has_slack(int p, double thr) {
+    PDG_A_TTFT_HAS_SLACK bool ttft_has_slack(int p, double thr) {
     const int64_t t0_ = pb();
     const bool r_ = ttft_has_slack_(p, thr);
     pe(20, t0_);
@@ -2025,7 +2084,7 @@ class EngineT {
 
   // Appends n consecutive steps (first index `first`, first end time t0,
   // each with ITL gap `gap` and `cnt` ITL samples) to worker d's log.
-    PDG_HD void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
+    PDG_A_SEG_APPEND void seg_append(int d, int32_t first, int32_t n, double t0, double gap, uint32_t cnt) {
     const int64_t t0_ = pb();
     seg_append_(d, first, n, t0, gap, cnt);
     pe(16, t0_);
@@ -2291,7 +2350,7 @@ class EngineT {
   }
 
   // Dequeues the next task (after reordering the head window).
-  PDG_HD int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
+  PDG_A_SELECT_NEXT int32_t select_next(TaskQueue& q, int32_t* qs, double* qc, double* cost) {
     const int64_t t0 = pb();
     const int32_t i = select_next_(q, qs, qc, cost);
     pe(kProfDequeue, t0);
@@ -2487,7 +2546,7 @@ class EngineT {
     try_start_compute(p);
   }
 
-    PDG_HD void try_stage(int p) {
+    PDG_A_TRY_STAGE void try_stage(int p) {
     const int64_t t0_ = pb();
     try_stage_(p);
     pe(23, t0_);
@@ -2552,7 +2611,7 @@ class EngineT {
   }
 
   // complete_task (sim_engine.cpp:458-484).
-  PDG_HD void complete_task(int32_t i, bool local, int p, int d) {
+  PDG_A_COMPLETE_TASK void complete_task(int32_t i, bool local, int p, int d) {
     const int64_t t0 = pb();
     complete_task_(i, local, p, d);
     pe(kProfComplete, t0);
@@ -2631,7 +2690,7 @@ class EngineT {
     advance_decode(d);
   }
 
-  PDG_HD void advance_decode(int d) {
+  PDG_A_ADVANCE_DECODE void advance_decode(int d) {
     const int64_t t0 = pb();
     advance_decode_(d);
     pe(kProfAdvance, t0);
@@ -2721,7 +2780,7 @@ class EngineT {
     }
   }
 
-  PDG_HD void catch_up_worker(int d, double t, uint32_t kind) {
+  PDG_A_CATCH_UP_WORKER void catch_up_worker(int d, double t, uint32_t kind) {
     const int64_t t0 = pb();
     catch_up_worker_(d, t, kind);
     pe(kProfCatchUp, t0);
@@ -2974,7 +3033,7 @@ class EngineT {
   }
 
   // ---- finisher heap (global): u64 keys (end_step << 32 | id rank) ----
-    PDG_HD void fh_push(int d, uint64_t key) {
+    PDG_A_FH_PUSH void fh_push(int d, uint64_t key) {
     const int64_t t0_ = pb();
     fh_push_(d, key);
     pe(17, t0_);
@@ -3003,7 +3062,7 @@ class EngineT {
     }
   }
 
-    PDG_HD void fh_pop(int d) {
+    PDG_A_FH_POP void fh_pop(int d) {
     const int64_t t0_ = pb();
     fh_pop_(d);
     pe(17, t0_);

@@ -65,8 +65,13 @@ __device__ __forceinline__ void write_empty_report(pdsim_report* rep, int64_t se
 // One warp per block; the warp replays pairs pulled from an atomic queue.
 // kD/kP: DecodeW/PrefillW entries reserved in shared memory; the engine
 // addresses slot state at compile-time offsets (engine.cuh smem_off).
+// PDG_MIN_BLOCKS: resident-warp target handed to ptxas (register budget per
+// lane = 64K / (32 * PDG_MIN_BLOCKS)); 1 = unconstrained.
+#ifndef PDG_MIN_BLOCKS
+#define PDG_MIN_BLOCKS 1
+#endif
 template <bool kProf, int kD, int kP, bool kRec, bool kPrune = false>
-__global__ void __launch_bounds__(32) replay_kernel(KernelArgs a) {
+__global__ void __launch_bounds__(32, PDG_MIN_BLOCKS) replay_kernel(KernelArgs a) {
   const int slot_id = blockIdx.x;
   GlobalSlot gslot;
   global_slot_bytes(a.caps, &gslot, a.ws + static_cast<size_t>(slot_id) * a.slot_bytes);

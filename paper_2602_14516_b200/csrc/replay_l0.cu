@@ -5,6 +5,11 @@
 namespace pdg {
 
 ReplayKernel replay_kernels_l0(int variant) {
+#if defined(PDG_SHARE_ALL)
+  // throughput build (namespace pdg_tp): attainment-only search kernels only
+  return variant == 3 ? replay_kernel<false, 8, 8, false, true> : variant == 0 ? replay_kernel<false, 8, 8, false>
+                                                               : nullptr;
+#else
   switch (variant) {
     case 1:
       return replay_kernel<true, 8, 8, false>;
@@ -15,6 +20,7 @@ ReplayKernel replay_kernels_l0(int variant) {
     default:
       return replay_kernel<false, 8, 8, false>;
   }
+#endif
 }
 
 cudaError_t replay_set_profile_l0(const pdsim_profile* profile, cudaStream_t stream) {

@@ -5,6 +5,11 @@
 namespace pdg {
 
 ReplayKernel replay_kernels_l1(int variant) {
+#if defined(PDG_SHARE_ALL)
+  // throughput build (namespace pdg_tp): attainment-only search kernels only
+  return variant == 3 ? replay_kernel<false, 16, 16, false, true> : variant == 0 ? replay_kernel<false, 16, 16, false>
+                                                               : nullptr;
+#else
   switch (variant) {
     case 2:
       return replay_kernel<false, 16, 16, true>;
@@ -13,6 +18,7 @@ ReplayKernel replay_kernels_l1(int variant) {
     default:  // diagnostics are built for the <8,8> layout only
       return replay_kernel<false, 16, 16, false>;
   }
+#endif
 }
 
 cudaError_t replay_set_profile_l1(const pdsim_profile* profile, cudaStream_t stream) {

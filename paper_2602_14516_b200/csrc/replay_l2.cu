@@ -5,6 +5,11 @@
 namespace pdg {
 
 ReplayKernel replay_kernels_l2(int variant) {
+#if defined(PDG_SHARE_ALL)
+  // throughput build (namespace pdg_tp): attainment-only search kernels only
+  return variant == 3 ? replay_kernel<false, 64, 32, false, true> : variant == 0 ? replay_kernel<false, 64, 32, false>
+                                                               : nullptr;
+#else
   switch (variant) {
     case 2:
       return replay_kernel<false, 64, 32, true>;
@@ -13,6 +18,7 @@ ReplayKernel replay_kernels_l2(int variant) {
     default:  // diagnostics are built for the <8,8> layout only
       return replay_kernel<false, 64, 32, false>;
   }
+#endif
 }
 
 cudaError_t replay_set_profile_l2(const pdsim_profile* profile, cudaStream_t stream) {

@@ -65,6 +65,8 @@ def lib():
         L.pdsim_format_double.restype = C.c_int32
         L.pdsim_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         L.pdsim_gpu_set_search_mode.argtypes = [C.c_void_p, C.c_int]
+        L.pdsim_gpu_set_kernel_build.argtypes = [C.c_void_p, C.c_int]
+        L.pdsim_gpu_last_kernel_build.argtypes = [C.c_void_p]
         L.pdsim_gpu_profile_counters.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         L.pdsim_gpu_search_staged.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, P(abi.SearchOutput)]
         L.pdsim_synth_spec_default.argtypes = [P(abi.SynthSpec)]
@@ -395,6 +397,13 @@ class Context:
         """abi.SEARCH_FULL (default) or abi.SEARCH_ARGMAX (exact pruning:
         same best_candidate / best_slo_ok, pruned candidates report -2)."""
         self._check(lib().pdsim_gpu_set_search_mode(self._h, int(mode)))
+
+    def set_kernel_build(self, build):
+        """abi.BUILD_AUTO / BUILD_LATENCY / BUILD_THROUGHPUT (pdsim_gpu_set_kernel_build)."""
+        self._check(lib().pdsim_gpu_set_kernel_build(self._h, int(build)))
+
+    def last_kernel_build(self):
+        return lib().pdsim_gpu_last_kernel_build(self._h)
 
     def set_profiling(self, enable):
         self._check(lib().pdsim_gpu_set_profiling(self._h, 1 if enable else 0))

@@ -12,8 +12,11 @@ from tests import parity
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("build", [abi.BUILD_AUTO, abi.BUILD_THROUGHPUT])
 @pytest.mark.parametrize("seed", range(24))
-def test_random_search_matches_reference(ctx, seed):
+def test_random_search_matches_reference(ctx, seed, build):
+    """Both kernel builds (the same engine source; THROUGHPUT keeps shared hot
+    subroutines out of line) against the reference."""
     from oracle import refbind
     if not refbind.available():
         pytest.skip("reference library not built")
@@ -30,16 +33,43 @@ def test_random_search_matches_reference(ctx, seed):
                              window=rng.randint(1, 8), stat_window=rng.choice([0.5, 3.0, 10.0]),
                              alpha=rng.choice([0.5, 0.9, 1.0]), beta=rng.choice([0.3, 0.85, 1.0]))
     es = rng.randrange(1 << 62)
-    res = ctx.plan_search(views, plans, prof, prm, es)
+    ctx.set_kernel_build(build)
+    try:
+        res = ctx.plan_search(views, plans, prof, prm, es)
+        assert ctx.last_kernel_build() == (abi.BUILD_THROUGHPUT if build == abi.BUILD_THROUGHPUT else abi.BUILD_LATENCY)
+        ctx.set_search_mode(abi.SEARCH_ARGMAX)
+        pr = ctx.plan_search(views, plans, prof, prm, es)
+    finally:
+        ctx.set_search_mode(abi.SEARCH_FULL)
+        ctx.set_kernel_build(abi.BUILD_AUTO)
     att, st_ref, _ = refbind.plan_search(views, plans, prof, prm, es)
     for p in range(res.n_pairs):
         assert res.pair_status[p] == st_ref[p], p
         if st_ref[p] == 0:
             for f in parity.ATT_FIELDS:
                 assert getattr(res.pair_attainment[p], f) == getattr(att[p], f), (p, f)
-    ctx.set_search_mode(abi.SEARCH_ARGMAX)
-    try:
-        pr = ctx.plan_search(views, plans, prof, prm, es)
-    finally:
-        ctx.set_search_mode(abi.SEARCH_FULL)
     assert (pr.best_candidate, pr.best_slo_ok) == (res.best_candidate, res.best_slo_ok)
+
+
+def test_auto_build_switches_to_throughput_for_many_pairs(ctx):
+    """AUTO launches the throughput build once a search replays more than 8
+    pairs per SM; both builds return identical per-pair results there."""
+    prof = native.synth_profile(native.default_synth_spec(), 3)
+    trs = [native.gen_trace(native.preset_stats("toolbench"), 8.0, 40, 50 + k) for k in range(8)]
+    views = [t.view for t in trs]
+    plans = native.enumerate_plans([1, 2, 4, 8], 8)  # 169 x 8 = 1352 pairs > 8 x 148
+    prm = abi.default_params()
+    auto = ctx.plan_search(views, plans, prof, prm, 9)
+    assert ctx.last_kernel_build() == abi.BUILD_THROUGHPUT
+    ctx.set_kernel_build(abi.BUILD_LATENCY)
+    try:
+        lat = ctx.plan_search(views, plans, prof, prm, 9)
+        assert ctx.last_kernel_build() == abi.BUILD_LATENCY
+    finally:
+        ctx.set_kernel_build(abi.BUILD_AUTO)
+    assert auto.n_pairs == lat.n_pairs == 1352
+    for p in range(auto.n_pairs):
+        assert auto.pair_status[p] == lat.pair_status[p], p
+        for f in parity.ATT_FIELDS:
+            assert getattr(auto.pair_attainment[p], f) == getattr(lat.pair_attainment[p], f), (p, f)
+    assert (auto.best_candidate, auto.best_slo_ok) == (lat.best_candidate, lat.best_slo_ok)
