@@ -37,7 +37,7 @@ $(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 # when many warps share an SM), in their own namespace pdg_tp.
 $(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 	@mkdir -p $(BUILD)
-	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=20 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
+	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=20 -DPDG_ROUTE_SCAN=1 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
 
 $(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(BUILD)

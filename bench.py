@@ -19,7 +19,8 @@ C-ABI call (H2D + kernels + D2H every step). `cpu_baseline` is the unmodified
 reference (oracle/_ref) on all host threads over a fixed-seed stratified
 random sample of the pairs (one random replica per candidate), extrapolated
 to the whole search; the same sampled pairs are the line's parity check.
-`secondary.C2` repeats the measurement on C2 (configs[1]).
+`secondary` repeats the measurement on C2 (configs[1]) and on a C5 slice
+(configs[4]: llama3-8b, 169 plans x 128 toolbench traces = 21 632 pairs).
 """
 import argparse
 import json
@@ -47,7 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--secondary", default="C2", help="second config measured in the same line ('none' to skip)")
+    ap.add_argument("--secondary", default="C2,C5",
+                    help="comma-separated configs measured in the same line ('none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-argmax-mode", action="store_true")
     return ap.parse_args()
@@ -193,6 +195,18 @@ def cpu_baseline(wl, gpu_pairs=None):
             key = [(-1 if bad[c] else sums[c], -c) for c in range(len(wl.plans))]
             parity["reference_best_candidate"] = max(range(len(wl.plans)), key=lambda c: key[c])
     return base, parity
+
+
+def attainment_spread(res, wl):
+    """How the candidates split between the regimes (SLO-attaining sessions over
+    all sessions of the candidate's replicas): the search is informative only
+    when both appear."""
+    total = sum(int(t.n_sessions) for t in wl.traces)
+    fr = sorted(res.candidate_slo_ok[c] / total for c in range(len(wl.plans)) if res.candidate_slo_ok[c] >= 0)
+    if not fr:
+        return None
+    return {"best": fr[-1], "median": fr[len(fr) // 2], "worst": fr[0], "candidates_ge_90pct": sum(f >= 0.9 for f in fr),
+            "candidates_lt_10pct": sum(f < 0.1 for f in fr), "valid_candidates": len(fr)}
 
 
 # ---- reference arm ------------------------------------------------------------
@@ -404,8 +418,10 @@ def run_ours(args, rank, world, local):
             parity["argmax_identical"] = parity["reference_best_candidate"] == best
 
     secondary = {}
-    if world == 1 and args.secondary and args.secondary.lower() != "none" and args.secondary != args.config:
-        s_spec = specs.SPECS[args.secondary]()
+    sec_names = [] if not args.secondary or args.secondary.lower() == "none" else \
+        [x for x in args.secondary.split(",") if x and x != args.config]
+    for sec in (sec_names if world == 1 else []):
+        s_spec = specs.SPECS[sec]()
         swl = workloads.build(s_spec)
         ctx.stage(swl.traces, swl.plans, swl.profile, swl.params)
         spairs = native.shard_pairs(swl.traces, swl.plans, 1, 0)
@@ -422,7 +438,8 @@ def run_ours(args, rank, world, local):
                  "unit": UNIT, "ms_per_step": statistics.mean(s_times), "kernel_ms": statistics.mean(s_kms),
                  "e2e": {"value": s_rounds / (statistics.median(se) / 1e3), "unit": UNIT,
                          "h2d_bytes_per_step": r_se.h2d_bytes, "d2h_bytes_per_step": r_se.d2h_bytes},
-                 "best_candidate": s_res.best_candidate, "best_slo_ok": s_res.best_slo_ok, "steps": len(s_times)}
+                 "best_candidate": s_res.best_candidate, "best_slo_ok": s_res.best_slo_ok, "steps": len(s_times),
+                 "candidate_attainment": attainment_spread(s_res, swl)}
         if not args.no_cpu_baseline:
             spos = {p: k for k, p in enumerate(spairs)}
             scpu, spar = cpu_baseline(swl, lambda p: (s_res.pair_status[spos[p]], s_res.pair_attainment[spos[p]]))
@@ -432,8 +449,9 @@ def run_ours(args, rank, world, local):
                 if "reference_best_candidate" in spar:
                     spar["argmax_identical"] = spar["reference_best_candidate"] == s_res.best_candidate
                 entry["parity"] = spar
-        secondary[args.secondary] = entry
-        launches_secondary = s_launches  # noqa: F841  (not part of the headline's timed region)
+        entry["kernel_build"] = {abi.BUILD_LATENCY: "latency", abi.BUILD_THROUGHPUT: "throughput"}.get(
+            ctx.last_kernel_build())
+        secondary[sec] = entry
 
     if rank == 0:
         line = {
@@ -449,6 +467,7 @@ def run_ours(args, rank, world, local):
             "planner_wall_ms": total_ms / args.steps,
             "kernel_ms": avg_k,
             "best_candidate": best, "best_slo_ok": best_cnt,
+            "candidate_attainment": attainment_spread(res, wl),
             "best_plan": abi.format_plan(wl.plans[best]) if best >= 0 else None,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

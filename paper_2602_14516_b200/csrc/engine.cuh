@@ -139,6 +139,20 @@ inline T* GLP(T* p) {
 #define PDG_A_TTFT_HAS_SLACK PDG_HD
 #endif
 
+// Route slack scan on the device: 0 sequential (worker by worker, warp-
+// collective trims; the latency build), 1 all workers in parallel (lane per
+// worker; the throughput build, Makefile), 2 the first worker alone, then
+// the rest in parallel. Same decisions in every mode (tests/test_gpu_random.py
+// runs both builds); A/B on one B200 (profiles/round2/ab_route_fh_v14.log):
+// mode 1 -2 % on C3s/C5, +2 % on C2.
+#ifndef PDG_ROUTE_SCAN
+#define PDG_ROUTE_SCAN 0
+#endif
+// Finisher heap arity (2 or 32; 32 measured neutral, the binary heap kept).
+#ifndef PDG_FH_ARITY
+#define PDG_FH_ARITY 2
+#endif
+
 constexpr int kMaxSlots = 64;
 constexpr int32_t kSmallHeap = 64;
 constexpr int32_t kShortBulk = 16;  // silent stretches up to this long are stepped with plain fp64 adds  // session events kept unordered (lanes scan them) up to this count
@@ -1828,6 +1842,22 @@ class EngineT {
         }
       }
       const double thr = dmul(s_->PR.alpha, s_->T.ttft_thres);
+#if defined(__CUDA_ARCH__) && PDG_ROUTE_SCAN > 0
+#if PDG_ROUTE_SCAN == 2
+      // The first worker of the scan alone (warp-collective trim); the rest,
+      // when it has no slack, in parallel.
+      const int p0 = packed ? static_cast<int>(perm & 15u) : order[0];
+      const int p = ttft_has_slack(p0, thr) ? p0 : n > 1 ? slack_scan(thr, perm, packed, n, p0) : -1;
+#else
+      const int p = slack_scan(thr, perm, packed, n, -1);
+#endif
+      if (p >= 0) {
+        r.local = 0;
+        r.p = p;
+        r.rationale = PDSIM_RATIONALE_SLACK_REMOTE;
+        return r;
+      }
+#else
       for (int k = 0; k < n; ++k) {
         const int p = packed ? static_cast<int>((perm >> (4 * k)) & 15u) : order[k];
         if (ttft_has_slack(p, thr)) {
@@ -1837,6 +1867,7 @@ class EngineT {
           return r;
         }
       }
+#endif
     }
     if (itl_has_slack(bound, dmul(s_->PR.beta, s_->T.itl_thres))) {
       r.local = 1;
@@ -1848,6 +1879,60 @@ class EngineT {
     r.rationale = PDSIM_RATIONALE_ARGMIN;
     return r;
   }
+
+#if defined(__CUDA_ARCH__)
+  // The slack scan of Coordinator::route (coordinator.cpp:139-150): the first
+  // prefill worker in the shuffled scan order whose windowed TTFT mean is
+  // <= thr (worker `skip`, already found without slack, excluded). Lane p
+  // tests worker p (its own window, trimmed by that lane), all at once; the
+  // winner is the lowest scan position with slack. Trimming a
+  // window the sequential scan would not have reached changes nothing: its
+  // expired samples are expired at every later query too (queries only move
+  // forward in time), and the ring only gains room.
+  PDG_HD int slack_scan(double thr, uint64_t perm, bool packed, int n, int skip) {
+    warp_sync();  // the scan order (ORD) was written by the whole warp
+    const int lane = lane_id();
+    bool slack = false, folded = false;
+    if (lane < n && lane != skip) {
+      PrefillW& w = PW(lane);
+      const size_t base = static_cast<size_t>(lane) * s_->C.twcap;
+      const uint32_t mask = static_cast<uint32_t>(s_->C.twcap - 1);
+      const double* times = GLP(s_->G.tw_t) + base;
+      const double cutoff = dsub(s_->now_, s_->PR.stat_window);
+      uint32_t head = w.tw.head;
+      const uint32_t end = w.tw.end;
+      while (head != end && times[head & mask] <= cutoff) ++head;
+      const Brk tail = w.tw.tail;
+      w.tw.head = head;  // this lane's own worker
+      if (head == end) {
+        slack = 0.0 <= thr;  // an empty window reads 0
+      } else {
+        const Brk hp = GLP(s_->G.tw_p)[base + (head & mask)];
+        double lo = sub_rd(tail.lo, hp.hi);
+        const double hi = sub_ru(tail.hi, hp.lo);
+        if (lo < 0.0) lo = 0.0;
+        const int dec = mean_le_bracket(lo, hi, static_cast<int64_t>(end - head), thr);
+        if (dec >= 0) {
+          slack = dec == 1;
+        } else {  // inside the error band: the reference's sequential fold
+          folded = true;
+          const double* v = GLP(s_->G.tw_v) + base;
+          double sum = 0.0;
+          for (uint32_t k = head; k != end; ++k) sum = dadd(sum, v[k & mask]);
+          slack = ddiv(sum, static_cast<double>(end - head)) <= thr;
+        }
+      }
+    }
+    const uint32_t nf = ballot(folded);
+    const int pk = lane < n ? (packed ? static_cast<int>((perm >> (4 * lane)) & 15u) : ORD()[lane]) : 0;
+    const bool sk = shfl_i(slack ? 1 : 0, pk) != 0;
+    const uint32_t b = ballot(lane < n && sk);
+    warp_sync();
+    if (nf) s_->folds_ += popc(nf);  // warp-uniform store
+    if (!b) return -1;
+    return shfl_i(pk, __ffs(b) - 1);
+  }
+#endif
 
   // ---- routing estimates (coordinator.cpp:74-100) ----
   PDG_HD double fold_queue(const TaskQueue& q, const double* qc, double init) const {
@@ -3038,6 +3123,38 @@ class EngineT {
     fh_push_(d, key);
     pe(17, t0_);
   }
+#if PDG_FH_ARITY == 32
+  // A 32-ary min-heap: the children of entry i are 32i+1 .. 32i+32, so a pop
+  // reads one level's children with one coalesced warp load and picks the
+  // smallest with two REDUX.MIN — depth log32(n) instead of log2(n)
+  // dependent loads. Keys are unique (one entry per session).
+  PDG_HD void fh_push_(int d, uint64_t key) {
+    DecodeW& w = DW(d);
+    const int32_t n = w.fh_n;
+    if (n >= s_->C.fcap) {
+      fail();
+      return;
+    }
+    uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
+    const uint64_t top = w.fh_top;
+    int32_t i = n;
+    while (i > 0) {
+      const int32_t par = (i - 1) >> 5;
+      const uint64_t pv = h[par];
+      if (pv <= key) break;
+      warp_sync();
+      if (lane_id() == 0) h[i] = pv;
+      i = par;
+    }
+    warp_sync();
+    if (lane_id() == 0) h[i] = key;
+    // warp-uniform stores
+    w.fh_n = n + 1;
+    if (n == 0 || key < top) w.fh_top = key;
+    warp_sync();
+  }
+
+#else
   PDG_HD void fh_push_(int d, uint64_t key) {
     DecodeW& w = DW(d);
     const int32_t n = w.fh_n;
@@ -3062,11 +3179,54 @@ class EngineT {
     }
   }
 
+#endif
     PDG_A_FH_POP void fh_pop(int d) {
     const int64_t t0_ = pb();
     fh_pop_(d);
     pe(17, t0_);
   }
+#if PDG_FH_ARITY == 32
+  PDG_HD void fh_pop_(int d) {
+    DecodeW& w = DW(d);
+    uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
+    const int32_t n = w.fh_n - 1;
+    const uint64_t last = h[n];
+    int32_t i = 0;
+    for (;;) {
+      const int32_t c0 = 32 * i + 1;
+      if (c0 >= n) break;
+#if defined(__CUDA_ARCH__)
+      const int32_t c = c0 + lane_id();
+      const uint64_t v = c < n ? h[c] : ~0ull;
+      const uint32_t hi = static_cast<uint32_t>(v >> 32);
+      const uint32_t mhi = __reduce_min_sync(0xffffffffu, hi);
+      const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? static_cast<uint32_t>(v) : 0xffffffffu);
+      const uint64_t m = (static_cast<uint64_t>(mhi) << 32) | mlo;
+      if (m >= last) break;
+      const int am = __ffs(__ballot_sync(0xffffffffu, v == m)) - 1;
+#else
+      uint64_t m = ~0ull;
+      int am = 0;
+      for (int k = 0; k < 32 && c0 + k < n; ++k) {
+        if (h[c0 + k] < m) {
+          m = h[c0 + k];
+          am = k;
+        }
+      }
+      if (m >= last) break;
+#endif
+      if (lane_id() == 0) h[i] = m;
+      i = c0 + am;
+    }
+    warp_sync();
+    if (n > 0 && lane_id() == 0) h[i] = last;
+    warp_sync();
+    // warp-uniform stores
+    w.fh_n = n;
+    w.fh_top = n > 0 ? h[0] : 0;
+    warp_sync();
+  }
+#else
   PDG_HD void fh_pop_(int d) {
     DecodeW& w = DW(d);
     uint64_t* h = GLP(s_->G.fh) + static_cast<size_t>(d) * s_->C.fcap;
@@ -3094,6 +3254,9 @@ class EngineT {
       w.fh_top = n > 0 ? h[0] : 0;
     }
   }
+#endif
+
+
 };
 
 using Engine = EngineT<false>;  // host (test) build: pointer-based slot layout
