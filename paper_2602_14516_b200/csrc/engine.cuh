@@ -309,28 +309,38 @@ struct DevParams {
   double stat_window;
 };
 
-// Per-session runtime state (SessionRt + the one PrefillTask in flight).
-struct SessRt {
+// Per-session runtime state (SessionRt + the one PrefillTask in flight),
+// split by access frequency. SessRt is what every mode touches on every
+// event of the session: 64 B, so one record is half a 128-byte line and two
+// 32-byte sectors (the throughput configs keep millions of these in DRAM,
+// profiles/traffic_C3.json). SessCold holds what only the exact engine and
+// the record outputs read.
+struct alignas(64) SessRt {
   double itl_lo;     // search mode: bracket [itl_lo, itl_hi] of the exact sum of this
   double itl_hi;     //   session's ITL samples (directed rounding)
   double t_enq;      // enqueue time of the current task (== created for r >= 2)
-  double itl_sum;    // exact mode: sequential fold of this session's ITL samples
-  double bind_time;  // admission time
   double e_join;     // lazy search mode: end time of step `join` (stamped when it starts)
   int32_t itl_cnt;
   int32_t next_pend; // lazy search mode: next session waiting for its round's first step
   int32_t join;      // step index at which the current round joined the batch
   int32_t ctx;       // context_len
-  int32_t seg_hint;  // bound worker's open-segment index when the round joined
+  int32_t roff;      // index of its first round in the round table (cached at admission)
   int16_t round;     // 1-based current round
+  int16_t nround;    // the session's round count (cached at admission)
   int8_t bound;      // decode worker index
   int8_t postpone;   // PrefillTask::postpone_count
   int8_t ttft_bad;   // some TTFT > threshold
   int8_t reserved;
-  int16_t nround;    // the session's round count (cached at admission)
-  int32_t roff;      // index of its first round in the round table (cached at admission)
+  int32_t reserved2;
 };
-static_assert(sizeof(SessRt) == 80, "SessRt layout");
+static_assert(sizeof(SessRt) == 64, "SessRt layout");
+struct SessCold {
+  double itl_sum;    // exact mode: sequential fold of this session's ITL samples
+  double bind_time;  // admission time (records)
+  int32_t seg_hint;  // exact mode: bound worker's open-segment index when the round joined
+  int32_t reserved;
+};
+static_assert(sizeof(SessCold) == 24, "SessCold layout");
 
 // A worker's task queue (global ring) + exact sum of the queued costs.
 struct TaskQueue {
@@ -441,6 +451,7 @@ struct SmemSlot {
 // Global-memory part of a workspace slot.
 struct GlobalSlot {
   SessRt* sess;
+  SessCold* sess_cold;
   HEv* heap;  // spill area [hcap]
   int32_t* pq_s;
   double* pq_c;
@@ -509,6 +520,7 @@ PDG_HD size_t global_slot_bytes(const Caps& c, GlobalSlot* s, char* base) {
   const size_t P = static_cast<size_t>(c.pmax > 0 ? c.pmax : 1), D = static_cast<size_t>(c.dmax);
   GlobalSlot t;
   t.sess = reinterpret_cast<SessRt*>(take(sizeof(SessRt) * static_cast<size_t>(c.S)));
+  t.sess_cold = reinterpret_cast<SessCold*>(take(sizeof(SessCold) * static_cast<size_t>(c.S)));
   t.heap = reinterpret_cast<HEv*>(take(sizeof(HEv) * static_cast<size_t>(c.hcap)));
   t.pq_s = reinterpret_cast<int32_t*>(take(4 * P * static_cast<size_t>(c.qcap)));
   t.pq_c = reinterpret_cast<double*>(take(8 * P * static_cast<size_t>(c.qcap)));
@@ -1710,16 +1722,19 @@ class EngineT {
       s.roff = roff;
       s.nround = static_cast<int16_t>(nround);
       s.bound = static_cast<int8_t>(best);
-      s.bind_time = s_->now_;
       s.round = 1;
       s.ctx = 0;
-      s.itl_sum = 0.0;
       s.itl_lo = 0.0;
       s.itl_hi = 0.0;
       s.itl_cnt = 0;
       s.join = 0;
       s.postpone = 0;
       s.ttft_bad = 0;
+    }
+    if (!kLazy || kRec) {  // the exact engine and the records only
+      SessCold& c = GLP(s_->G.sess_cold)[i];
+      c.bind_time = s_->now_;  // warp-uniform stores
+      c.itl_sum = 0.0;
     }
     start_round(i, 1, best, 0, r1.incr);
     return true;
@@ -2747,11 +2762,11 @@ class EngineT {
       warp_sync();
       if (newly_bad) s_->fails_ += 1;  // warp-uniform store
     }
+    if ((!kLazy || kRec) && lane_id() == 0) GLP(s_->G.sess_cold)[i].seg_hint = hint;
     if (lane_id() == 0) {
       if (value > s_->T.ttft_thres) s.ttft_bad = 1;
       s.ctx += incr;
       s.join = join;
-      s.seg_hint = hint;
       if (kLazy) {
         s.next_pend = w.pend_head;
         w.pend_head = i;
@@ -3011,10 +3026,12 @@ class EngineT {
       const RoundTr rt = round_tr(s.roff + s.round - 1);
       const int32_t dec = rt.dec;
       // This round's ITL samples, in token order (sim_engine.cpp:544-555).
-      double sum = s.itl_sum;
       double ilo = s.itl_lo, ihi = s.itl_hi;
       if (!kLazy || (kRec && s_->exact_itl_)) {
-        sum = seg_fold(d, s.join + 1, k, sum, s.seg_hint);
+        SessCold& c = GLP(s_->G.sess_cold)[i];
+        const double sum = seg_fold(d, s.join + 1, k, c.itl_sum, c.seg_hint);
+        warp_sync();
+        c.itl_sum = sum;  // warp-uniform store
       } else if (dec > 1) {
         // ITL samples at steps join+1..k sum to within a relative u of
         // e_k - e_join (every sample is fl(e_j - e_{j-1})).
@@ -3040,7 +3057,6 @@ class EngineT {
       }
       const bool last = s.round == s.nround;
       {  // warp-uniform stores (every lane writes the same values)
-        s.itl_sum = sum;
         s.itl_lo = ilo;
         s.itl_hi = ihi;
         s.itl_cnt += dec - 1;
@@ -3074,7 +3090,10 @@ class EngineT {
     SessRt& s = GLP(s_->G.sess)[i];
     const int32_t ctx = s.ctx;
     const int32_t cnt = s.itl_cnt;
-    const double mean_itl = cnt > 0 ? ddiv(s.itl_sum, static_cast<double>(cnt)) : 0.0;
+    // the exact sequential fold exists only where the exact engine or the
+    // records ran (SessCold); search mode decides on the bracket below
+    const double mean_itl =
+        (!kLazy || kRec) && cnt > 0 ? ddiv(GLP(s_->G.sess_cold)[i].itl_sum, static_cast<double>(cnt)) : 0.0;
     const bool ttft_ok = !s.ttft_bad;
     bool itl_ok;
     if (!kLazy || (kRec && s_->exact_itl_) || cnt == 0) {
@@ -3101,7 +3120,7 @@ class EngineT {
         o.session_id = GLP(s_->T.sid)[i];
         o.arrival_time = arrival;
         o.completion_time = s_->now_;
-        o.admission_wait = dsub(s.bind_time, arrival);
+        o.admission_wait = dsub(GLP(s_->G.sess_cold)[i].bind_time, arrival);
         o.mean_itl = mean_itl;
         o.rounds = s.nround;
         o.ttft_ok = ttft_ok;
