@@ -34,6 +34,11 @@ struct SearchOptions {
   // win stop early; best_candidate / best_slo_ok are unchanged, pruned
   // candidates get candidate_slo_ok = -2 and pairs valid = false.
   bool prune = false;
+  // Several GPUs of this process (pdsim_multi_plan_search): the whole search
+  // is sharded over `devices` (cost-aware LPT split) and the per-candidate
+  // counts all-reduced over NCCL; outputs as for one device. Needs the whole
+  // pair range and no reports. Empty: one device (`device`).
+  std::vector<int> devices;
 };
 
 struct SearchResult {

@@ -952,12 +952,19 @@ SearchResult plan_search(const std::vector<Trace>& replicas, const std::vector<D
     reps.resize(static_cast<size_t>(std::max<int64_t>(n, 1)));
     out.pair_report = reps.data();
   }
-  pdsim_gpu_ctx* ctx = context(options.device >= 0 ? options.device : default_device());
-  check_ctx(pdsim_gpu_set_search_mode(ctx, options.prune && !options.report ? PDSIM_SEARCH_ARGMAX : PDSIM_SEARCH_FULL),
-            ctx);
-  const int rc = pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out);
-  pdsim_gpu_set_search_mode(ctx, PDSIM_SEARCH_FULL);
-  check_ctx(rc, ctx);
+  if (!options.devices.empty()) {
+    if (options.report) raise(PDSIM_ERR_CONFIG, "plan_search: reports are single-device");
+    check(pdsim_multi_plan_search(static_cast<int32_t>(options.devices.size()), options.devices.data(), &in, &prof,
+                                  &pparams, engine_seed, options.prune ? PDSIM_SEARCH_ARGMAX : PDSIM_SEARCH_FULL,
+                                  &out));
+  } else {
+    pdsim_gpu_ctx* ctx = context(options.device >= 0 ? options.device : default_device());
+    check_ctx(pdsim_gpu_set_search_mode(ctx, options.prune && !options.report ? PDSIM_SEARCH_ARGMAX : PDSIM_SEARCH_FULL),
+              ctx);
+    const int rc = pdsim_gpu_plan_search(ctx, &in, &prof, &pparams, engine_seed, &out);
+    pdsim_gpu_set_search_mode(ctx, PDSIM_SEARCH_FULL);
+    check_ctx(rc, ctx);
+  }
   if (options.report) {
     for (int64_t k = 0; k < n; ++k) {
       r.reports.push_back(report_from_pod(

@@ -204,6 +204,23 @@ int main() {
     }
   }
 
+  // SearchOptions::devices (pdsim_multi_plan_search: shards over the listed
+  // GPUs, NCCL all-reduce of the counts): the same search result.
+  {
+    const std::vector<DeploymentPlan> cands = enumerate_plans({1, 2, 4}, 8);
+    const Trace gen3 = gen_trace(preset_stats("hotpotqa"), 12.0, 150, 21);
+    const SearchResult one = plan_search({gen, gen3}, cands, p, SchedulerParams{}, 3);
+    SearchOptions so;
+    so.devices = {0};
+    const SearchResult md = plan_search({gen, gen3}, cands, p, SchedulerParams{}, 3, so);
+    CHECK(md.best_candidate == one.best_candidate && md.best_slo_ok == one.best_slo_ok);
+    CHECK(md.candidate_slo_ok == one.candidate_slo_ok);
+    CHECK(md.pairs.size() == one.pairs.size());
+    for (size_t k = 0; k < md.pairs.size(); ++k) {
+      CHECK(md.pairs[k].slo_ok == one.pairs[k].slo_ok && md.pairs[k].valid == one.pairs[k].valid);
+    }
+  }
+
   // sweep() (pdsim sweep, pdsim.cpp:501-590): one launch over traces x
   // settings; each report equals build_report of run() under that setting.
   {
