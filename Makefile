@@ -9,6 +9,8 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 EXTRA     ?=
 # NVEXTRA: nvcc-only flags of a variant build (e.g. -Xptxas -O2)
 NVEXTRA   ?=
+# resident warps per SM the throughput build is register-allocated for
+TP_MINB   ?= 24
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
              -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA) $(NVEXTRA)
 HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC) $(EXTRA)
@@ -35,9 +37,9 @@ $(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 # Throughput build of the search kernels: the same sources
 # with the shared hot subroutines kept out of line (smaller I-cache footprint
 # when many warps share an SM), in their own namespace pdg_tp.
-$(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
+$(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS) Makefile
 	@mkdir -p $(BUILD)
-	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=20 -DPDG_ROUTE_SCAN=1 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
+	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=$(TP_MINB) -DPDG_ROUTE_SCAN=1 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
 
 $(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(BUILD)

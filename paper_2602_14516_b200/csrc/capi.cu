@@ -328,7 +328,7 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   const int64_t pairs = static_cast<int64_t>(in->n_traces) * in->n_candidates;
   size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
                        : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
-                                                    : (size_t(10) << 10);
+                                                    : size_t(9216);  // 24 warps/SM (the throughput build's register budget)
   if (const char* v = getenv("PDSIM_SMEM_BUDGET")) smem_budget = static_cast<size_t>(atoll(v));  // tuning only
   // Compiled shared-memory layouts (replay_kernel<.., kD, kP>): N <= 8 plans
   // fit <8, 8>, N <= 16 plans <16, 16>; D + 2P <= 64 bounds the rest.

@@ -3,7 +3,8 @@ alternates runs of a staged search in fresh processes.
 
 usage: python tools/ab.py CONFIG ROUNDS LIB [LIB ...]
 LIB_x is a libpdsim_gpu.so, or a directory holding a whole package copy
-(paper_2602_14516_b200/ with its .so) when the Python bindings differ too.
+(paper_2602_14516_b200/ with its .so) when the Python bindings differ too;
+LIB@VAR=VALUE[,VAR=VALUE] runs that arm with extra environment variables.
 """
 import os
 import subprocess
@@ -24,18 +25,21 @@ print(min(ms))
 
 def main(libs, rounds=3, cfg="C2", pb="0", pe="-1"):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {lib: [] for lib in libs}
+    res = {spec: [] for spec in libs}
     for _ in range(int(rounds)):
-        for lib in libs:
+        for spec in libs:
+            lib, _, extra = spec.partition("@")
+            add = dict(kv.split("=", 1) for kv in extra.split(",") if kv)
             if os.path.isdir(lib):
                 env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
                 cwd = os.path.abspath(lib)
             else:
                 env = dict(os.environ, PDSIM_LIB=os.path.abspath(lib))
                 cwd = root
+            env.update(add)
             out = subprocess.run([sys.executable, "-c", CHILD, cfg, pb, pe], cwd=cwd, env=env, capture_output=True,
                                  text=True)
-            res[lib].append(float(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else None)
+            res[spec].append(float(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else None)
             if out.returncode != 0:
                 print(out.stderr[-2000:], file=sys.stderr)
     for lib, v in res.items():
