@@ -11,6 +11,8 @@ EXTRA     ?=
 NVEXTRA   ?=
 # resident warps per SM the throughput build is register-allocated for
 TP_MINB   ?= 24
+# extra defines of the throughput build only (A/B variants)
+TP_EXTRA  ?=
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
              -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA) $(NVEXTRA)
 HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC) $(EXTRA)
@@ -39,7 +41,7 @@ $(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 # when many warps share an SM), in their own namespace pdg_tp.
 $(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS) Makefile
 	@mkdir -p $(BUILD)
-	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=$(TP_MINB) -DPDG_ROUTE_SCAN=1 -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
+	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=$(TP_MINB) -DPDG_ROUTE_SCAN=1 $(TP_EXTRA) -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
 
 $(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(BUILD)
