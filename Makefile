@@ -13,6 +13,10 @@ NVEXTRA   ?=
 TP_MINB   ?= 24
 # extra defines of the throughput build only (A/B variants)
 TP_EXTRA  ?=
+# hot subroutines the throughput build keeps out of line (engine.cuh PDG_SHARE_*)
+TP_SHARE  ?= -DPDG_SHARE_SEG_APPEND -DPDG_SHARE_CATCH_UP_WORKER -DPDG_SHARE_TRY_STAGE -DPDG_SHARE_COMPLETE_TASK \
+             -DPDG_SHARE_HEAP_PUSH -DPDG_SHARE_ADVANCE_DECODE -DPDG_SHARE_START_ROUND -DPDG_SHARE_TTFT_HAS_SLACK \
+             -DPDG_SHARE_SELECT_NEXT
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -Xptxas -v \
              -Xcompiler -fPIC,-ffp-contract=off,-O2 -Iinclude -I$(CSRC) $(EXTRA) $(NVEXTRA)
 HOSTFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude -I$(CSRC) $(EXTRA)
@@ -41,7 +45,7 @@ $(BUILD)/replay_l%.o: $(CSRC)/replay_l%.cu $(HDRS)
 # when many warps share an SM), in their own namespace pdg_tp.
 $(BUILD)/replay_tp_l%.o: $(CSRC)/replay_l%.cu $(HDRS) Makefile
 	@mkdir -p $(BUILD)
-	$(NVCC) $(NVFLAGS) -DPDG_SHARE_ALL -DPDG_MIN_BLOCKS=$(TP_MINB) -DPDG_ROUTE_SCAN=1 $(TP_EXTRA) -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
+	$(NVCC) $(NVFLAGS) -DPDG_TP_BUILD $(TP_SHARE) -DPDG_MIN_BLOCKS=$(TP_MINB) -DPDG_ROUTE_SCAN=1 $(TP_EXTRA) -Dpdg=pdg_tp -c $< -o $@ 2> $(BUILD)/ptxas_tp_l$*.log || (cat $(BUILD)/ptxas_tp_l$*.log; false)
 
 $(BUILD)/host_gen.o: $(CSRC)/host_gen.cpp $(HDRS)
 	@mkdir -p $(BUILD)

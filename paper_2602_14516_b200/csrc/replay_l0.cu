@@ -5,7 +5,7 @@
 namespace pdg {
 
 ReplayKernel replay_kernels_l0(int variant) {
-#if defined(PDG_SHARE_ALL)
+#if defined(PDG_TP_BUILD)
   // throughput build (namespace pdg_tp): attainment-only search kernels only
   return variant == 3 ? replay_kernel<false, 8, 8, false, true> : variant == 0 ? replay_kernel<false, 8, 8, false>
                                                                : nullptr;
