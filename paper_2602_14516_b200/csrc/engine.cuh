@@ -2659,19 +2659,27 @@ class EngineT {
                                     GLP(s_->G.pq_c) + static_cast<size_t>(p) * s_->C.qcap, &cost);
     const int32_t hist = GLP(s_->G.sess)[stg].ctx;
     double ready = s_->now_;
+    bool event = false;
     if (hist > 0) {
       // Lazy history read from the bound decode worker (sim_engine.cpp:368-383).
       const int dd = DW(GLP(s_->G.sess)[stg].bound).deg;
       ready = dadd(s_->now_, t_kv(hist, dd, w.deg));
+      // The read's completion event only clears the pending flag and retries
+      // the compute start (sim_engine.cpp:438-443). While the worker computes
+      // until done >= ready, that retry is a no-op and the start happens at
+      // done (on_prefill_done), where staged_ready <= now holds: the event is
+      // not scheduled. (Sequence numbers of later events shift uniformly, so
+      // their order is unchanged.)
+      event = !(w.computing && s_->st_[slot_compute(p)] >= ready);
     }
     {  // warp-uniform stores (every lane writes the same values)
       w.stg = stg;
       w.stg_cost = cost;
       w.staged = 1;
       w.staged_ready = ready;
-      w.pending = hist > 0 ? 1 : 0;
+      w.pending = event ? 1 : 0;
     }
-    if (hist > 0) set_slot(slot_history(p), ready, kKvTransferDone);
+    if (event) set_slot(slot_history(p), ready, kKvTransferDone);
   }
 
   PDG_HD void try_start_compute(int p) {
