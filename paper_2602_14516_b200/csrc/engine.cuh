@@ -153,6 +153,12 @@ inline T* GLP(T* p) {
 #define PDG_FH_ARITY 2
 #endif
 
+// Branch hints for the rare paths (capacity failures, lazy-mode aborts,
+// exact-fold fallbacks): keeps them off the fall-through path of the hot
+// code (instruction fetch).
+#define PDG_UNLIKELY(x) __builtin_expect(!!(x), 0)
+#define PDG_LIKELY(x) __builtin_expect(!!(x), 1)
+
 constexpr int kMaxSlots = 64;
 constexpr int32_t kSmallHeap = 64;
 constexpr int32_t kShortBulk = 16;  // silent stretches up to this long are stepped with plain fp64 adds  // session events kept unordered (lanes scan them) up to this count
@@ -889,7 +895,7 @@ class EngineT {
       const uint32_t kind = static_cast<uint32_t>(bk >> 58);
       // Two decode-step events at the same time: their order is the
       // scheduling order, which lazily materialised steps do not carry.
-      if (kLazy && src == 0 && kind == kDecodeStep && slot_tie) {
+      if (PDG_UNLIKELY(kLazy && src == 0 && kind == kDecodeStep && slot_tie)) {
         s_->abort_ = 1;
         return;
       }
@@ -949,7 +955,7 @@ class EngineT {
       }
       h = (h + 1) & mask;
     }
-    if (!placed) fail();  // histogram capacity exceeded: loud failure
+    if (PDG_UNLIKELY(!placed)) fail();  // histogram capacity exceeded: loud failure
   }
 
   // k-th smallest (1-based) of the keys item(i) yields for i < n (items
@@ -1516,7 +1522,7 @@ class EngineT {
       warp_sync();
       s_->heap_spilled_ = true;
     }
-    if (s_->hn_ >= s_->C.hcap) {
+    if (PDG_UNLIKELY(s_->hn_ >= s_->C.hcap)) {
       fail();
       return;
     }
@@ -1927,7 +1933,7 @@ class EngineT {
         const double hi = sub_ru(tail.hi, hp.lo);
         if (lo < 0.0) lo = 0.0;
         const int dec = mean_le_bracket(lo, hi, static_cast<int64_t>(end - head), thr);
-        if (dec >= 0) {
+        if (PDG_LIKELY(dec >= 0)) {
           slack = dec == 1;
         } else {  // inside the error band: the reference's sequential fold
           folded = true;
@@ -2109,7 +2115,7 @@ class EngineT {
   PDG_HD bool window_room(WinState& w, const double* times, uint32_t cap, double now) {
     if (w.end - w.head >= cap - 1) {
       window_trim(w, times, cap - 1, now);
-      if (w.end - w.head >= cap - 1) {
+      if (PDG_UNLIKELY(w.end - w.head >= cap - 1)) {
         fail();
         return false;
       }
@@ -2162,7 +2168,7 @@ class EngineT {
     const double hi = sub_ru(w.tw.tail.hi, hp.lo);
     if (lo < 0.0) lo = 0.0;
     const int dec = mean_le_bracket(lo, hi, static_cast<int64_t>(end - head), thr);
-    if (dec >= 0) return dec == 1;
+    if (PDG_LIKELY(dec >= 0)) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
     for (uint32_t k = head; k != end; ++k) sum = dadd(sum, GLP(s_->G.tw_v)[base + (k & mask)]);
@@ -2209,7 +2215,7 @@ class EngineT {
       if (end - w.seg_keep >= s_->C.segcap) {
         seg_trim(d, t0);  // later queries are at >= t0
         seg_reclaim(d, first);
-        if (end - w.seg_keep >= s_->C.segcap) {
+        if (PDG_UNLIKELY(end - w.seg_keep >= s_->C.segcap)) {
           fail();
           return;
         }
@@ -2318,7 +2324,7 @@ class EngineT {
     if (lo < 0.0) lo = 0.0;
     if (terms == 0) return 0.0 <= thr;  // an empty window reads 0
     const int dec = mean_le_bracket(lo, hi, terms, thr);
-    if (dec >= 0) return dec == 1;
+    if (PDG_LIKELY(dec >= 0)) return dec == 1;
     ++s_->folds_;
     double sum = 0.0;
     for (int32_t i = w.seg_head; i <= w.seg_end; ++i) {
@@ -2344,13 +2350,13 @@ class EngineT {
   }
   PDG_HD void seg_span_(int d, int32_t j0, int32_t hint, double* lo, double* hi) {
     const DecodeW& w = DW(d);
-    if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
+    if (PDG_UNLIKELY(hint < w.seg_keep)) {  // the needed steps were reclaimed: capacity bound broken
       fail();
       *lo = *hi = 0.0;
       return;
     }
     const int32_t gi = seg_find(d, j0, hint);
-    if (gi < 0) {
+    if (PDG_UNLIKELY(gi < 0)) {
       fail();
       *lo = *hi = 0.0;
       return;
@@ -2401,7 +2407,7 @@ class EngineT {
   PDG_HD double seg_fold(int d, int32_t a, int32_t k, double s, int32_t hint) {
     const DecodeW& w = DW(d);
     if (a > k) return s;
-    if (hint < w.seg_keep) {  // the needed steps were reclaimed: capacity bound broken
+    if (PDG_UNLIKELY(hint < w.seg_keep)) {  // the needed steps were reclaimed: capacity bound broken
       fail();
       return s;
     }
@@ -2433,7 +2439,7 @@ class EngineT {
   // ---- queues + reorder (reorder.cpp:76-146; select_next sim_engine.cpp:335-350) ----
   PDG_HD bool queue_push(TaskQueue& q, int32_t* qs, double* qc, int32_t i, double cost) {
     const uint32_t qh = q.qh, qt = q.qt;
-    if (qt - qh >= static_cast<uint32_t>(s_->C.qcap)) {
+    if (PDG_UNLIKELY(qt - qh >= static_cast<uint32_t>(s_->C.qcap))) {
       fail();
       return false;
     }
@@ -2916,7 +2922,7 @@ class EngineT {
       double end = e;
       int32_t done = 1;
       double next = dadd(e, dur);
-      if (!(next > e)) {  // a zero-length step cannot be advanced lazily
+      if (PDG_UNLIKELY(!(next > e))) {  // a zero-length step cannot be advanced lazily
         s_->abort_ = 1;
         return;
       }
@@ -2950,7 +2956,7 @@ class EngineT {
           end = last_end;
           done += static_cast<int32_t>(m);
           next = nxt;
-          if (!(next > end)) {
+          if (PDG_UNLIKELY(!(next > end))) {
             s_->abort_ = 1;
             return;
           }
@@ -3022,7 +3028,7 @@ class EngineT {
 
     bool any_terminated = false;
     while (!s_->failed_ && w.fh_n > 0 && static_cast<int32_t>(w.fh_top >> 32) <= k) {
-      if (static_cast<int32_t>(w.fh_top >> 32) < k) {  // a round end was missed
+      if (PDG_UNLIKELY(static_cast<int32_t>(w.fh_top >> 32) < k)) {  // a round end was missed
         fail();
         return;
       }
@@ -3109,7 +3115,7 @@ class EngineT {
     } else {
       // search mode: certified decision of fl(fold / cnt) <= itl_thres
       const int dec = mean_le_bracket(s.itl_lo, s.itl_hi, cnt, s_->T.itl_thres);
-      if (dec < 0) {  // inside the error band: replay this pair with exact folds
+      if (PDG_UNLIKELY(dec < 0)) {  // inside the error band: replay this pair with exact folds
         s_->abort_ = 1;
         return;
       }
@@ -3158,7 +3164,7 @@ class EngineT {
   PDG_HD void fh_push_(int d, uint64_t key) {
     DecodeW& w = DW(d);
     const int32_t n = w.fh_n;
-    if (n >= s_->C.fcap) {
+    if (PDG_UNLIKELY(n >= s_->C.fcap)) {
       fail();
       return;
     }
@@ -3185,7 +3191,7 @@ class EngineT {
   PDG_HD void fh_push_(int d, uint64_t key) {
     DecodeW& w = DW(d);
     const int32_t n = w.fh_n;
-    if (n >= s_->C.fcap) {
+    if (PDG_UNLIKELY(n >= s_->C.fcap)) {
       fail();
       return;
     }
