@@ -19,8 +19,9 @@ C-ABI call (H2D + kernels + D2H every step). `cpu_baseline` is the unmodified
 reference (oracle/_ref) on all host threads over a fixed-seed stratified
 random sample of the pairs (one random replica per candidate), extrapolated
 to the whole search; the same sampled pairs are the line's parity check.
-`secondary` repeats the measurement on C2 (configs[1]) and on a C5 slice
-(configs[4]: llama3-8b, 169 plans x 128 toolbench traces = 21 632 pairs).
+`secondary` repeats the measurement on C2 (configs[1]), on a C5 slice
+(configs[4]: llama3-8b, 169 plans x 128 toolbench traces = 21 632 pairs) and
+on C1 (configs[0]: one replay, the reference's own CPU-runnable case).
 """
 import argparse
 import json
@@ -44,11 +45,11 @@ SAMPLE_SEED = 20260217
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--secondary", default="C2,C5",
+    ap.add_argument("--secondary", default="C2,C5,C1",
                     help="comma-separated configs measured in the same line ('none' to skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-argmax-mode", action="store_true")
@@ -350,7 +351,8 @@ def run_ours(args, rank, world, local):
     # e2e: host buffers through the public C-ABI call every step — stage
     # (pack + H2D) + replay + reduction + D2H.
     e2e_ms, h2d, d2h = [], 0, 0
-    for _ in range(2):
+    reps = 1 if total_ms / args.steps > 5000 else 2  # bounded bench time on the long searches
+    for _ in range(reps):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -377,7 +379,7 @@ def run_ours(args, rank, world, local):
     if world == 1 and not args.no_argmax_mode and C > 1:
         ctx.set_search_mode(abi.SEARCH_ARGMAX)
         am = []
-        for _ in range(2):
+        for _ in range(reps):
             flush.zero_()
             torch.cuda.synchronize()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
