@@ -363,7 +363,13 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
     d.S = t.S;
     d.R = t.R;
     d.max_dec = t.max_dec;
-    d.reserved = 0;
+    d.rank_is_index = 1;
+    for (size_t k = 0; k < t.by_rank.size(); ++k) {
+      if (t.by_rank[k] != static_cast<int32_t>(k)) {
+        d.rank_is_index = 0;
+        break;
+      }
+    }
     d.ttft_thres = t.ttft_thres;
     d.itl_thres = t.itl_thres;
     d.ss = static_cast<const pdg::SessTr*>(put(t.stab.data(), t.stab.size() * sizeof(pdg::SessTr)));

@@ -287,7 +287,7 @@ struct DevTrace {
   int32_t S;
   int32_t R;
   int32_t max_dec;
-  int32_t reserved;
+  int32_t rank_is_index;     // by_rank[k] == k for every k (generated traces): skip the lookup
   double ttft_thres;
   double itl_thres;
   const SessTr* ss;          // [sess_table_len(S)]; entry S: round_off = R
@@ -3035,7 +3035,7 @@ class EngineT {
       const int64_t tf0 = pb();
       const uint32_t rank = static_cast<uint32_t>(w.fh_top);
       fh_pop(d);
-      const int32_t i = GLP(s_->T.by_rank)[rank];
+      const int32_t i = s_->T.rank_is_index ? static_cast<int32_t>(rank) : GLP(s_->T.by_rank)[rank];
       SessRt& s = GLP(s_->G.sess)[i];
       const RoundTr rt = round_tr(s.roff + s.round - 1);
       const int32_t dec = rt.dec;

@@ -63,7 +63,8 @@ int hostsim_run(const pdsim_trace* trace, const pdsim_plan* plan, const pdsim_pr
   dt.S = t.S;
   dt.R = t.R;
   dt.max_dec = t.max_dec;
-  dt.reserved = 0;
+  dt.rank_is_index = 1;
+  for (size_t k = 0; k < t.by_rank.size(); ++k) dt.rank_is_index &= t.by_rank[k] == static_cast<int32_t>(k) ? 1 : 0;
   dt.ttft_thres = t.ttft_thres;
   dt.itl_thres = t.itl_thres;
   dt.ss = t.stab.data();
