@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstdio>
@@ -278,9 +279,33 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   }
   ctx->packed.assign(static_cast<size_t>(in->n_traces), pdg::PackedTrace());
   bool any_sessions = false;
-  for (int r = 0; r < in->n_traces; ++r) {
-    if (!pdg::pack_trace(in->traces[r], &ctx->packed[static_cast<size_t>(r)], &err)) return set_err(ctx, err.code, err.msg);
-    any_sessions |= ctx->packed[static_cast<size_t>(r)].S > 0;
+  {
+    // Replicas are validated and packed on all host threads; the first
+    // failing trace in input order is reported.
+    const int nt = in->n_traces;
+    std::vector<pdg::HostError> errs(static_cast<size_t>(nt));
+    std::vector<char> ok(static_cast<size_t>(nt), 1);
+    auto pack = [&](int r) {
+      ok[static_cast<size_t>(r)] =
+          pdg::pack_trace(in->traces[r], &ctx->packed[static_cast<size_t>(r)], &errs[static_cast<size_t>(r)]) ? 1 : 0;
+    };
+    const int nth = std::min<int>(nt, static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
+    if (nth > 1) {
+      std::atomic<int> next{0};
+      std::vector<std::thread> pool;
+      for (int k = 0; k < nth; ++k) {
+        pool.emplace_back([&] {
+          for (int r = next++; r < nt; r = next++) pack(r);
+        });
+      }
+      for (auto& t : pool) t.join();
+    } else {
+      for (int r = 0; r < nt; ++r) pack(r);
+    }
+    for (int r = 0; r < nt; ++r) {
+      if (!ok[static_cast<size_t>(r)]) return set_err(ctx, errs[static_cast<size_t>(r)].code, errs[static_cast<size_t>(r)].msg);
+      any_sessions |= ctx->packed[static_cast<size_t>(r)].S > 0;
+    }
   }
   if (!pdg::validate_profile(*profile, &err)) return set_err(ctx, err.code, err.msg);
   for (int k = 0; k < n_set; ++k) {

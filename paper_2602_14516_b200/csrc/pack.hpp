@@ -139,6 +139,7 @@ struct PackedTrace {
   std::vector<int32_t> round_off, incr, dec, rank, by_rank;
   std::vector<int64_t> sid;
   std::vector<int64_t> first_round_incr;  // for the KV precheck
+  int64_t max_first_incr = 0;              // its maximum: the precheck of a plan is one comparison
   // the replay engine's record tables (engine.cuh SessTr / RoundTr)
   std::vector<SessTr> stab;   // [sess_table_len(S)]
   std::vector<RoundTr> rtab;  // [R]
@@ -175,35 +176,53 @@ inline bool pack_trace(const pdsim_trace& t, PackedTrace* out, HostError* err) {
   out->delay.assign(t.interaction_delay, t.interaction_delay + R);
   out->first_round_incr.resize(static_cast<size_t>(S));
   out->max_dec = 0;
+  out->max_first_incr = 0;
   out->max_incr = 0;
   out->total_decode = 0;
-  std::unordered_set<int64_t> seen;
-  seen.reserve(static_cast<size_t>(S) * 2);
+  // Duplicate ids are found after the id sort below (adjacent equal ids).
+  // The reference checks them first for each session in trace order
+  // (workload.cpp:90-134), so an error at session i (or a duplicate found
+  // by the sort) reports the first session j <= i whose id repeats, if any.
+  auto dup_error = [&](int64_t upto) -> bool {
+    std::unordered_set<int64_t> seen;
+    for (int64_t j = 0; j <= upto && j < S; ++j) {
+      if (!seen.insert(t.session_id[j]).second) {
+        err->set(PDSIM_ERR_CONFIG, "trace: session[" + std::to_string(j) + "] (id " + std::to_string(t.session_id[j]) +
+                                       "): duplicate session_id");
+        return true;
+      }
+    }
+    return false;
+  };
+  auto fail_at = [&](int64_t i, const std::string& msg) -> bool {
+    if (dup_error(i)) return false;
+    return err->set(PDSIM_ERR_CONFIG, msg);
+  };
   double prev_arrival = 0.0;
   for (int64_t i = 0; i < S; ++i) {
-    const std::string where = "session[" + std::to_string(i) + "] (id " + std::to_string(t.session_id[i]) + ")";
-    if (!seen.insert(t.session_id[i]).second) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": duplicate session_id");
-    if (t.arrival_time[i] < 0.0) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": arrival_time must be >= 0");
+    // error texts are built only on the failing path (the loop runs per round)
+    auto where = [&] { return "session[" + std::to_string(i) + "] (id " + std::to_string(t.session_id[i]) + ")"; };
+    if (t.arrival_time[i] < 0.0) return fail_at(i, "trace: " + where() + ": arrival_time must be >= 0");
     if (i > 0 && t.arrival_time[i] < prev_arrival) {
-      return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": sessions must be sorted by arrival_time");
+      return fail_at(i, "trace: " + where() + ": sessions must be sorted by arrival_time");
     }
     prev_arrival = t.arrival_time[i];
     const int64_t b = t.round_offset[i], e = t.round_offset[i + 1];
-    if (e <= b) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": rounds must be non-empty");
-    if (e > R) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": round_offset out of range");
-    if (e - b > 32000) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": too many rounds for the device layout");
+    if (e <= b) return fail_at(i, "trace: " + where() + ": rounds must be non-empty");
+    if (e > R) return fail_at(i, "trace: " + where() + ": round_offset out of range");
+    if (e - b > 32000) return fail_at(i, "trace: " + where() + ": too many rounds for the device layout");
     int64_t ctx = 0;
     for (int64_t r = b; r < e; ++r) {
-      const std::string ra = where + ".rounds[" + std::to_string(r - b) + "]";
+      auto ra = [&] { return where() + ".rounds[" + std::to_string(r - b) + "]"; };
       const int64_t inc = t.incr_input_len[r], dl = t.decode_len[r];
-      if (inc < 1) return err->set(PDSIM_ERR_CONFIG, "trace: " + ra + ": incr_input_len must be >= 1");
-      if (dl < 1) return err->set(PDSIM_ERR_CONFIG, "trace: " + ra + ": decode_len must be >= 1");
-      if (t.interaction_delay[r] < 0.0) return err->set(PDSIM_ERR_CONFIG, "trace: " + ra + ": interaction_delay must be >= 0");
+      if (inc < 1) return fail_at(i, "trace: " + ra() + ": incr_input_len must be >= 1");
+      if (dl < 1) return fail_at(i, "trace: " + ra() + ": decode_len must be >= 1");
+      if (t.interaction_delay[r] < 0.0) return fail_at(i, "trace: " + ra() + ": interaction_delay must be >= 0");
       if (r + 1 == e && t.interaction_delay[r] != 0.0) {
-        return err->set(PDSIM_ERR_CONFIG, "trace: " + ra + ": final round must have interaction_delay 0");
+        return fail_at(i, "trace: " + ra() + ": final round must have interaction_delay 0");
       }
       ctx += inc + dl;
-      if (ctx > INT32_MAX / 2) return err->set(PDSIM_ERR_CONFIG, "trace: " + where + ": context too long for the device layout");
+      if (ctx > INT32_MAX / 2) return fail_at(i, "trace: " + where() + ": context too long for the device layout");
       out->incr[static_cast<size_t>(r)] = static_cast<int32_t>(inc);
       out->dec[static_cast<size_t>(r)] = static_cast<int32_t>(dl);
       out->max_dec = std::max<int32_t>(out->max_dec, static_cast<int32_t>(dl));
@@ -212,6 +231,7 @@ inline bool pack_trace(const pdsim_trace& t, PackedTrace* out, HostError* err) {
     }
     out->round_off[static_cast<size_t>(i)] = static_cast<int32_t>(b);
     out->first_round_incr[static_cast<size_t>(i)] = t.incr_input_len[b];
+    out->max_first_incr = std::max<int64_t>(out->max_first_incr, t.incr_input_len[b]);
   }
   if (S > 0 && t.round_offset[S] != R) return err->set(PDSIM_ERR_CONFIG, "trace: round_offset end mismatch");
   out->round_off[static_cast<size_t>(S)] = static_cast<int32_t>(R);
@@ -221,6 +241,12 @@ inline bool pack_trace(const pdsim_trace& t, PackedTrace* out, HostError* err) {
   std::iota(out->by_rank.begin(), out->by_rank.end(), 0);
   std::sort(out->by_rank.begin(), out->by_rank.end(),
             [&](int32_t a, int32_t b) { return t.session_id[a] < t.session_id[b]; });
+  for (int64_t k = 1; k < S; ++k) {
+    if (t.session_id[out->by_rank[static_cast<size_t>(k)]] == t.session_id[out->by_rank[static_cast<size_t>(k - 1)]]) {
+      dup_error(S - 1);
+      return false;
+    }
+  }
   out->rank.resize(static_cast<size_t>(S));
   for (int32_t k = 0; k < static_cast<int32_t>(S); ++k) out->rank[static_cast<size_t>(out->by_rank[k])] = k;
   out->stab.assign(static_cast<size_t>(sess_table_len(S)), SessTr{0.0, static_cast<int32_t>(R), 0});
@@ -301,10 +327,9 @@ inline bool precheck(const PackedTrace& t, const DevPlan& plan, const pdsim_prof
   for (int d = 0; d < plan.D; ++d) {
     max_cap = std::max<int64_t>(max_cap, static_cast<int64_t>(prof.degrees[plan.ddeg[d]]) * prof.gpu_memory_capacity);
   }
-  for (int64_t first : t.first_round_incr) {
-    if (first * prof.kv_bytes_per_token > max_cap) return false;
-  }
-  return true;
+  // some session's first round exceeds every decode worker <=> the largest
+  // one does (kv_bytes_per_token > 0, validated)
+  return !(t.max_first_incr * prof.kv_bytes_per_token > max_cap);
 }
 
 // Index of the first session (trace order) precheck_sessions would reject,

@@ -81,3 +81,38 @@ def test_c4_slice_search_matches_reference(ctx):
     # both regimes are covered: some pair saturates, some attains everything
     fr = [att[p].slo_ok / att[p].sessions_total for p in range(wl.n_pairs) if st_ref[p] == 0]
     assert min(fr) < 0.5 and max(fr) == 1.0
+
+
+@pytest.mark.parametrize("case", ["dup-before-arrival", "arrival-before-dup", "dup-only", "bad-round-after-dup",
+                                  "same-session-dup-and-arrival"])
+def test_trace_validation_reports_the_reference_error(case):
+    """pdsim_trace_validate finds duplicate ids by sorting (no per-session
+    set) but must name the same first error as the reference's
+    Trace::validate (workload.cpp:90-134), which checks each session's id
+    before its other fields, in trace order."""
+    from oracle import refbind
+    if not refbind.available():
+        pytest.skip("reference library not built")
+    ok = lambda i, a: {"id": i, "arrival": a, "rounds": [[10, 2, 0.0]]}  # noqa: E731
+    s = [ok(k, float(k)) for k in range(8)]
+    if case == "dup-before-arrival":
+        s[3]["id"] = 1
+        s[5]["arrival"] = 0.5
+    elif case == "arrival-before-dup":
+        s[5]["id"] = 1
+        s[3]["arrival"] = 0.5
+    elif case == "dup-only":
+        s[6]["id"] = 2
+    elif case == "bad-round-after-dup":
+        s[2]["id"] = 0
+        s[4]["rounds"] = [[0, 2, 0.0]]
+    else:
+        s[4]["id"] = 0
+        s[4]["arrival"] = 0.1
+    tr = parity.manual_trace(s, (1.0, 0.05))
+    rc = native.lib().pdsim_trace_validate(C.byref(tr.view))
+    ours = native.lib().pdsim_last_error().decode()
+    rrc = refbind.lib().ref_trace_validate(C.byref(tr.view))
+    theirs = refbind.lib().ref_last_error().decode()
+    assert rc != 0 and rrc != 0
+    assert ours == theirs, (ours, theirs)
