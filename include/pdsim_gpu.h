@@ -383,7 +383,7 @@ int pdsim_gpu_set_search_mode(pdsim_gpu_ctx* ctx, int mode);
  * keeps the subroutines shared by several handlers out of line (smaller
  * instruction footprint: many warps per SM, where instruction fetch binds,
  * DESIGN.md §3.1). AUTO (default): THROUGHPUT when a launch replays more than
- * 8 pairs per SM. Record, report and diagnostics searches use LATENCY. */
+ * 4 pairs per SM. Record, report and diagnostics searches use LATENCY. */
 enum { PDSIM_BUILD_AUTO = 0, PDSIM_BUILD_LATENCY = 1, PDSIM_BUILD_THROUGHPUT = 2 };
 int pdsim_gpu_set_kernel_build(pdsim_gpu_ctx* ctx, int build);
 /* Build the context's last replay launch used (LATENCY or THROUGHPUT; 0 before any). */

@@ -560,11 +560,12 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     // 3: attainment-only search in argmax mode (Prune, engine.cuh).
     const int variant = with_rec ? 2 : ctx->profiling ? 1 : prune ? 3 : 0;
     pdg::ReplayKernel kern = pdg::replay_kernel_for(ctx->layout, variant);
-    // Many warps per SM (more than 8 pairs per SM in this launch): the
+    // Many warps per SM (more than 4 pairs per SM in this launch; measured crossover,
+    // tools/build_threshold.py, profiles/round2/build_threshold_v20.jsonl): the
     // throughput build. Few pairs: the inlined build (lowest latency per event).
     const bool search_only = variant == 0 || variant == 3;
     const bool tp = search_only && (ctx->kernel_build == PDSIM_BUILD_THROUGHPUT ||
-                                    (ctx->kernel_build == PDSIM_BUILD_AUTO && n > 8 * static_cast<int64_t>(ctx->sm_count)));
+                                    (ctx->kernel_build == PDSIM_BUILD_AUTO && n > 4 * static_cast<int64_t>(ctx->sm_count)));
     if (tp) kern = reinterpret_cast<pdg::ReplayKernel>(pdg_tp::replay_kernel_for(ctx->layout, variant));
     ctx->last_build = tp ? PDSIM_BUILD_THROUGHPUT : PDSIM_BUILD_LATENCY;
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));
