@@ -105,6 +105,9 @@ struct pdsim_gpu_ctx {
   int64_t total_sessions = 0;        // sum of S over the staged traces
   int64_t global_sessions = 0;       // > 0: sum of S over every replica of a sharded search (argmax bounds)
   DevBuf d_pair_list;                // launch pair list (sharded / cost-ordered searches)
+  DevBuf d_sm_items, d_sm_off, d_sm_next;  // candidate-affine per-SM queues (throughput build)
+  std::vector<int64_t> h_sm_items;         // their host staging (asynchronous copies)
+  std::vector<int32_t> h_sm_off;
   ncclComm_t comm = nullptr;         // set: every search all-reduces its candidate counts over it
   int32_t comm_world = 1, comm_rank = 0;
   int search_mode = 0;               // PDSIM_SEARCH_*
@@ -526,6 +529,50 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     CU(ctx, cudaMemcpyAsync(ctx->d_pair_list.p, list, 8 * static_cast<size_t>(n), cudaMemcpyHostToDevice, ctx->stream));
     a.pair_list = ctx->d_pair_list.as<int64_t>();
   }
+  // Build choice (needed by the queue policy below): many warps per SM (more
+  // than 4 pairs per SM in this launch; measured crossover,
+  // tools/build_threshold.py, profiles/round2/build_threshold_v20.jsonl) run
+  // the throughput build; few pairs the inlined build (lowest latency per event).
+  const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
+  // variant 0: attainment-only search, 1: diagnostics (clock64 phases; N <= 8
+  // layout only), 2: record / report outputs (drop-in run(), ITL samples, pair
+  // reports), 3: attainment-only search in argmax mode (Prune, engine.cuh).
+  const int variant = with_rec ? 2 : ctx->profiling ? 1 : prune ? 3 : 0;
+  const bool search_only = variant == 0 || variant == 3;
+  const bool tp = search_only && (ctx->kernel_build == PDSIM_BUILD_THROUGHPUT ||
+                                  (ctx->kernel_build == PDSIM_BUILD_AUTO && n > 4 * static_cast<int64_t>(ctx->sm_count)));
+  // Candidate-affine queues (throughput build): one list per SM holding a
+  // contiguous run of the launch items grouped by candidate (launch order kept
+  // within a candidate), taken first by the warps of that SM, then stolen in
+  // ring order. Co-resident warps then replay the same plan, whose handler mix
+  // shares the instruction cache: the throughput regime is bound by
+  // instruction fetch; measured C3s -8.7 %, C5 slice -4 %
+  // (profiles/round2/ab_sm_affinity_v22.log). PDSIM_SM_AFFINITY=0 turns it off.
+  const char* aff_env = getenv("PDSIM_SM_AFFINITY");
+  const bool affine = n > 0 && (aff_env ? atoi(aff_env) > 0 : tp);
+  if (affine) {
+    const int L = ctx->sm_count;
+    auto& items = ctx->h_sm_items;
+    auto& off = ctx->h_sm_off;
+    std::vector<int64_t> start(static_cast<size_t>(C) + 1, 0);  // counting sort by candidate
+    for (int64_t i = 0; i < n; ++i) ++start[static_cast<size_t>((list ? list[i] : b + i) / ctx->n_traces) + 1];
+    for (int64_t c = 0; c < C; ++c) start[static_cast<size_t>(c) + 1] += start[static_cast<size_t>(c)];
+    items.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) items[static_cast<size_t>(start[static_cast<size_t>((list ? list[i] : b + i) / ctx->n_traces)]++)] = i;
+    off.resize(static_cast<size_t>(L) + 1);
+    for (int s = 0; s <= L; ++s) off[static_cast<size_t>(s)] = static_cast<int32_t>(n * s / L);
+    CU(ctx, ctx->d_sm_items.reserve(8 * static_cast<size_t>(n)));
+    CU(ctx, ctx->d_sm_off.reserve(4 * off.size()));
+    CU(ctx, ctx->d_sm_next.reserve(4 * static_cast<size_t>(L)));
+    // (host vectors live in the context: the copies are asynchronous)
+    CU(ctx, cudaMemcpyAsync(ctx->d_sm_items.p, items.data(), 8 * items.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ctx->d_sm_off.p, off.data(), 4 * off.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx, cudaMemsetAsync(ctx->d_sm_next.p, 0, 4 * static_cast<size_t>(L), ctx->stream));
+    a.sm_items = ctx->d_sm_items.as<int64_t>();
+    a.sm_off = ctx->d_sm_off.as<int32_t>();
+    a.sm_next = ctx->d_sm_next.as<unsigned>();
+    a.n_lists = L;
+  }
   if (prune) {
     // bounds are indexed by global pair (every replica of a candidate)
     const size_t nb = 4 * static_cast<size_t>(total);
@@ -551,21 +598,9 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   CU(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
   if (n > 0) {
     // The diagnostics build (per-phase clock64 counters) is a separate
-    // instantiation so the product kernel carries no instrumentation.
-    // variant 0: attainment-only search, 1: diagnostics (clock64 phases;
-    // N <= 8 layout only), 2: record / report outputs (drop-in run(), ITL
-    // samples, pair reports). Each layout's kernels live in their own
-    // translation unit (replay_l*.cu).
-    const bool with_rec = a.reports || rec.decisions || rec.ttft || rec.sessions || rec.steps;
-    // 3: attainment-only search in argmax mode (Prune, engine.cuh).
-    const int variant = with_rec ? 2 : ctx->profiling ? 1 : prune ? 3 : 0;
+    // instantiation so the product kernel carries no instrumentation. Each
+    // layout's kernels live in their own translation unit (replay_l*.cu).
     pdg::ReplayKernel kern = pdg::replay_kernel_for(ctx->layout, variant);
-    // Many warps per SM (more than 4 pairs per SM in this launch; measured crossover,
-    // tools/build_threshold.py, profiles/round2/build_threshold_v20.jsonl): the
-    // throughput build. Few pairs: the inlined build (lowest latency per event).
-    const bool search_only = variant == 0 || variant == 3;
-    const bool tp = search_only && (ctx->kernel_build == PDSIM_BUILD_THROUGHPUT ||
-                                    (ctx->kernel_build == PDSIM_BUILD_AUTO && n > 4 * static_cast<int64_t>(ctx->sm_count)));
     if (tp) kern = reinterpret_cast<pdg::ReplayKernel>(pdg_tp::replay_kernel_for(ctx->layout, variant));
     ctx->last_build = tp ? PDSIM_BUILD_THROUGHPUT : PDSIM_BUILD_LATENCY;
     CU(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_bytes)));

@@ -41,7 +41,32 @@ struct KernelArgs {
   const int8_t* cand_invalid;          // prune: [n_candidates] any pair of c invalid (whole search)
   int64_t total_sessions;              // prune: sum of S over ALL replicas of the search (every shard)
   const int64_t* pair_list;            // optional: the launch replays pair_list[0 .. pair_end - pair_begin)
+  // optional SM-affine queues: list s = sm_items[sm_off[s] .. sm_off[s+1]) of
+  // launch items, taken first by warps on SM (smid % n_lists), then stolen
+  const int64_t* sm_items;
+  const int32_t* sm_off;               // [n_lists + 1]
+  unsigned int* sm_next;               // [n_lists], zeroed per launch
+  int32_t n_lists;
+  int32_t reserved4;
 };
+
+// Next launch item of a warp on an SM-affine queue set: its home list first,
+// then the other lists in ring order; -1 when every list is exhausted. The
+// warp stays converged (lane 0 takes the tickets, broadcast by shuffle).
+__device__ __forceinline__ int64_t take_sm_affine(const int64_t* items, const int32_t* off, unsigned* next, int L,
+                                                  unsigned smid) {
+  int s = static_cast<int>(smid % static_cast<unsigned>(L));
+  for (int k = 0; k < L; ++k) {
+    const int32_t lo = off[s];
+    const unsigned cnt = static_cast<unsigned>(off[s + 1] - lo);
+    unsigned t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(&next[s], 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t < cnt) return items[lo + t];
+    s = s + 1 == L ? 0 : s + 1;
+  }
+  return -1;
+}
 
 // Result of a pair that is not replayed (pruned / invalid), field by field.
 __device__ __forceinline__ void write_empty_result(PairResult* out, int32_t status, int64_t sessions) {
@@ -85,15 +110,23 @@ __global__ void __launch_bounds__(32, PDG_MIN_BLOCKS) replay_kernel(KernelArgs a
     }
   }
   const int lane = threadIdx.x & 31;
+  unsigned smid = 0;
+  if (a.sm_items) asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
   for (;;) {
-    unsigned long long ticket = 0;
-    if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
-    ticket = __shfl_sync(0xffffffffu, ticket, 0);
     // Item `idx` of the launch: pair_begin + idx, or pair_list[idx] (a shard
     // of the search in cost order, pdsim_shard_pairs). Per-pair outputs are
     // indexed by item; argmax-mode bounds by global pair (c * n_traces + r).
-    const int64_t idx = static_cast<int64_t>(ticket);
-    if (idx >= a.pair_end - a.pair_begin) break;
+    int64_t idx;
+    if (a.sm_items) {
+      idx = take_sm_affine(a.sm_items, a.sm_off, a.sm_next, a.n_lists, smid);
+      if (idx < 0) break;
+    } else {
+      unsigned long long ticket = 0;
+      if (lane == 0) ticket = atomicAdd(a.next_pair, 1ull);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+      idx = static_cast<int64_t>(ticket);
+      if (idx >= a.pair_end - a.pair_begin) break;
+    }
     const int64_t pair = a.pair_list ? a.pair_list[idx] : a.pair_begin + idx;
     const int32_t c = static_cast<int32_t>(pair / a.n_traces);
     const int32_t r = static_cast<int32_t>(pair % a.n_traces);

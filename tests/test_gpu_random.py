@@ -73,3 +73,34 @@ def test_auto_build_switches_to_throughput_for_many_pairs(ctx):
         for f in parity.ATT_FIELDS:
             assert getattr(auto.pair_attainment[p], f) == getattr(lat.pair_attainment[p], f), (p, f)
     assert (auto.best_candidate, auto.best_slo_ok) == (lat.best_candidate, lat.best_slo_ok)
+
+
+@pytest.mark.parametrize("build", [abi.BUILD_LATENCY, abi.BUILD_THROUGHPUT])
+def test_candidate_affine_queues_equal_the_plain_queue(ctx, monkeypatch, build):
+    """The per-SM candidate-affine queues (default with the throughput build)
+    replay every pair exactly once: per-pair results, event counts and the
+    argmax equal the plain atomic queue, for a whole search and for an LPT
+    shard list (outputs follow the list)."""
+    prof = native.synth_profile(native.default_synth_spec(), 5)
+    trs = [native.gen_trace(native.preset_stats("hotpotqa"), 6.0, 60, 70 + k) for k in range(6)]
+    views = [t.view for t in trs]
+    plans = native.enumerate_plans([1, 2, 4, 8], 8)
+    ctx.set_kernel_build(build)
+    try:
+        ctx.stage(views, plans, prof, abi.default_params())
+        shard = native.shard_pairs(views, plans, 2, 1)
+        got = {}
+        for aff in ("0", "1"):
+            monkeypatch.setenv("PDSIM_SM_AFFINITY", aff)
+            got[aff] = (ctx.search_staged(3), ctx.search_staged_list(3, shard))
+    finally:
+        ctx.set_kernel_build(abi.BUILD_AUTO)
+    for k in range(2):
+        a, b = got["0"][k], got["1"][k]
+        assert a.n_pairs == b.n_pairs > 0
+        for p in range(a.n_pairs):
+            assert a.pair_status[p] == b.pair_status[p], p
+            assert a.pair_events[p] == b.pair_events[p], p
+            for f in parity.ATT_FIELDS:
+                assert getattr(a.pair_attainment[p], f) == getattr(b.pair_attainment[p], f), (p, f)
+        assert (a.best_candidate, a.best_slo_ok) == (b.best_candidate, b.best_slo_ok)
