@@ -559,10 +559,35 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
     std::vector<int64_t> start(static_cast<size_t>(C) + 1, 0);  // counting sort by candidate
     for (int64_t i = 0; i < n; ++i) ++start[static_cast<size_t>((list ? list[i] : b + i) / ctx->n_traces) + 1];
     for (int64_t c = 0; c < C; ++c) start[static_cast<size_t>(c) + 1] += start[static_cast<size_t>(c)];
-    items.resize(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) items[static_cast<size_t>(start[static_cast<size_t>((list ? list[i] : b + i) / ctx->n_traces)]++)] = i;
+    std::vector<int64_t> srt(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) srt[static_cast<size_t>(start[static_cast<size_t>((list ? list[i] : b + i) / ctx->n_traces)]++)] = i;
     off.resize(static_cast<size_t>(L) + 1);
-    for (int s = 0; s <= L; ++s) off[static_cast<size_t>(s)] = static_cast<int32_t>(n * s / L);
+    // One contiguous chunk per SM. In argmax mode with more pairs than
+    // resident warps, groups of one SM's resident warps are dealt round-robin
+    // instead (list s = groups s, s+L, ...): each SM still works on one group
+    // at a time, but the search as a whole advances in launch order, so the
+    // incumbent rises as early as with the plain queue (C5 grid, argmax:
+    // contiguous 89.3 s, plain 59.8 s, round-robin 55.9 s; full mode on the
+    // C5 slice: contiguous -4.4 %, round-robin -2.5 % vs plain;
+    // profiles/round2/ab_sm_affinity_v22.log).
+    const int64_t per_sm = (slots + L - 1) / L;
+    const char* gv = getenv("PDSIM_SM_GROUP");  // A/B: 0 contiguous, 1 round-robin
+    const bool round_robin = gv ? atoi(gv) == 1 : prune;
+    if (n <= slots || !round_robin) {
+      items.swap(srt);
+      for (int s = 0; s <= L; ++s) off[static_cast<size_t>(s)] = static_cast<int32_t>(n * s / L);
+    } else {
+      const int64_t G = std::max<int64_t>(1, per_sm), ng = (n + G - 1) / G;
+      items.clear();
+      items.reserve(static_cast<size_t>(n));
+      for (int s = 0; s < L; ++s) {
+        off[static_cast<size_t>(s)] = static_cast<int32_t>(items.size());
+        for (int64_t g = s; g < ng; g += L) {
+          for (int64_t k = g * G; k < std::min(n, (g + 1) * G); ++k) items.push_back(srt[static_cast<size_t>(k)]);
+        }
+      }
+      off[static_cast<size_t>(L)] = static_cast<int32_t>(n);
+    }
     CU(ctx, ctx->d_sm_items.reserve(8 * static_cast<size_t>(n)));
     CU(ctx, ctx->d_sm_off.reserve(4 * off.size()));
     CU(ctx, ctx->d_sm_next.reserve(4 * static_cast<size_t>(L)));
