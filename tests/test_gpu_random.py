@@ -104,3 +104,37 @@ def test_candidate_affine_queues_equal_the_plain_queue(ctx, monkeypatch, build):
             for f in parity.ATT_FIELDS:
                 assert getattr(a.pair_attainment[p], f) == getattr(b.pair_attainment[p], f), (p, f)
         assert (a.best_candidate, a.best_slo_ok) == (b.best_candidate, b.best_slo_ok)
+
+
+@pytest.mark.parametrize("mode", [abi.SEARCH_FULL, abi.SEARCH_ARGMAX])
+def test_affine_round_robin_groups_equal_the_plain_queue(ctx, monkeypatch, mode):
+    """More pairs than resident warps (2 slots per SM): contiguous lists and
+    round-robin groups replay every pair once; full-mode per-pair results and
+    the argmax (both modes) equal the plain atomic queue."""
+    prof = native.synth_profile(native.default_synth_spec(), 6)
+    trs = [native.gen_trace(native.preset_stats("toolbench"), 10.0, 50, 90 + k) for k in range(4)]
+    views = [t.view for t in trs]
+    plans = native.enumerate_plans([1, 2, 4, 8], 8)  # 676 pairs > 2 x 148 slots
+    monkeypatch.setenv("PDSIM_SLOTS_PER_SM", "2")
+    ctx.set_kernel_build(abi.BUILD_THROUGHPUT)
+    ctx.set_search_mode(mode)
+    got = {}
+    try:
+        ctx.stage(views, plans, prof, abi.default_params())
+        for name, env in (("plain", {"PDSIM_SM_AFFINITY": "0"}),
+                          ("contiguous", {"PDSIM_SM_AFFINITY": "1", "PDSIM_SM_GROUP": "0"}),
+                          ("round_robin", {"PDSIM_SM_AFFINITY": "1", "PDSIM_SM_GROUP": "1"})):
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            got[name] = ctx.search_staged(4)
+    finally:
+        ctx.set_search_mode(abi.SEARCH_FULL)
+        ctx.set_kernel_build(abi.BUILD_AUTO)
+    a = got["plain"]
+    for name in ("contiguous", "round_robin"):
+        b = got[name]
+        assert (a.best_candidate, a.best_slo_ok) == (b.best_candidate, b.best_slo_ok), name
+        if mode == abi.SEARCH_FULL:
+            for p in range(a.n_pairs):
+                assert a.pair_status[p] == b.pair_status[p], (name, p)
+                assert a.pair_events[p] == b.pair_events[p], (name, p)
