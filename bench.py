@@ -470,7 +470,8 @@ def run_ours(args, rank, world, local):
             "config": specs.config_dict(spec),
             "parallelism": (f"the same search sharded over {world} GPUs (cost-aware LPT split, pdsim_shard_pairs); "
                             "per-candidate counts all-reduced in-library over NCCL" if world > 1 else
-                            "1 GPU, pairs in cost order (persistent kernel, atomic queue)"),
+                            "1 GPU, pairs in cost order (persistent kernel; above 8 pairs per SM, "
+                            "per-SM queues grouping each candidate's pairs)"),
             "replays_per_s": wl.n_pairs * args.steps / (total_ms / 1e3),
             "planner_wall_ms": total_ms / args.steps,
             "kernel_ms": avg_k,

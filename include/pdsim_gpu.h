@@ -406,7 +406,9 @@ int64_t pdsim_shard_pairs(int32_t n_traces, const int64_t* trace_rounds,
                           int64_t capacity);
 
 /* Replays the staged pairs listed in `pairs` (global indices, no duplicates)
- * in list order: the persistent kernel's queue hands them out in that order.
+ * in list order: the persistent kernel's queue hands them out in that order
+ * (with more than 8 pairs per SM, per-SM queues keep the pairs of one
+ * candidate together on an SM, list order kept within a candidate).
  * Per-pair outputs follow the list; per-candidate outputs cover the pairs
  * replayed (or, with a communicator, the whole sharded search). */
 int pdsim_gpu_search_staged_list(pdsim_gpu_ctx* ctx, const int64_t* pairs,
