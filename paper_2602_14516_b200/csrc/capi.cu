@@ -357,6 +357,15 @@ int stage_impl(pdsim_gpu_ctx* ctx, const pdsim_search_input* in, const pdsim_pro
   size_t smem_budget = pairs <= 2 * ctx->sm_count ? (size_t(96) << 10)
                        : pairs <= 8 * ctx->sm_count ? (size_t(24) << 10)
                                                     : size_t(9216);  // 24 warps/SM (the throughput build's register budget)
+  if (pairs > 8 * ctx->sm_count && pairs < 22 * static_cast<int64_t>(ctx->sm_count)) {
+    // Every pair resident at once (C3: 18.3 per SM): the largest slot that
+    // still fits ceil(pairs / SMs) blocks per SM (228 KB shared memory per
+    // SM, 1 KB reserved per block): C3s 10-11 KB vs 9 KB -2 %
+    // (profiles/round2/ab_smem_budget_v24.log).
+    const int64_t per_sm = (pairs + ctx->sm_count - 1) / ctx->sm_count;
+    const size_t fit = ((size_t(228) << 10) / static_cast<size_t>(per_sm) - 1024) & ~size_t(511);
+    smem_budget = std::max(smem_budget, std::min(fit, size_t(24) << 10));
+  }
   if (const char* v = getenv("PDSIM_SMEM_BUDGET")) smem_budget = static_cast<size_t>(atoll(v));  // tuning only
   // Compiled shared-memory layouts (replay_kernel<.., kD, kP>): N <= 8 plans
   // fit <8, 8>, N <= 16 plans <16, 16>; D + 2P <= 64 bounds the rest.
