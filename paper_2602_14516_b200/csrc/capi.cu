@@ -560,7 +560,8 @@ int search_impl(pdsim_gpu_ctx* ctx, int64_t b, int64_t e, uint64_t seed, pdsim_s
   // SM (C3s shards, profiles/round2/shard_affinity_c3s_v23.jsonl: 9 per SM
   // -7 %, 4.6 per SM +3 %, 2.3 per SM neutral). PDSIM_SM_AFFINITY=0/1 forces it.
   const char* aff_env = getenv("PDSIM_SM_AFFINITY");
-  const bool affine = n > 0 && (aff_env ? atoi(aff_env) > 0 : tp && n > 8 * static_cast<int64_t>(ctx->sm_count));
+  const bool affine = n > 0 && n < (int64_t(1) << 31) &&  // (int32 list offsets)
+                     (aff_env ? atoi(aff_env) > 0 : tp && n > 8 * static_cast<int64_t>(ctx->sm_count));
   if (affine) {
     const int L = ctx->sm_count;
     auto& items = ctx->h_sm_items;
